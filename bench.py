@@ -1,0 +1,355 @@
+#!/usr/bin/env python3
+"""CK-MPM per-substep transfer benchmark (BASELINE.json metric:
+particle-substeps/s and P2G+G2P HBM roofline) on B200.
+
+Default workload (N=1): SURVEY Appendix C `C5_block_108` — fixed-corotated
+block of 108^3 cells at 8 ppc (10,077,696 particles), res 512, APIC, sticky
+floor, gravity -9.8, FP64 (the reference's Simulation<double>).  One "step"
+is one full substep (sort, activate, clear, P2G, grid update, G2P) at the
+fixed dt = cfl_dt(t=0) (the replayed schedule of the reference's
+`ckmpm bench`, proj/tools/ckmpm_main.cpp:146-159).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N>1 runs under torchrun, one process per GPU (see DESIGN.md §6 for the
+multi-GPU status).  The particle state (2.26 GB) exceeds L2 (126 MB), so no
+explicit flush is needed between substeps.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2412_10399_b200 import abi  # noqa: E402
+from paper_2412_10399_b200.scene import block_scene, seed_particles  # noqa: E402
+
+METRIC = "particle-substeps/s"
+UNIT = "particle-substeps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cells", type=int, default=108, help="C5 block edge in cells (108 -> 10.08M p)")
+    ap.add_argument("--res", type=int, default=512)
+    ap.add_argument("--scheme", default="apic")
+    ap.add_argument("--precision", type=int, default=8, choices=[8, 4])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-cells", type=int, default=64, help="CPU baseline sample block edge (64 -> 2.1M p)")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        load = [s for s in sm if s is not None]
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def algorithmic_bytes(n, nblocks, scheme, precision):
+    """SURVEY §8(d) compulsory bytes per launch:
+    P2G reads x,v,F,(B),m,V0,mat + perm, writes every active node once
+    (2 grids x {m,p} x 64 nodes); G2P reads x,F,J,m,V0,mat (+B for PIC) + perm
+    and the nodal velocities, writes the full 27-field state + mat."""
+    s = precision
+    b_read = 9 * s if scheme != "pic" else 0
+    p2g = n * (3 * s + 3 * s + 9 * s + b_read + s + s + 4 + 4) + nblocks * 2 * 64 * 4 * s
+    g2p = n * (3 * s + 9 * s + s + s + s + 4 + 4 + (9 * s if scheme == "pic" else 0) + 27 * s + 4) \
+        + nblocks * 2 * 64 * 3 * s
+    return p2g, g2p
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(args, threads):
+    """Reference engine (oracle/_ref, compiled unmodified) on the host cores:
+    Simulation<double>::step on a bounded sample of the same workload family
+    (C5 block, same res/material/scheme/dt rule), atomic (default) mode."""
+    from oracle import bind
+    cfg = block_scene(args.cpu_cells, resolution=args.res, scheme=args.scheme)
+    p = seed_particles(cfg, args.precision)
+    ref = bind.Ref(cfg, p, precision=args.precision, threads=threads, deterministic=False)
+    dt = ref.cfl_dt(1.0)
+    rc, msg = ref.step(dt)  # warm-up (allocations, first touch)
+    if rc:
+        raise RuntimeError(msg)
+    t0 = time.perf_counter()
+    for _ in range(args.cpu_steps):
+        rc, msg = ref.step(dt)
+        if rc:
+            raise RuntimeError(msg)
+    el = time.perf_counter() - t0
+    ref.close()
+    kind = "reference"
+    return {"value": len(p) * args.cpu_steps / el, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"C5 block {args.cpu_cells}^3 cells ({len(p)} p) res {args.res} {args.scheme} "
+                      f"FP{8 * args.precision}, {args.cpu_steps} substeps after 1 warm-up, "
+                      f"ckmpm::Simulation<T>::step (atomic P2G), wall clock"}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    from oracle import bind
+    cfg = block_scene(args.cpu_cells, resolution=args.res, scheme=args.scheme)
+    p = seed_particles(cfg, args.precision)
+    ref = bind.Ref(cfg, p, precision=args.precision, threads=threads, deterministic=False)
+    dt = ref.cfl_dt(1.0)
+    for _ in range(max(args.warmup, 1)):
+        rc, msg = ref.step(dt)
+        assert rc == 0, msg
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        rc, msg = ref.step(dt)
+        assert rc == 0, msg
+    el = time.perf_counter() - t0
+    val = len(p) * args.steps / el
+    tm = ref.timers()
+    sample = (f"C5 block {args.cpu_cells}^3 cells ({len(p)} p) res {args.res} {args.scheme} FP{8 * args.precision}; "
+              f"ckmpm::Simulation<T>::step, atomic P2G, {threads} threads")
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.precision == 8 else "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"C5_block_{args.cells} family (CPU sample {args.cpu_cells}^3 cells)",
+                       "particles_sample": len(p), "resolution": args.res, "scheme": args.scheme,
+                       "material": "fixed_corotated", "parallelism": f"cpu threads={threads}"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "phase_s": dict(zip(abi.PHASE_NAMES, tm))}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch
+        import torch.distributed as dist_mod
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl")
+        dist = dist_mod
+    import torch
+
+    from paper_2412_10399_b200._lib import lib
+    from paper_2412_10399_b200.api import Simulation
+
+    L = lib()
+    prec = args.precision
+    cfg = block_scene(args.cells, resolution=args.res, scheme=args.scheme)
+    host = seed_particles(cfg, prec)
+    n = len(host)
+    sim = Simulation(cfg, precision=prec, device=local, particles=host)
+    ctx = sim._ctx
+    dt = sim.cfl_dt(1.0)
+    out = abi.StepOut()
+
+    def step_once():
+        rc = L.ckg_step(ctx, dt, C.byref(out))
+        if rc != 0:
+            buf = C.create_string_buffer(256)
+            L.ckg_last_error_message(ctx, buf, 256)
+            raise RuntimeError(f"ckg_step failed: {buf.value.decode()}")
+
+    for _ in range(args.warmup):
+        step_once()
+    # phase shares from one steady-state step (device events on the library stream)
+    step_once()
+    phase_ms = list(out.phase_ms)
+    nblocks = int(out.active_blocks)
+    launches_per_step = int(out.kernel_launches)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    barrier()
+    sampler.start()
+    time.sleep(0.3)
+    L.ckg_timer_mark(ctx, 0)
+    p2g_ms, g2p_ms = [], []
+    total_launch = 0
+    for _ in range(args.steps):
+        step_once()
+        p2g_ms.append(out.phase_ms[3])
+        g2p_ms.append(out.phase_ms[5])
+        total_launch += int(out.kernel_launches)
+    L.ckg_timer_mark(ctx, 1)
+    el_ms = C.c_double()
+    L.ckg_timer_elapsed(ctx, 0, 1, C.byref(el_ms))
+    clocks = sampler.stop()
+    barrier()
+    t_ms = el_ms.value
+    if dist is not None:
+        tt = torch.tensor([t_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = n * ws * args.steps / (t_ms * 1e-3)
+
+    # e2e: the same substep through the C-ABI with HOST buffers: each step
+    # uploads the full Particle<T> AoS from pinned host memory, steps, and
+    # downloads the new state (the round trip a host-resident caller pays).
+    nbytes = n * abi.particle_dtype(prec).itemsize
+    pinned = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy().view(abi.particle_dtype(prec))
+    pinned[:] = sim.particles()
+    e2e_steps = max(1, args.e2e_steps)
+    barrier()
+    L.ckg_timer_mark(ctx, 2)
+    for _ in range(e2e_steps):
+        rc = L.ckg_upload(ctx, abi.ptr(pinned), n)
+        assert rc == 0
+        step_once()
+        rc = L.ckg_download(ctx, abi.ptr(pinned), n)
+        assert rc == 0
+    L.ckg_timer_mark(ctx, 3)
+    L.ckg_timer_elapsed(ctx, 2, 3, C.byref(el_ms))
+    e2e_ms = el_ms.value
+    if dist is not None:
+        tt = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_val = n * ws * e2e_steps / (e2e_ms * 1e-3)
+
+    # roofline of the dominant kernel (device events around each launch)
+    p2g_bytes, g2p_bytes = algorithmic_bytes(n, nblocks, args.scheme, prec)
+    p2g_avg = float(np.mean(p2g_ms))
+    g2p_avg = float(np.mean(g2p_ms))
+    peak, peak_kind = measured_peak_hbm()
+    if p2g_avg >= g2p_avg:
+        dom, dom_bytes, dom_ms = "p2g_kernel", p2g_bytes, p2g_avg
+    else:
+        dom, dom_bytes, dom_ms = "g2p_kernel", g2p_bytes, g2p_avg
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(dom)
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        cb = None
+        if not args.no_cpu_baseline and ws == 1:
+            try:
+                cb = cpu_baseline(args, os.cpu_count() or 1)
+            except Exception as e:  # reported, never silently substituted
+                cb = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                      "sample": f"unavailable: {e}"}
+        ms_step = t_ms / args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if prec == 8 else "f32", "data": "synthetic",
+            "config": {"workload": f"C5_block_{args.cells}", "particles_per_gpu": n, "resolution": args.res,
+                       "scheme": args.scheme, "material": "fixed_corotated", "ppc": 8,
+                       "active_blocks": nblocks, "dt": dt,
+                       "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas (weak)",
+                       "l2": "state 2.26 GB >> 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "algorithmic_bytes": dom_bytes, "avg_ms": dom_ms},
+            "p2g_g2p": {"p2g_ms": p2g_avg, "g2p_ms": g2p_avg,
+                        "p2g_gbs": p2g_bytes / (p2g_avg * 1e-3) / 1e9,
+                        "g2p_gbs": g2p_bytes / (g2p_avg * 1e-3) / 1e9,
+                        "combined_frac": (p2g_bytes + g2p_bytes) / ((p2g_avg + g2p_avg) * 1e-3) / 1e9 / peak},
+            "phase_ms": dict(zip(abi.PHASE_NAMES, phase_ms)),
+            "cpu_baseline": cb,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                    "steps": e2e_steps, "path": "ckg_upload(pinned AoS) + ckg_step + ckg_download per step"},
+            "gpu_launches": total_launch,
+            "launches_per_step": launches_per_step,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

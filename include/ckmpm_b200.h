@@ -1,0 +1,233 @@
+/*
+ * ckmpm_b200.h — C-ABI of the B200-native CK-MPM per-substep transfer path.
+ *
+ * The reference (CK-MPM, arXiv 2412.10399, shipped as the header-only C++
+ * engine under proj/include/ckmpm/) has no plugin/FFI seam: callers drive
+ * `ckmpm::Simulation<T>` directly (proj/include/ckmpm/simulation.hpp:85-219).
+ * This header is the seam a maintainer binds instead of the CPU engine's
+ * `Simulation<T>::step` (simulation.hpp:150-188).  Every entry point below
+ * names the reference interface it replaces.  Plain pointers and sizes only;
+ * no torch or C++ types cross this boundary.
+ *
+ * Status convention (reference exception taxonomy, proj/include/ckmpm/
+ * errors.hpp:9-32, exit codes of proj/tools/ckmpm_main.cpp:218-230):
+ *   0 ok, 2 ConfigError, 3 NumericalError (sub-code in ckg_step_out), 4 IoError,
+ *   5 device/runtime failure (no reference equivalent; never silently ignored).
+ */
+#ifndef CKMPM_B200_H_
+#define CKMPM_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKG_ABI_VERSION 1
+
+#define CKG_OK 0
+#define CKG_ERR_CONFIG 2
+#define CKG_ERR_NUMERICAL 3
+#define CKG_ERR_IO 4
+#define CKG_ERR_DEVICE 5
+
+/* Numerical sub-codes; each maps to one throw site of the reference. */
+#define CKG_NUM_NONE 0
+#define CKG_NUM_OUT_OF_DOMAIN 1      /* grid.hpp:122-126 OutOfDomainError "particle N violates the 2-cell domain inset on axis A" */
+#define CKG_NUM_FC_STRESS_INVERTED 2 /* transfer.hpp:192-193 InvertedElementError "fixed corotated stress: det F <= 0" */
+#define CKG_NUM_DP_STRESS_INVERTED 3 /* transfer.hpp:202-203 InvertedElementError "granular stress: det F <= 0" */
+#define CKG_NUM_FLUID_STATE_J 4      /* material.hpp:134 NumericalError "fluid state: J must be > 0" */
+#define CKG_NUM_NEAR_SINGULAR_D 5    /* transfer.hpp:226-227 NumericalError "near-singular APIC D matrix" */
+#define CKG_NUM_SINGULAR_MLS 6       /* simulation.hpp:305-306 NumericalError "singular MLS moment matrix" */
+#define CKG_NUM_RETURN_MAP_INVERTED 7/* material.hpp:159-160 InvertedElementError "plastic return map: det F <= 0" */
+#define CKG_NUM_F_INVERTED 8         /* transfer.hpp:622-623 InvertedElementError "deformation gradient inverted" */
+#define CKG_NUM_FLUID_J 9            /* transfer.hpp:616 NumericalError "fluid compression drove J <= 0" */
+#define CKG_NUM_NONFINITE 10         /* simulation.hpp:384-387 NumericalError "non-finite particle state after step N" */
+#define CKG_NUM_INACTIVE_BLOCK 11    /* grid.hpp:166-169 NumericalError "access to inactive grid block ..." (defensive) */
+
+#define CKG_MAX_MATERIALS 16
+#define CKG_MAX_BOUNDARIES 32
+
+/* MaterialModel (material.hpp:12) — same ordinal values. */
+#define CKG_MODEL_FIXED_COROTATED 0
+#define CKG_MODEL_J_FLUID 1
+#define CKG_MODEL_DRUCKER_PRAGER 2
+
+/* TransferScheme (transfer.hpp:16) — same ordinal values. */
+#define CKG_SCHEME_PIC 0
+#define CKG_SCHEME_APIC 1
+#define CKG_SCHEME_MLS 2
+
+/* BcKind (grid.hpp:20) — same ordinal values. */
+#define CKG_BC_STICKY 0
+#define CKG_BC_SLIP 1
+#define CKG_BC_SEPARATE 2
+
+/* Phases of Simulation::step (simulation.hpp:150-187), also the stop points
+ * of ckg_step_phases. */
+#define CKG_PHASE_SORT 1
+#define CKG_PHASE_ACTIVATE 2
+#define CKG_PHASE_CLEAR 3
+#define CKG_PHASE_P2G 4
+#define CKG_PHASE_GRID 5
+#define CKG_PHASE_G2P 6
+
+/* Material<T> after finalize_material (material.hpp:34-50, :61-88).  The host
+ * runs the reference's finalize; derived fields (mu, lambda, dp_alpha) are
+ * passed in, never recomputed on the device. */
+typedef struct ckg_material {
+  int32_t model;
+  int32_t _pad;
+  double density, E, nu, mu, lambda;
+  double bulk, gamma, viscosity;
+  double friction_angle_deg, dp_alpha;
+} ckg_material;
+
+/* BoundaryCondition<T> (grid.hpp:26-56). */
+typedef struct ckg_boundary {
+  int32_t kind;
+  int32_t _pad;
+  double lo[3], hi[3], normal[3], velocity[3], omega[3], center[3];
+} ckg_boundary;
+
+/* Flattened SimConfig<T> (scene.hpp:159-182), the fields the step consumes.
+ * precision: 8 = Simulation<double>, 4 = Simulation<float>.  All reals are
+ * carried as double; in float mode they must be the exact widening of the
+ * host's float values (dx and inv_dx included: dx = extent/T(res) and
+ * inv_dx = T(1)/dx as the reference computes them in T, simulation.hpp:250,
+ * grid.hpp:117, scene.hpp:181). */
+typedef struct ckg_config {
+  int32_t abi_version;   /* CKG_ABI_VERSION */
+  int32_t precision;     /* 8 or 4 */
+  int32_t resolution;    /* cubic cell resolution */
+  int32_t scheme;        /* CKG_SCHEME_* */
+  double extent, dx, inv_dx;
+  double gravity[3];
+  double mass_eps;       /* Simulation::compute_mass_epsilon (simulation.hpp:227-232) */
+  int32_t clamp_singular;
+  int32_t deterministic; /* fixed-order reduction mode */
+  double clamp_floor;
+  int32_t n_materials;
+  int32_t n_boundaries;
+  ckg_material materials[CKG_MAX_MATERIALS];
+  ckg_boundary boundaries[CKG_MAX_BOUNDARIES];
+  int32_t device;        /* CUDA ordinal */
+  int32_t flags;         /* reserved, 0 */
+} ckg_config;
+
+/* Particle<T> (transfer.hpp:19-28), byte-identical layout: 224 B (double),
+ * 112 B (float).  Upload/download take arrays of these. */
+typedef struct ckg_particle_f64 {
+  double x[3], v[3], F[9], B[9];
+  double J, mass, volume0;
+  uint32_t material;
+  uint32_t _pad;
+} ckg_particle_f64;
+
+typedef struct ckg_particle_f32 {
+  float x[3], v[3], F[9], B[9];
+  float J, mass, volume0;
+  uint32_t material;
+} ckg_particle_f32;
+
+/* What Simulation::step/gather_all leave behind for cfl_dt and the caller
+ * (simulation.hpp:380-395), plus TransferCounters (transfer.hpp:32-45) and
+ * PhaseTimers (simulation.hpp:34-42) deltas for this step. */
+typedef struct ckg_step_out {
+  double vmax;                        /* sqrt(max |v|^2) over particles */
+  double min_j[CKG_MAX_MATERIALS];    /* per-material min J over fluid particles, 1 if none */
+  uint64_t p2g_node_visits, g2p_node_visits, p2g_transfers, g2p_transfers;
+  double phase_ms[6];                 /* sort, activate, clear, p2g, grid, g2p (device time) */
+  int32_t status;                     /* CKG_OK / CKG_ERR_* */
+  int32_t error_code;                 /* CKG_NUM_* */
+  int32_t error_axis;                 /* OutOfDomain axis */
+  int32_t error_phase;                /* CKG_PHASE_* where the error was raised */
+  uint64_t error_particle;            /* sorted particle index (OutOfDomainError::particle_index) */
+  uint64_t active_blocks;             /* BlockSparseGrid::active_block_count after activate */
+  uint64_t kernel_launches;           /* device kernels this call enqueued */
+} ckg_step_out;
+
+/* DiagnosticsRow<T> (simulation.hpp:44-53), computed on the device
+ * (compute_diagnostics, simulation.hpp:55-69). */
+typedef struct ckg_diagnostics {
+  double momentum[3], angular[3], momentum_massfree[3];
+  double kinetic_energy, vmax;
+} ckg_diagnostics;
+
+typedef struct ckg_ctx ckg_ctx;
+
+/* ABI/build identification. */
+int32_t ckg_abi_version(void);
+const char* ckg_build_info(void);
+const char* ckg_status_string(int32_t status);
+
+/* Replaces Simulation<T>::Simulation(SimConfig) minus seeding
+ * (simulation.hpp:88-101): validates, allocates device state on cfg->device.
+ * The caller seeds with the reference's seed_particles (scene.hpp:204) and
+ * passes the particles to ckg_upload. */
+int32_t ckg_create(const ckg_config* cfg, ckg_ctx** out);
+void ckg_destroy(ckg_ctx* ctx);
+
+/* Replaces Simulation<T>::restore(particles, ...) / the seeded particles_
+ * (simulation.hpp:120-129): host AoS -> device SoA.  Layout per precision. */
+int32_t ckg_upload(ckg_ctx* ctx, const void* particles, uint64_t n);
+/* Replaces Simulation<T>::particles() (simulation.hpp:106-107): device SoA ->
+ * host AoS, in the device's current (sorted) order. */
+int32_t ckg_download(ckg_ctx* ctx, void* particles, uint64_t n);
+uint64_t ckg_particle_count(const ckg_ctx* ctx);
+
+/* Replaces Simulation<T>::mass_eps_ (simulation.hpp:227-232; restore() sets it). */
+int32_t ckg_set_mass_epsilon(ckg_ctx* ctx, double mass_eps);
+
+/* Replaces Simulation<T>::step(dt) (simulation.hpp:150-188): one substep,
+ * synchronous; on return `out` holds vmax/minJ/error for cfl_dt. */
+int32_t ckg_step(ckg_ctx* ctx, double dt, ckg_step_out* out);
+/* Enqueue `count` substeps of fixed dt without a host round trip in between
+ * (errors are latched on the device and reported by ckg_sync).  `out` may be
+ * NULL; when given it receives the state after the last substep. */
+int32_t ckg_step_many(ckg_ctx* ctx, double dt, int32_t count, ckg_step_out* out);
+/* Runs step(dt) only up to and including `stop_after` (CKG_PHASE_*); particle
+ * state is not advanced unless stop_after == CKG_PHASE_G2P.  Test/parity hook
+ * (the reference exposes the same cut points through full_step's pieces,
+ * transfer.hpp:634-669). */
+int32_t ckg_step_phases(ckg_ctx* ctx, double dt, int32_t stop_after, ckg_step_out* out);
+
+/* Binning parity hooks (simulation.hpp:248-274, kernel.hpp:114-120).  Both
+ * work on the current device state without changing it.
+ * ckg_debug_sort: keys[i] = block key of sorted position i, order[i] = index
+ * (in current order) of the particle placed at sorted position i.
+ * ckg_debug_bases: bases[(p*2+g)*3+a] = axis_pair(x_p[a], k_g, dx).base for
+ * the particle at current position p (g = 0: k = -1, g = 1: k = +1). */
+int32_t ckg_debug_sort(ckg_ctx* ctx, uint32_t* keys, uint32_t* order, uint64_t n);
+int32_t ckg_debug_bases(ckg_ctx* ctx, int32_t* bases, uint64_t n);
+
+/* Grid facade (BlockSparseGrid<T>, grid.hpp:75-281) over the device grid as
+ * left by the last step / ckg_step_phases. */
+uint64_t ckg_grid_active_block_count(ckg_ctx* ctx);     /* active_block_count (grid.hpp:153) */
+/* coords: 3*nb int32 block coordinates; nodes: nb * 128 * 4 doubles in the
+ * reference's Block::nodes order ((g<<6)|(i&3)<<4|(j&3)<<2|(k&3), each
+ * {mass, p.x, p.y, p.z}; grid.hpp:81-84, :172-175).  Blocks are listed in
+ * ascending directory order (the reference lists them in first-touch order;
+ * compare as sets keyed by coordinate).  nodes may be NULL. */
+int32_t ckg_grid_download(ckg_ctx* ctx, int32_t* coords, double* nodes, uint64_t nb);
+/* total_mass / total_momentum per grid slot (grid.hpp:199-213). */
+int32_t ckg_grid_totals(ckg_ctx* ctx, double mass[2], double momentum[6]);
+
+/* compute_diagnostics on the device (simulation.hpp:55-69). */
+int32_t ckg_diagnostics_compute(ckg_ctx* ctx, ckg_diagnostics* out);
+
+/* Device-side timing on the context's stream (the stream every kernel of
+ * this context is launched on): record marker `slot` (0..15); elapsed ms
+ * between two recorded markers (synchronises on `b`). */
+int32_t ckg_timer_mark(ckg_ctx* ctx, int32_t slot);
+int32_t ckg_timer_elapsed(ckg_ctx* ctx, int32_t a, int32_t b, double* ms);
+
+/* Formats the last error exactly as the reference's exception message. */
+int32_t ckg_last_error_message(ckg_ctx* ctx, char* buf, uint64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CKMPM_B200_H_ */

@@ -1,0 +1,774 @@
+// ckg_api.cu — device context and the C-ABI (include/ckmpm_b200.h) of the
+// B200-native CK-MPM transfer path.  Host orchestration of one substep in the
+// reference's phase order (proj/include/ckmpm/simulation.hpp:150-188), one
+// CUDA stream per context, no host round trip inside a substep.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/ckmpm_b200.h"
+#include "ckg_kernels.cuh"
+#include "ckg_scan.cuh"
+
+namespace ckg {
+
+struct CudaError {
+  cudaError_t e;
+  const char* what;
+};
+
+namespace {
+
+#define CKG_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) throw CudaError{_e, #call};   \
+  } while (0)
+
+struct ConfigFail {
+  std::string msg;
+};
+
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+template <typename T>
+T* dalloc(uint64_t count) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  CKG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+int grid_for(uint64_t work, int threads, int max_blocks = 148 * 16) {
+  uint64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > uint64_t(max_blocks)) b = max_blocks;
+  return int(b);
+}
+
+const char* num_message(int code) {
+  switch (code) {
+    case CKG_NUM_FC_STRESS_INVERTED: return "fixed corotated stress: det F <= 0";
+    case CKG_NUM_DP_STRESS_INVERTED: return "granular stress: det F <= 0";
+    case CKG_NUM_FLUID_STATE_J: return "fluid state: J must be > 0";
+    case CKG_NUM_NEAR_SINGULAR_D: return "near-singular APIC D matrix";
+    case CKG_NUM_SINGULAR_MLS: return "singular MLS moment matrix";
+    case CKG_NUM_RETURN_MAP_INVERTED: return "plastic return map: det F <= 0";
+    case CKG_NUM_F_INVERTED: return "deformation gradient inverted";
+    case CKG_NUM_FLUID_J: return "fluid compression drove J <= 0";
+    case CKG_NUM_INACTIVE_BLOCK: return "access to inactive grid block";
+    default: return "numerical error";
+  }
+}
+
+}  // namespace
+
+// Precision-independent interface of a context.
+struct CtxBase {
+  ckg_config cfg{};
+  std::string last_error;
+  uint64_t step_count = 0;  // substeps completed (for the non-finite message)
+  virtual ~CtxBase() = default;
+  virtual int upload(const void* p, uint64_t n) = 0;
+  virtual int download(void* p, uint64_t n) = 0;
+  virtual uint64_t count() const = 0;
+  virtual int step(double dt, int stop_after, int count, ckg_step_out* out) = 0;
+  virtual int debug_sort(uint32_t* keys, uint32_t* order, uint64_t n) = 0;
+  virtual int debug_bases(int32_t* bases, uint64_t n) = 0;
+  virtual uint64_t active_blocks() = 0;
+  virtual int grid_download(int32_t* coords, double* nodes, uint64_t nb) = 0;
+  virtual int grid_totals(double* mass, double* mom) = 0;
+  virtual int diagnostics(ckg_diagnostics* out) = 0;
+  virtual int timer_mark(int slot) = 0;
+  virtual int timer_elapsed(int a, int b, double* ms) = 0;
+};
+
+template <typename T>
+struct Context final : CtxBase {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[7] = {};
+  cudaEvent_t tev[16] = {};
+  uint64_t launches = 0;  // kernels enqueued by the current API call
+  uint64_t n = 0;
+  int D = 0;
+  uint64_t nd = 0;  // D^3
+  int key_bits = 1;
+  // particles (double-buffered SoA)
+  T* fbuf[2] = {nullptr, nullptr};
+  uint32_t* mbuf[2] = {nullptr, nullptr};
+  int cur = 0;
+  // staging for AoS transfers
+  T* staging = nullptr;
+  uint64_t staging_words = 0;
+  // sort
+  uint32_t* keys = nullptr;
+  uint32_t* vals = nullptr;
+  RadixScratch rs;
+  uint32_t* perm = nullptr;  // points into vals or rs.vals_alt after a sort
+  uint32_t* skeys = nullptr;
+  // grid
+  uint32_t* flags = nullptr;
+  int32_t* dir = nullptr;
+  uint32_t* active = nullptr;
+  uint32_t* scan_partials = nullptr;
+  T* pool = nullptr;
+  uint32_t pool_cap = 0;
+  // status
+  DevStatus* dstat = nullptr;
+  DevStatus* hstat = nullptr;  // pinned
+  BcParam<T>* dbcs = nullptr;
+  double* dacc = nullptr;  // diagnostics accumulators (11)
+  uint64_t last_active = 0;
+  bool grid_valid = false;
+
+  explicit Context(const ckg_config& c) {
+    cfg = c;
+    device = c.device;
+    CKG_CUDA(cudaSetDevice(device));
+    CKG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : ev) CKG_CUDA(cudaEventCreate(&e));
+    for (auto& e : tev) CKG_CUDA(cudaEventCreate(&e));
+    D = c.resolution / 4 + 2;
+    nd = uint64_t(D) * D * D;
+    key_bits = 1;
+    while ((uint64_t(1) << key_bits) < nd) ++key_bits;
+    flags = dalloc<uint32_t>(nd);
+    CKG_CUDA(cudaMemset(flags, 0, nd * sizeof(uint32_t)));
+    dir = dalloc<int32_t>(nd);
+    CKG_CUDA(cudaMemset(dir, 0xff, nd * sizeof(int32_t)));
+    scan_partials = dalloc<uint32_t>(scan_tiles(std::max<uint64_t>(nd, 1)) + 1);
+    // Block pool: the dense bound (every directory slot active) when it fits
+    // in 16 GiB, so no substep can overflow; otherwise grown on demand.
+    uint64_t dense_bytes = nd * kBlockVals * sizeof(T);
+    uint64_t cap = dense_bytes <= (16ull << 30) ? nd : std::min<uint64_t>(nd, 1u << 16);
+    set_pool_cap(uint32_t(cap));
+    dstat = dalloc<DevStatus>(1);
+    CKG_CUDA(cudaMallocHost(&hstat, sizeof(DevStatus)));
+    std::memset(hstat, 0, sizeof(DevStatus));
+    dbcs = dalloc<BcParam<T>>(kMaxBoundaries);
+    std::vector<BcParam<T>> hb(kMaxBoundaries);
+    for (int b = 0; b < c.n_boundaries; ++b) {
+      const ckg_boundary& s = c.boundaries[b];
+      BcParam<T>& d = hb[b];
+      d.kind = s.kind;
+      for (int a = 0; a < 3; ++a) {
+        d.lo[a] = T(s.lo[a]);
+        d.hi[a] = T(s.hi[a]);
+        d.normal[a] = T(s.normal[a]);
+        d.velocity[a] = T(s.velocity[a]);
+        d.omega[a] = T(s.omega[a]);
+        d.center[a] = T(s.center[a]);
+      }
+    }
+    CKG_CUDA(cudaMemcpy(dbcs, hb.data(), sizeof(BcParam<T>) * kMaxBoundaries, cudaMemcpyHostToDevice));
+    dacc = dalloc<double>(12);
+  }
+
+  ~Context() override {
+    cudaSetDevice(device);
+    if (st) cudaStreamSynchronize(st);
+    for (int b = 0; b < 2; ++b) {
+      dfree(fbuf[b]);
+      dfree(mbuf[b]);
+    }
+    dfree(staging);
+    dfree(keys);
+    dfree(vals);
+    dfree(rs.keys_alt);
+    dfree(rs.vals_alt);
+    dfree(rs.hist);
+    dfree(rs.partials);
+    dfree(flags);
+    dfree(dir);
+    dfree(active);
+    dfree(scan_partials);
+    dfree(pool);
+    dfree(dstat);
+    dfree(dbcs);
+    dfree(dacc);
+    if (hstat) cudaFreeHost(hstat);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : tev)
+      if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  void set_pool_cap(uint32_t cap) {
+    dfree(pool);
+    dfree(active);
+    pool_cap = cap;
+    pool = dalloc<T>(uint64_t(cap) * kBlockVals);
+    active = dalloc<uint32_t>(cap);
+  }
+
+  PState<T> state(int b) const { return PState<T>{fbuf[b], mbuf[b], n}; }
+
+  void ensure_particles(uint64_t count) {
+    if (count == n && fbuf[0]) return;
+    for (int b = 0; b < 2; ++b) {
+      dfree(fbuf[b]);
+      dfree(mbuf[b]);
+    }
+    dfree(keys);
+    dfree(vals);
+    dfree(rs.keys_alt);
+    dfree(rs.vals_alt);
+    dfree(rs.hist);
+    dfree(rs.partials);
+    n = count;
+    for (int b = 0; b < 2; ++b) {
+      fbuf[b] = dalloc<T>(uint64_t(kNumFields) * std::max<uint64_t>(n, 1));
+      mbuf[b] = dalloc<uint32_t>(std::max<uint64_t>(n, 1));
+    }
+    keys = dalloc<uint32_t>(n);
+    vals = dalloc<uint32_t>(n);
+    rs.keys_alt = dalloc<uint32_t>(n);
+    rs.vals_alt = dalloc<uint32_t>(n);
+    uint64_t nh = uint64_t(kRadix) * sort_tiles(std::max<uint64_t>(n, 1));
+    rs.hist = dalloc<uint32_t>(nh);
+    rs.partials = dalloc<uint32_t>(scan_tiles(nh) + 1);
+    cur = 0;
+  }
+
+  void ensure_staging(uint64_t words) {
+    if (staging_words >= words) return;
+    dfree(staging);
+    staging = dalloc<T>(words);
+    staging_words = words;
+  }
+
+  int upload(const void* p, uint64_t count) override {
+    CKG_CUDA(cudaSetDevice(device));
+    ensure_particles(count);
+    if (count == 0) return CKG_OK;
+    const uint64_t words = count * (kNumFields + 1);
+    ensure_staging(words);
+    CKG_CUDA(cudaMemcpyAsync(staging, p, words * sizeof(T), cudaMemcpyHostToDevice, st));
+    aos_to_soa_kernel<T><<<grid_for(words, 256), 256, 0, st>>>(staging, state(cur));
+    CKG_CUDA(cudaGetLastError());
+    CKG_CUDA(cudaStreamSynchronize(st));
+    grid_valid = false;
+    return CKG_OK;
+  }
+
+  int download(void* p, uint64_t count) override {
+    if (count != n) {
+      last_error = "download: particle count mismatch";
+      return CKG_ERR_CONFIG;
+    }
+    if (count == 0) return CKG_OK;
+    CKG_CUDA(cudaSetDevice(device));
+    const uint64_t words = count * (kNumFields + 1);
+    ensure_staging(words);
+    soa_to_aos_kernel<T><<<grid_for(words, 256), 256, 0, st>>>(state(cur), staging);
+    CKG_CUDA(cudaGetLastError());
+    CKG_CUDA(cudaMemcpyAsync(p, staging, words * sizeof(T), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    return CKG_OK;
+  }
+
+  uint64_t count() const override { return n; }
+
+  StepConst<T> make_const(double dt) const {
+    StepConst<T> c{};
+    c.dx = T(cfg.dx);
+    c.inv_dx = T(cfg.inv_dx);
+    c.dt = T(dt);
+    c.mass_eps = T(cfg.mass_eps);
+    c.clamp_floor = T(cfg.clamp_floor);
+    for (int a = 0; a < 3; ++a) c.gravity[a] = T(cfg.gravity[a]);
+    c.res = cfg.resolution;
+    c.D = D;
+    c.scheme = cfg.scheme;
+    c.n_materials = cfg.n_materials;
+    c.clamp_singular = cfg.clamp_singular;
+    c.n_boundaries = cfg.n_boundaries;
+    for (int m = 0; m < cfg.n_materials && m < kMaxMaterials; ++m) {
+      const ckg_material& s = cfg.materials[m];
+      MatParam<T>& d = c.mats[m];
+      d.model = s.model;
+      d.mu = T(s.mu);
+      d.lambda = T(s.lambda);
+      d.dp_alpha = T(s.dp_alpha);
+      d.bulk = T(s.bulk);
+      d.gamma = T(s.gamma);
+      d.viscosity = T(s.viscosity);
+      d.density = T(s.density);
+    }
+    return c;
+  }
+
+  // key + stable sort: perm[i] = source index of sorted position i.
+  void enqueue_sort() {
+    PState<T> cs = state(cur);
+    key_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(cs, T(cfg.inv_dx), D, keys);
+    radix_sort_pairs(keys, vals, n, key_bits, rs, st, &skeys, &perm);
+  }
+
+  void enqueue_activate(int step_idx) {
+    PState<T> cs = state(cur);
+    activate_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(cs, perm, T(cfg.inv_dx), cfg.resolution,
+                                                                  D, flags, dstat, step_idx);
+    exclusive_scan(flags, reinterpret_cast<uint32_t*>(dir), nd, scan_partials, st);
+    compact_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(flags, dir, active, nd, pool_cap, dstat);
+  }
+
+  template <int S>
+  void enqueue_p2g(const StepConst<T>& c, int step_idx) {
+    p2g_kernel<T, S><<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(state(cur), perm, c, dir, pool, pool_cap,
+                                                                 dstat, step_idx);
+  }
+  template <int S>
+  void enqueue_g2p(const StepConst<T>& c, int step_idx) {
+    g2p_kernel<T, S><<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir,
+                                                                 pool, pool_cap, dstat, step_idx);
+  }
+
+  // Enqueue one substep up to stop_after; returns nothing (errors latched).
+  // Kernels enqueue_step launches (status reset, key, 5 per radix pass,
+  // activate, 3-kernel scan, compact, clear, P2G, grid, G2P).
+  uint64_t launches_per_step(int stop_after) const {
+    int passes = (key_bits + kRadixBits - 1) / kRadixBits;
+    uint64_t k = 2 + uint64_t(passes) * 5;
+    if (stop_after >= CKG_PHASE_ACTIVATE) k += 5;
+    if (stop_after >= CKG_PHASE_CLEAR) k += 1;
+    if (stop_after >= CKG_PHASE_P2G) k += 1;
+    if (stop_after >= CKG_PHASE_GRID) k += 1;
+    if (stop_after >= CKG_PHASE_G2P) k += 1;
+    return k;
+  }
+
+  void enqueue_step(double dt, int stop_after, int step_idx, bool reset_err, bool timed) {
+    const StepConst<T> c = make_const(dt);
+    launches += launches_per_step(stop_after);
+    status_reset_kernel<<<1, 32, 0, st>>>(dstat, reset_err ? 1 : 0);
+    if (timed) CKG_CUDA(cudaEventRecord(ev[0], st));
+    enqueue_sort();
+    if (timed) CKG_CUDA(cudaEventRecord(ev[1], st));
+    if (stop_after >= CKG_PHASE_ACTIVATE) enqueue_activate(step_idx);
+    if (timed) CKG_CUDA(cudaEventRecord(ev[2], st));
+    if (stop_after >= CKG_PHASE_CLEAR)
+      clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
+    if (timed) CKG_CUDA(cudaEventRecord(ev[3], st));
+    if (stop_after >= CKG_PHASE_P2G) {
+      if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, step_idx);
+      else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_p2g<kSchemeApic>(c, step_idx);
+      else enqueue_p2g<kSchemeMls>(c, step_idx);
+    }
+    if (timed) CKG_CUDA(cudaEventRecord(ev[4], st));
+    if (stop_after >= CKG_PHASE_GRID)
+      grid_update_kernel<T><<<148 * 8, 256, 0, st>>>(pool, active, dstat, pool_cap, c, dbcs);
+    if (timed) CKG_CUDA(cudaEventRecord(ev[5], st));
+    if (stop_after >= CKG_PHASE_G2P) {
+      if (cfg.scheme == CKG_SCHEME_PIC) enqueue_g2p<kSchemePic>(c, step_idx);
+      else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_g2p<kSchemeApic>(c, step_idx);
+      else enqueue_g2p<kSchemeMls>(c, step_idx);
+    }
+    if (timed) CKG_CUDA(cudaEventRecord(ev[6], st));
+    CKG_CUDA(cudaGetLastError());
+  }
+
+  void fill_out(ckg_step_out* out, bool timed, int stop_after) {
+    std::memset(out, 0, sizeof(*out));
+    const DevStatus& h = *hstat;
+    double vm2 = 0;
+    unsigned long long vb = h.vmax2;
+    std::memcpy(&vm2, &vb, sizeof vm2);
+    out->vmax = double(std::sqrt(T(vm2)));
+    for (int m = 0; m < CKG_MAX_MATERIALS; ++m) {
+      double j;
+      unsigned long long b = h.minj[m];
+      std::memcpy(&j, &b, sizeof j);
+      out->min_j[m] = std::isfinite(j) ? j : 1.0;
+    }
+    const uint64_t per = cfg.scheme == CKG_SCHEME_MLS ? 32 : 16;
+    if (stop_after >= CKG_PHASE_P2G) {
+      out->p2g_node_visits = per * n;
+      out->p2g_transfers = n;
+    }
+    if (stop_after >= CKG_PHASE_G2P) {
+      out->g2p_node_visits = 16 * n;
+      out->g2p_transfers = n;
+    }
+    out->active_blocks = h.n_active;
+    if (timed) {
+      for (int k = 0; k < 6; ++k) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+        out->phase_ms[k] = ms;
+      }
+    }
+  }
+
+  // Returns CKG status; fills out.
+  int decode_status(ckg_step_out* out, int stop_after) {
+    const DevStatus& h = *hstat;
+    if (h.err != ~0ull) {
+      const unsigned long long p = h.err;
+      const int code = int(p & 0xff);
+      const int axis = int((p >> 8) & 0xf);
+      const uint64_t particle = (p >> 12) & 0xffffffffffull;
+      const int phase = int((p >> 52) & 0xf);
+      out->status = CKG_ERR_NUMERICAL;
+      out->error_code = code;
+      out->error_axis = axis;
+      out->error_particle = particle;
+      out->error_phase = phase;
+      char buf[256];
+      if (code == CKG_NUM_OUT_OF_DOMAIN)
+        std::snprintf(buf, sizeof buf, "particle %llu violates the 2-cell domain inset on axis %d",
+                      (unsigned long long)particle, axis);
+      else
+        std::snprintf(buf, sizeof buf, "%s", num_message(code));
+      last_error = buf;
+      return CKG_ERR_NUMERICAL;
+    }
+    if (stop_after >= CKG_PHASE_G2P && h.nonfinite) {
+      out->status = CKG_ERR_NUMERICAL;
+      out->error_code = CKG_NUM_NONFINITE;
+      out->error_phase = CKG_PHASE_G2P;
+      last_error = "non-finite particle state after step " + std::to_string(step_count + 1);
+      return CKG_ERR_NUMERICAL;
+    }
+    return CKG_OK;
+  }
+
+  int step(double dt, int stop_after, int count_steps, ckg_step_out* out) override {
+    CKG_CUDA(cudaSetDevice(device));
+    ckg_step_out local;
+    if (!out) out = &local;
+    if (n == 0) {
+      std::memset(out, 0, sizeof(*out));
+      for (double& j : out->min_j) j = 1.0;
+      if (stop_after >= CKG_PHASE_G2P) step_count += uint64_t(count_steps);
+      return CKG_OK;
+    }
+    const bool timed = count_steps == 1;
+    launches = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (count_steps == 1) {
+        enqueue_step(dt, stop_after, 0, true, timed);
+      } else {
+        for (int k = 0; k < count_steps; ++k) {
+          enqueue_step(dt, CKG_PHASE_G2P, k, k == 0, false);
+          cur ^= 1;
+        }
+      }
+      CKG_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+      CKG_CUDA(cudaStreamSynchronize(st));
+      if (hstat->overflow && count_steps == 1) {
+        // grow the pool (state untouched: G2P writes the other buffer)
+        uint64_t want = std::min<uint64_t>(nd, uint64_t(hstat->n_active) * 5 / 4 + 64);
+        set_pool_cap(uint32_t(want));
+        continue;
+      }
+      break;
+    }
+    fill_out(out, timed, count_steps == 1 ? stop_after : CKG_PHASE_G2P);
+    out->kernel_launches = launches;
+    grid_valid = true;
+    last_active = hstat->n_active;
+    if (hstat->overflow) {
+      last_error = "grid block pool capacity exceeded";
+      out->status = CKG_ERR_DEVICE;
+      return CKG_ERR_DEVICE;
+    }
+    int rc = decode_status(out, count_steps == 1 ? stop_after : CKG_PHASE_G2P);
+    if (count_steps == 1) {
+      if (rc == CKG_OK && stop_after >= CKG_PHASE_G2P) {
+        cur ^= 1;
+        step_count += 1;
+      }
+    } else if (rc == CKG_OK) {
+      step_count += uint64_t(count_steps);
+    }
+    out->status = rc;
+    return rc;
+  }
+
+  int debug_sort(uint32_t* hkeys, uint32_t* horder, uint64_t count) override {
+    if (count != n) return CKG_ERR_CONFIG;
+    if (n == 0) return CKG_OK;
+    CKG_CUDA(cudaSetDevice(device));
+    enqueue_sort();
+    CKG_CUDA(cudaMemcpyAsync(hkeys, skeys, n * 4, cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaMemcpyAsync(horder, perm, n * 4, cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    return CKG_OK;
+  }
+
+  int debug_bases(int32_t* hb, uint64_t count) override {
+    if (count != n) return CKG_ERR_CONFIG;
+    if (n == 0) return CKG_OK;
+    CKG_CUDA(cudaSetDevice(device));
+    int32_t* d = dalloc<int32_t>(n * 6);
+    bases_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), T(cfg.dx), d);
+    CKG_CUDA(cudaMemcpyAsync(hb, d, n * 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d);
+    return CKG_OK;
+  }
+
+  uint64_t active_blocks() override { return grid_valid ? std::min<uint64_t>(last_active, pool_cap) : 0; }
+
+  int grid_download(int32_t* coords, double* nodes, uint64_t nb) override {
+    CKG_CUDA(cudaSetDevice(device));
+    nb = std::min<uint64_t>(nb, active_blocks());
+    if (nb == 0) return CKG_OK;
+    int32_t* dc = coords ? dalloc<int32_t>(nb * 3) : nullptr;
+    double* dn = nodes ? dalloc<double>(nb * 128 * 4) : nullptr;
+    grid_export_kernel<T><<<grid_for(nb * 128, 256), 256, 0, st>>>(pool, active, nb, D, dc, dn);
+    CKG_CUDA(cudaGetLastError());
+    if (dc) CKG_CUDA(cudaMemcpyAsync(coords, dc, nb * 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (dn) CKG_CUDA(cudaMemcpyAsync(nodes, dn, nb * 512 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    if (dc) cudaFree(dc);
+    if (dn) cudaFree(dn);
+    return CKG_OK;
+  }
+
+  int grid_totals(double* mass, double* mom) override {
+    uint64_t nb = active_blocks();
+    std::vector<double> nodes(std::max<uint64_t>(nb, 1) * 512);
+    for (int g = 0; g < 2; ++g) {
+      mass[g] = 0;
+      for (int a = 0; a < 3; ++a) mom[g * 3 + a] = 0;
+    }
+    if (nb == 0) return CKG_OK;
+    int rc = grid_download(nullptr, nodes.data(), nb);
+    if (rc) return rc;
+    // Same summation order as BlockSparseGrid::total_mass (grid.hpp:199-213)
+    // over blocks in directory order.
+    for (uint64_t b = 0; b < nb; ++b)
+      for (int g = 0; g < 2; ++g)
+        for (int l = 0; l < 64; ++l) {
+          const double* o = &nodes[(b * 128 + g * 64 + l) * 4];
+          mass[g] += o[0];
+          for (int a = 0; a < 3; ++a) mom[g * 3 + a] += o[1 + a];
+        }
+    return CKG_OK;
+  }
+
+  int timer_mark(int slot) override {
+    if (slot < 0 || slot >= 16) return CKG_ERR_CONFIG;
+    CKG_CUDA(cudaEventRecord(tev[slot], st));
+    return CKG_OK;
+  }
+
+  int timer_elapsed(int a, int b, double* ms) override {
+    if (a < 0 || a >= 16 || b < 0 || b >= 16 || !ms) return CKG_ERR_CONFIG;
+    CKG_CUDA(cudaEventSynchronize(tev[b]));
+    float f = 0;
+    CKG_CUDA(cudaEventElapsedTime(&f, tev[a], tev[b]));
+    *ms = f;
+    return CKG_OK;
+  }
+
+  int diagnostics(ckg_diagnostics* out) override {
+    std::memset(out, 0, sizeof(*out));
+    if (n == 0) return CKG_OK;
+    CKG_CUDA(cudaSetDevice(device));
+    CKG_CUDA(cudaMemsetAsync(dacc, 0, 12 * sizeof(double), st));
+    diagnostics_kernel<T><<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(
+        state(cur), dacc, reinterpret_cast<unsigned long long*>(dacc + 10));
+    double h[12];
+    CKG_CUDA(cudaMemcpyAsync(h, dacc, sizeof h, cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    for (int a = 0; a < 3; ++a) {
+      out->momentum[a] = h[a];
+      out->angular[a] = h[3 + a];
+      out->momentum_massfree[a] = h[6 + a];
+    }
+    out->kinetic_energy = h[9];
+    double vm2;
+    std::memcpy(&vm2, &h[10], sizeof vm2);
+    out->vmax = std::sqrt(vm2);
+    return CKG_OK;
+  }
+};
+
+}  // namespace ckg
+
+struct ckg_ctx {
+  std::unique_ptr<ckg::CtxBase> impl;
+  std::string err;
+};
+
+namespace {
+
+int32_t guard(ckg_ctx* ctx, const char* where, const std::function<int32_t()>& f) {
+  try {
+    return f();
+  } catch (const ckg::CudaError& e) {
+    if (ctx) ctx->err = std::string(where) + ": CUDA error " + cudaGetErrorString(e.e) + " in " + e.what;
+    std::fprintf(stderr, "[ckmpm_b200] %s: CUDA error %s in %s\n", where, cudaGetErrorString(e.e), e.what);
+    return CKG_ERR_DEVICE;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->err = std::string(where) + ": host allocation failed";
+    return CKG_ERR_DEVICE;
+  }
+}
+
+std::string validate(const ckg_config* c) {
+  if (!c) return "config: null";
+  if (c->abi_version != CKG_ABI_VERSION) return "config: ABI version mismatch";
+  if (c->precision != 8 && c->precision != 4) return "precision: must be 4 or 8";
+  if (c->resolution < 8) return "resolution: must be at least 8";
+  if (!(c->extent > 0)) return "extent: must be positive";
+  if (!(c->dx > 0) || !(c->inv_dx > 0)) return "grid dx must be positive";
+  if (c->scheme < 0 || c->scheme > 2) return "scheme: expected 'pic', 'apic' or 'mls'";
+  if (c->n_materials < 1) return "materials: at least one required";
+  if (c->n_materials > CKG_MAX_MATERIALS) return "materials: too many for the device table";
+  if (c->n_boundaries < 0 || c->n_boundaries > CKG_MAX_BOUNDARIES) return "boundaries: too many";
+  for (int m = 0; m < c->n_materials; ++m) {
+    int model = c->materials[m].model;
+    if (model != CKG_MODEL_FIXED_COROTATED && model != CKG_MODEL_J_FLUID && model != CKG_MODEL_DRUCKER_PRAGER)
+      return "material: reserved tag and not implemented";
+  }
+  long long D = c->resolution / 4 + 2;
+  if (D * D * D >= (1ll << 31)) return "resolution: too large for the block directory";
+  return {};
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ckg_abi_version(void) { return CKG_ABI_VERSION; }
+
+const char* ckg_build_info(void) {
+  return "ckmpm_b200 abi 1; sm_100a";
+}
+
+const char* ckg_status_string(int32_t s) {
+  switch (s) {
+    case CKG_OK: return "ok";
+    case CKG_ERR_CONFIG: return "ConfigError";
+    case CKG_ERR_NUMERICAL: return "NumericalError";
+    case CKG_ERR_IO: return "IoError";
+    case CKG_ERR_DEVICE: return "DeviceError";
+    default: return "unknown";
+  }
+}
+
+int32_t ckg_create(const ckg_config* cfg, ckg_ctx** out) {
+  if (!out) return CKG_ERR_CONFIG;
+  *out = nullptr;
+  std::string v = validate(cfg);
+  if (!v.empty()) {
+    std::fprintf(stderr, "[ckmpm_b200] ckg_create: %s\n", v.c_str());
+    return CKG_ERR_CONFIG;
+  }
+  auto* ctx = new ckg_ctx();
+  int32_t rc = guard(ctx, "ckg_create", [&]() -> int32_t {
+    int ndev = 0;
+    { cudaError_t e_ = cudaGetDeviceCount(&ndev); if (e_ != cudaSuccess) throw ckg::CudaError{e_, "cudaGetDeviceCount"}; }
+    if (cfg->device < 0 || cfg->device >= ndev) throw ckg::CudaError{cudaErrorInvalidDevice, "device ordinal"};
+    if (cfg->precision == 8)
+      ctx->impl.reset(new ckg::Context<double>(*cfg));
+    else
+      ctx->impl.reset(new ckg::Context<float>(*cfg));
+    return CKG_OK;
+  });
+  if (rc != CKG_OK) {
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return CKG_OK;
+}
+
+void ckg_destroy(ckg_ctx* ctx) { delete ctx; }
+
+int32_t ckg_upload(ckg_ctx* ctx, const void* particles, uint64_t n) {
+  if (!ctx || (!particles && n)) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_upload", [&] { return ctx->impl->upload(particles, n); });
+}
+
+int32_t ckg_download(ckg_ctx* ctx, void* particles, uint64_t n) {
+  if (!ctx || (!particles && n)) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_download", [&] { return ctx->impl->download(particles, n); });
+}
+
+uint64_t ckg_particle_count(const ckg_ctx* ctx) { return ctx ? ctx->impl->count() : 0; }
+
+int32_t ckg_set_mass_epsilon(ckg_ctx* ctx, double eps) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  ctx->impl->cfg.mass_eps = eps;
+  return CKG_OK;
+}
+
+int32_t ckg_step(ckg_ctx* ctx, double dt, ckg_step_out* out) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_step", [&] { return ctx->impl->step(dt, CKG_PHASE_G2P, 1, out); });
+}
+
+int32_t ckg_step_many(ckg_ctx* ctx, double dt, int32_t count, ckg_step_out* out) {
+  if (!ctx || count < 1 || count > 255) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_step_many", [&] { return ctx->impl->step(dt, CKG_PHASE_G2P, count, out); });
+}
+
+int32_t ckg_step_phases(ckg_ctx* ctx, double dt, int32_t stop_after, ckg_step_out* out) {
+  if (!ctx || stop_after < CKG_PHASE_SORT || stop_after > CKG_PHASE_G2P) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_step_phases", [&] { return ctx->impl->step(dt, stop_after, 1, out); });
+}
+
+int32_t ckg_debug_sort(ckg_ctx* ctx, uint32_t* keys, uint32_t* order, uint64_t n) {
+  if (!ctx || (n && (!keys || !order))) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_debug_sort", [&] { return ctx->impl->debug_sort(keys, order, n); });
+}
+
+int32_t ckg_debug_bases(ckg_ctx* ctx, int32_t* bases, uint64_t n) {
+  if (!ctx || (n && !bases)) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_debug_bases", [&] { return ctx->impl->debug_bases(bases, n); });
+}
+
+uint64_t ckg_grid_active_block_count(ckg_ctx* ctx) { return ctx ? ctx->impl->active_blocks() : 0; }
+
+int32_t ckg_grid_download(ckg_ctx* ctx, int32_t* coords, double* nodes, uint64_t nb) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_grid_download", [&] { return ctx->impl->grid_download(coords, nodes, nb); });
+}
+
+int32_t ckg_grid_totals(ckg_ctx* ctx, double mass[2], double momentum[6]) {
+  if (!ctx || !mass || !momentum) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_grid_totals", [&] { return ctx->impl->grid_totals(mass, momentum); });
+}
+
+int32_t ckg_diagnostics_compute(ckg_ctx* ctx, ckg_diagnostics* out) {
+  if (!ctx || !out) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_diagnostics_compute", [&] { return ctx->impl->diagnostics(out); });
+}
+
+int32_t ckg_timer_mark(ckg_ctx* ctx, int32_t slot) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_timer_mark", [&] { return ctx->impl->timer_mark(slot); });
+}
+
+int32_t ckg_timer_elapsed(ckg_ctx* ctx, int32_t a, int32_t b, double* ms) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_timer_elapsed", [&] { return ctx->impl->timer_elapsed(a, b, ms); });
+}
+
+int32_t ckg_last_error_message(ckg_ctx* ctx, char* buf, uint64_t cap) {
+  if (!ctx || !buf || cap == 0) return CKG_ERR_CONFIG;
+  const std::string& s = ctx->impl && !ctx->impl->last_error.empty() ? ctx->impl->last_error : ctx->err;
+  std::snprintf(buf, cap, "%s", s.c_str());
+  return CKG_OK;
+}
+
+}  // extern "C"

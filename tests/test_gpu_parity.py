@@ -1,0 +1,218 @@
+"""GPU parity vs the reference engine / C oracle, through the C-ABI.
+
+Bit-exact: block keys, stable sorted order, the 6 stencil bases, the active
+block set (SURVEY §8c parity protocol).  Tolerance: P2G node sums <= 1e-13
+relative to the field scale (test_transfer.cpp:139-141); particle state after
+1 / 10 / 100 substeps <= 1e-12 / 1e-10 / 1e-8 relative (north star: float
+atomics reorder sums)."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from oracle import bind
+from paper_2412_10399_b200 import abi
+from paper_2412_10399_b200.scene import (InvertedElementError, NumericalError, OutOfDomainError,
+                                         SceneConfig, seed_particles)
+from tests.gpu_util import field_rel, gpu_sim, match_by_tag, nodes_by_coord, tag_volumes
+from tests.util import perturb, small_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _shuffled(p, seed=0):
+    return p[np.random.default_rng(seed).permutation(len(p))]
+
+
+def _adversarial(res, n=20000, seed=0):
+    """Positions on and next to quarter-cell / block boundaries at a
+    non-power-of-two resolution (where the multiply- and divide-form bin
+    formulas can disagree)."""
+    obj = {"resolution": res, "scheme": "apic", "materials": [{"model": "fixed_corotated", "density": 1000.0,
+                                                                "E": 1e5, "nu": 0.3}],
+           "bodies": [{"shape": {"kind": "box", "lo": [0.3, 0.3, 0.3], "hi": [0.4, 0.4, 0.4]}, "material": 0}]}
+    cfg = SceneConfig.from_json(obj)
+    dx = cfg.dx()
+    rng = np.random.default_rng(seed)
+    cells = rng.integers(3, res - 4, (n, 3)).astype(np.float64)
+    frac = rng.choice([0.0, 0.25, 0.5, 0.75, 1.0], (n, 3))
+    ulps = rng.integers(-3, 4, (n, 3))
+    x = (cells + frac) * dx
+    x = x + ulps * np.spacing(x)
+    p = np.zeros(n, dtype=abi.particle_dtype(8))
+    p["x"] = x
+    p["F"] = np.eye(3)
+    p["J"] = 1.0
+    p["mass"] = 1.0
+    p["volume0"] = dx ** 3 / 8
+    return cfg, p
+
+
+@pytest.mark.parametrize("res", [32, 96, 100, 200])
+def test_binning_bitwise(res):
+    if res == 32:
+        cfg = small_scene(res=32)
+        p = _shuffled(perturb(seed_particles(cfg), seed=1, xscale=1.5, dx=1 / 32))
+    else:
+        cfg, p = _adversarial(res, seed=res)
+    k_ref, o_ref = bind.ref_sort(cfg, p)
+    sim = gpu_sim(cfg, p)
+    k_gpu, o_gpu = sim.debug_sort()
+    assert np.array_equal(k_gpu, k_ref)
+    assert np.array_equal(o_gpu, o_ref)
+    # stencil bases, both grids (kernel.hpp:114-120), vs the reference axis_pair
+    bases = sim.debug_bases()
+    r = bind.ref_lib()
+    b = C.c_int32()
+    v = (C.c_double * 5)()
+    dx = cfg.dx()
+    idx = np.random.default_rng(res).choice(len(p), min(len(p), 3000), replace=False)
+    for i in idx:
+        for g, k in ((0, -1), (1, 1)):
+            for a in range(3):
+                r.ckref_axis_pair(float(p["x"][i, a]), k, float(dx), C.byref(b), v)
+                assert bases[i, g, a] == b.value
+
+
+def test_activation_set_bitwise():
+    cfg = small_scene(res=32)
+    p = perturb(seed_particles(cfg), seed=3, xscale=1.0, dx=1 / 32)
+    ref = bind.Ref(cfg, p)
+    assert ref.step(1e-5)[0] == 0
+    rc, _ = ref.grid()
+    sim = gpu_sim(cfg, p)
+    sim.step_phases(1e-5, abi.PHASE_ACTIVATE)
+    gc, _ = sim.grid().blocks()
+    assert sim.grid().active_block_count() == len(rc)
+    assert set(map(tuple, gc)) == set(map(tuple, rc))
+
+
+@pytest.mark.parametrize("scheme", ["pic", "apic", "mls"])
+@pytest.mark.parametrize("model", ["fixed_corotated", "drucker_prager", "j_fluid"])
+def test_p2g_nodes(scheme, model):
+    cfg = small_scene(scheme=scheme, model=model, res=32)
+    p = perturb(seed_particles(cfg), seed=4, fscale=0.05, dx=1 / 32)
+    dt = 2e-4
+    rc, msg, rcoords, rnodes = bind.ref_p2g(cfg, p, dt)
+    assert rc == 0, msg
+    sim = gpu_sim(cfg, p)
+    sim.step_phases(dt, abi.PHASE_P2G)
+    gcoords, gnodes = sim.grid().blocks()
+    G = nodes_by_coord(gcoords, gnodes)
+    R = nodes_by_coord(rcoords, rnodes)
+    assert set(G) == set(R)
+    a = np.stack([G[k] for k in R])
+    b = np.stack([R[k] for k in R])
+    for comp in range(4):
+        scale = np.max(np.abs(b[..., comp]))
+        err = np.max(np.abs(a[..., comp] - b[..., comp])) / scale
+        assert err <= 1e-13, (comp, err)
+
+
+STEP_CASES = [
+    ("pic", "fixed_corotated", "sticky"),
+    ("apic", "fixed_corotated", "sticky"),
+    ("mls", "fixed_corotated", "none"),
+    ("apic", "drucker_prager", "separate"),
+    ("apic", "j_fluid", "slip"),
+]
+
+
+@pytest.mark.parametrize("scheme,model,bc", STEP_CASES)
+def test_state_after_n_steps(scheme, model, bc):
+    cfg = small_scene(scheme=scheme, model=model, bc=bc, res=32)
+    p0 = tag_volumes(perturb(seed_particles(cfg), seed=5, fscale=0.02, dx=1 / 32))
+    orc = bind.Oracle(cfg, p0)
+    sim = gpu_sim(cfg, p0)
+    tol = {1: 1e-12, 10: 1e-10, 100: 1e-8}
+    done = 0
+    for target in (1, 10, 100):
+        while done < target:
+            dt = orc.cfl_dt(1.0)
+            gdt = sim.cfl_dt(1.0)
+            assert abs(dt - gdt) <= 1e-9 * dt
+            rc, msg, _ = orc.step(dt)
+            assert rc == 0, msg
+            sim.step(dt)
+            done += 1
+        a, b = match_by_tag(sim.particles(), orc.particles())
+        for f in ("x", "v", "F", "B", "J"):
+            e = field_rel(a, b, f)
+            assert e <= tol[target], (target, f, e)
+
+
+def test_momentum_conservation_matches_reference_level():
+    # force-free colliding blocks: total momentum must stay at round-off
+    cfg = small_scene(scheme="apic", res=48, bc="none", gravity=(0, 0, 0), lo=(0.3, 0.3, 0.3),
+                      hi=(0.45, 0.45, 0.45), velocity=(0.3, -0.2, 0.1), E=1e4)
+    p = seed_particles(cfg)
+    sim = gpu_sim(cfg, p)
+    d0 = sim.diagnostics()
+    for _ in range(100):
+        sim.step(sim.cfl_dt(1.0))
+    d1 = sim.diagnostics()
+    pscale = float(np.sum(p["mass"]) * np.max(np.abs(p["v"])))
+    assert np.max(np.abs(d1.momentum - d0.momentum)) <= 1e-12 * pscale
+
+
+def test_out_of_domain_error_identifies_particle():
+    cfg = small_scene(res=32)
+    p = seed_particles(cfg)
+    p["x"][5, 0] = 1.5 / 32
+    ref = bind.Ref(cfg, p)
+    rc, msg = ref.step(1e-4)
+    sim = gpu_sim(cfg, p)
+    with pytest.raises(OutOfDomainError) as ei:
+        sim.step(1e-4)
+    assert str(ei.value) == msg
+    assert ei.value.particle_index == int(msg.split()[1])
+
+
+def test_nonfinite_state_aborts_loudly():
+    cfg = small_scene(res=32)
+    p = seed_particles(cfg)
+    p["v"][10, 1] = np.nan  # test_sim.cpp:412-417
+    sim = gpu_sim(cfg, p)
+    with pytest.raises(NumericalError, match="non-finite particle state after step 1"):
+        sim.step(1e-4)
+
+
+def test_inverted_element_raises():
+    cfg = small_scene(res=32)
+    p = seed_particles(cfg)
+    p["F"][3] = np.diag([1.0, 1.0, -1.0])
+    sim = gpu_sim(cfg, p)
+    with pytest.raises(InvertedElementError, match="fixed corotated stress: det F <= 0"):
+        sim.step(1e-4)
+
+
+def test_float_mode_vs_reference_float():
+    cfg = small_scene(scheme="apic", res=32)
+    p32 = seed_particles(cfg, 4)
+    k_ref, o_ref = bind.ref_sort(cfg, p32, precision=4)
+    sim = gpu_sim(cfg, p32, precision=4)
+    k, o = sim.debug_sort()
+    assert np.array_equal(k, k_ref) and np.array_equal(o, o_ref)
+    ref = bind.Ref(cfg, p32, precision=4)
+    for _ in range(3):
+        dt = ref.cfl_dt(1.0)
+        assert ref.step(dt)[0] == 0
+        sim.step(dt)
+    a, b = sim.particles(), ref.particles()
+    for f in ("x", "v", "F"):
+        assert field_rel(a, b, f) <= 1e-5, f
+
+
+def test_step_many_equals_single_steps():
+    cfg = small_scene(scheme="apic", res=32)
+    p = seed_particles(cfg)
+    s1 = gpu_sim(cfg, p)
+    s2 = gpu_sim(cfg, p)
+    dt = s1.cfl_dt(1.0)
+    for _ in range(5):
+        s1.step(dt)
+    s2.step_many(dt, 5)
+    a, b = s1.particles(), s2.particles()
+    for f in ("x", "v", "F", "B"):
+        assert field_rel(a, b, f) <= 1e-12
