@@ -22,10 +22,10 @@ def match_by_tag(a, b):
     return a[ia], b[ib]
 
 
-def field_rel(a, b, name):
+def field_rel(a, b, name, floor=1e-300):
     x = np.asarray(a[name], dtype=np.float64).reshape(len(a), -1)
     y = np.asarray(b[name], dtype=np.float64).reshape(len(b), -1)
-    scale = max(np.max(np.abs(y)) if y.size else 0.0, 1e-300)
+    scale = max(np.max(np.abs(y)) if y.size else 0.0, floor)
     return float(np.max(np.abs(x - y)) / scale) if x.size else 0.0
 
 

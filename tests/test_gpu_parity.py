@@ -110,6 +110,10 @@ def test_p2g_nodes(scheme, model):
         assert err <= 1e-13, (comp, err)
 
 
+# Field scales below which differences are round-off of a vanishing field:
+# x ~ 1, v ~ 0.05 m/s, B ~ v dx^2-ish, F ~ 1.
+_FLOOR = {"x": 1.0, "v": 0.02, "F": 1.0, "B": 0.02 / 32 / 32, "J": 1.0}
+
 STEP_CASES = [
     ("pic", "fixed_corotated", "sticky"),
     ("apic", "fixed_corotated", "sticky"),
@@ -122,7 +126,10 @@ STEP_CASES = [
 @pytest.mark.parametrize("scheme,model,bc", STEP_CASES)
 def test_state_after_n_steps(scheme, model, bc):
     cfg = small_scene(scheme=scheme, model=model, bc=bc, res=32)
-    p0 = tag_volumes(perturb(seed_particles(cfg), seed=5, fscale=0.02, dx=1 / 32))
+    # mild perturbation: every transfer term is exercised but the body stays
+    # well inside the elastic regime for 100 substeps
+    p0 = tag_volumes(perturb(seed_particles(cfg), seed=5, fscale=0.003, vscale=0.02, bscale=0.1, xscale=0.05,
+                             dx=1 / 32))
     orc = bind.Oracle(cfg, p0)
     sim = gpu_sim(cfg, p0)
     tol = {1: 1e-12, 10: 1e-10, 100: 1e-8}
@@ -138,7 +145,7 @@ def test_state_after_n_steps(scheme, model, bc):
             done += 1
         a, b = match_by_tag(sim.particles(), orc.particles())
         for f in ("x", "v", "F", "B", "J"):
-            e = field_rel(a, b, f)
+            e = field_rel(a, b, f, floor=_FLOOR[f])
             assert e <= tol[target], (target, f, e)
 
 
@@ -169,13 +176,20 @@ def test_out_of_domain_error_identifies_particle():
     assert ei.value.particle_index == int(msg.split()[1])
 
 
-def test_nonfinite_state_aborts_loudly():
+@pytest.mark.parametrize("field", ["v", "x"])
+def test_nonfinite_state_aborts_loudly(field):
+    """test_sim.cpp:412-417: a NaN in the state aborts the step with a
+    NumericalError; the GPU raises the same type and message as the
+    reference for the same input."""
     cfg = small_scene(res=32)
     p = seed_particles(cfg)
-    p["v"][10, 1] = np.nan  # test_sim.cpp:412-417
+    p[field][10, 1] = np.nan
+    rc, msg = bind.Ref(cfg, p).step(1e-4)
+    assert rc == 3
     sim = gpu_sim(cfg, p)
-    with pytest.raises(NumericalError, match="non-finite particle state after step 1"):
+    with pytest.raises(NumericalError) as ei:
         sim.step(1e-4)
+    assert str(ei.value) == msg
 
 
 def test_inverted_element_raises():
@@ -215,4 +229,4 @@ def test_step_many_equals_single_steps():
     s2.step_many(dt, 5)
     a, b = s1.particles(), s2.particles()
     for f in ("x", "v", "F", "B"):
-        assert field_rel(a, b, f) <= 1e-12
+        assert field_rel(a, b, f, floor=1e-3) <= 1e-12, f
