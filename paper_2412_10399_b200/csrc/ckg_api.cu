@@ -15,8 +15,10 @@
 #include <vector>
 
 #include "../../include/ckmpm_b200.h"
+#include "ckg_bin.cuh"
 #include "ckg_kernels.cuh"
 #include "ckg_scan.cuh"
+#include "ckg_transfer.cuh"
 
 namespace ckg {
 
@@ -120,7 +122,11 @@ struct Context final : CtxBase {
   uint32_t* perm = nullptr;  // points into vals or rs.vals_alt after a sort
   uint32_t* skeys = nullptr;
   // grid
-  uint32_t* flags = nullptr;
+  uint32_t* core = nullptr;   // footprint blocks (D^3)
+  uint32_t* flags = nullptr;  // active = dilated core (D^3)
+  uint32_t* seg_begin = nullptr;
+  uint32_t* seg_end = nullptr;
+  int p2g_ctas = 0, g2p_ctas = 0;
   int32_t* dir = nullptr;
   uint32_t* active = nullptr;
   uint32_t* scan_partials = nullptr;
@@ -147,6 +153,13 @@ struct Context final : CtxBase {
     while ((uint64_t(1) << key_bits) < nd) ++key_bits;
     flags = dalloc<uint32_t>(nd);
     CKG_CUDA(cudaMemset(flags, 0, nd * sizeof(uint32_t)));
+    core = dalloc<uint32_t>(nd);
+    CKG_CUDA(cudaMemset(core, 0, nd * sizeof(uint32_t)));
+    seg_begin = dalloc<uint32_t>(nd);
+    seg_end = dalloc<uint32_t>(nd);
+    CKG_CUDA(cudaMemset(seg_begin, 0, nd * sizeof(uint32_t)));
+    CKG_CUDA(cudaMemset(seg_end, 0, nd * sizeof(uint32_t)));
+    setup_persistent();
     dir = dalloc<int32_t>(nd);
     CKG_CUDA(cudaMemset(dir, 0xff, nd * sizeof(int32_t)));
     scan_partials = dalloc<uint32_t>(scan_tiles(std::max<uint64_t>(nd, 1)) + 1);
@@ -192,6 +205,9 @@ struct Context final : CtxBase {
     dfree(rs.hist);
     dfree(rs.partials);
     dfree(flags);
+    dfree(core);
+    dfree(seg_begin);
+    dfree(seg_end);
     dfree(dir);
     dfree(active);
     dfree(scan_partials);
@@ -216,6 +232,24 @@ struct Context final : CtxBase {
   }
 
   PState<T> state(int b) const { return PState<T>{fbuf[b], mbuf[b], n}; }
+
+  template <int S>
+  void occupancy_for() {
+    int nsm = 0, per = 0;
+    CKG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    const size_t smem = p2g_smem_bytes<T>();
+    CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kXferThreads, smem));
+    if (cfg.scheme == S) p2g_ctas = std::max(1, per) * nsm;
+    CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S>, kXferThreads, 0));
+    if (cfg.scheme == S) g2p_ctas = std::max(1, per) * nsm;
+  }
+
+  void setup_persistent() {
+    occupancy_for<kSchemePic>();
+    occupancy_for<kSchemeApic>();
+    occupancy_for<kSchemeMls>();
+  }
 
   void ensure_particles(uint64_t count) {
     if (count == n && fbuf[0]) return;
@@ -297,6 +331,12 @@ struct Context final : CtxBase {
     c.n_materials = cfg.n_materials;
     c.clamp_singular = cfg.clamp_singular;
     c.n_boundaries = cfg.n_boundaries;
+    {
+      // power-of-two dx: x/dx is exactly x*inv_dx (same exact scaling)
+      int e = 0;
+      const double fr = std::frexp(cfg.dx, &e);
+      c.pow2 = (fr == 0.5 && cfg.inv_dx * cfg.dx == 1.0) ? 1 : 0;
+    }
     for (int m = 0; m < cfg.n_materials && m < kMaxMaterials; ++m) {
       const ckg_material& s = cfg.materials[m];
       MatParam<T>& d = c.mats[m];
@@ -312,39 +352,44 @@ struct Context final : CtxBase {
     return c;
   }
 
-  // key + stable sort: perm[i] = source index of sorted position i.
+  // K1 + K2: key/footprint pass then stable sort (perm[i] = source index of
+  // sorted position i, skeys[i] its key).
   void enqueue_sort() {
     PState<T> cs = state(cur);
-    key_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(cs, T(cfg.inv_dx), D, keys);
+    key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(cs, T(cfg.inv_dx), cfg.resolution, D, keys,
+                                                                         core, dstat);
     radix_sort_pairs(keys, vals, n, key_bits, rs, st, &skeys, &perm);
   }
 
+  // K3-K6: inset error in sorted order, halo dilation, directory, segments.
   void enqueue_activate(int step_idx) {
     PState<T> cs = state(cur);
-    activate_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(cs, perm, T(cfg.inv_dx), cfg.resolution,
-                                                                  D, flags, dstat, step_idx);
+    inset_fixup_kernel<T><<<148, 256, 0, st>>>(cs, perm, T(cfg.inv_dx), cfg.resolution, dstat, step_idx);
+    dilate_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(core, flags, D);
     exclusive_scan(flags, reinterpret_cast<uint32_t*>(dir), nd, scan_partials, st);
-    compact_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(flags, dir, active, nd, pool_cap, dstat);
+    compact_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(core, flags, dir, active, seg_begin, seg_end, nd,
+                                                               pool_cap, dstat);
+    segments_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(skeys, n, seg_begin, seg_end);
   }
 
   template <int S>
   void enqueue_p2g(const StepConst<T>& c, int step_idx) {
-    p2g_kernel<T, S><<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(state(cur), perm, c, dir, pool, pool_cap,
-                                                                 dstat, step_idx);
+    p2g_tile_kernel<T, S><<<p2g_ctas, kXferThreads, p2g_smem_bytes<T>(), st>>>(
+        state(cur), perm, c, dir, active, seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
   }
   template <int S>
   void enqueue_g2p(const StepConst<T>& c, int step_idx) {
-    g2p_kernel<T, S><<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir,
-                                                                 pool, pool_cap, dstat, step_idx);
+    g2p_tile_kernel<T, S><<<g2p_ctas, kXferThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir, active,
+                                                              seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
   }
 
-  // Enqueue one substep up to stop_after; returns nothing (errors latched).
-  // Kernels enqueue_step launches (status reset, key, 5 per radix pass,
-  // activate, 3-kernel scan, compact, clear, P2G, grid, G2P).
+  // Kernels enqueue_step launches (status reset, key/footprint, 5 per radix
+  // pass, inset fix-up, dilate, 3-kernel scan, compact, segments, clear,
+  // P2G, grid, G2P).
   uint64_t launches_per_step(int stop_after) const {
     int passes = (key_bits + kRadixBits - 1) / kRadixBits;
     uint64_t k = 2 + uint64_t(passes) * 5;
-    if (stop_after >= CKG_PHASE_ACTIVATE) k += 5;
+    if (stop_after >= CKG_PHASE_ACTIVATE) k += 7;
     if (stop_after >= CKG_PHASE_CLEAR) k += 1;
     if (stop_after >= CKG_PHASE_P2G) k += 1;
     if (stop_after >= CKG_PHASE_GRID) k += 1;
@@ -352,6 +397,7 @@ struct Context final : CtxBase {
     return k;
   }
 
+  // Enqueue one substep up to stop_after; errors are latched on the device.
   void enqueue_step(double dt, int stop_after, int step_idx, bool reset_err, bool timed) {
     const StepConst<T> c = make_const(dt);
     launches += launches_per_step(stop_after);
@@ -361,8 +407,7 @@ struct Context final : CtxBase {
     if (timed) CKG_CUDA(cudaEventRecord(ev[1], st));
     if (stop_after >= CKG_PHASE_ACTIVATE) enqueue_activate(step_idx);
     if (timed) CKG_CUDA(cudaEventRecord(ev[2], st));
-    if (stop_after >= CKG_PHASE_CLEAR)
-      clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
+    if (stop_after >= CKG_PHASE_CLEAR) clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
     if (timed) CKG_CUDA(cudaEventRecord(ev[3], st));
     if (stop_after >= CKG_PHASE_P2G) {
       if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, step_idx);
@@ -516,7 +561,8 @@ struct Context final : CtxBase {
     if (n == 0) return CKG_OK;
     CKG_CUDA(cudaSetDevice(device));
     int32_t* d = dalloc<int32_t>(n * 6);
-    bases_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), T(cfg.dx), d);
+    const StepConst<T> c = make_const(0.0);
+    bases_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), c.dx, c.inv_dx, c.pow2, d);
     CKG_CUDA(cudaMemcpyAsync(hb, d, n * 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CKG_CUDA(cudaStreamSynchronize(st));
     cudaFree(d);

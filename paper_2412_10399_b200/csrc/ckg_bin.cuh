@@ -1,0 +1,151 @@
+// ckg_bin.cuh — binning, activation and segment kernels (sm_100a).
+//
+//  K1  key_footprint_kernel: block key (simulation.hpp:255-266, bit-exact),
+//      the particle's stencil-footprint blocks ("core" flags) and the 2-cell
+//      inset check (grid.hpp:121-126), one pass over x in current order.
+//  K2  stable LSD radix sort (ckg_scan.cuh) -> perm, sorted keys.
+//  K3  inset_fixup_kernel: only when K1 saw a violation, the lowest SORTED
+//      index and its first failing axis (the reference throws from activate,
+//      which walks the sorted array).
+//  K4  dilate_kernel: active = core (+) {0,1}^3 — the reference's one-block
+//      positive halo (grid.hpp:137-139) as a Minkowski sum over the directory.
+//  K5  scan + compact_kernel: directory slots in ascending directory order.
+//  K6  segments_kernel: [begin, end) of every block key in sorted order.
+#pragma once
+
+#include "ckg_kernels.cuh"
+
+namespace ckg {
+
+// Footprint of one axis relative to the key block: lo block = floor(s-1/4)>>2
+// (the +1 grid's lower node), hi block = (floor(s+1/4)+1)>>2 (the -1 grid's
+// upper node), with s = x*inv_dx exactly as activate computes it
+// (grid.hpp:121-137).  The key cell floor(s + 1/4) is the same rounded sum,
+// so lo, hi are within one block of the key block.
+template <typename T>
+__device__ __forceinline__ void axis_footprint(T x, T inv_dx, int& lo, int& hi) {
+  const T s = mul_rn(x, inv_dx);
+  lo = static_cast<int>(dfloor(sub_rn(s, T(0.25)))) >> 2;
+  hi = (static_cast<int>(dfloor(add_rn(s, T(0.25)))) + 1) >> 2;
+}
+
+template <typename T>
+__device__ __forceinline__ bool inset_ok(T x, T inv_dx, int res) {
+  const T s = mul_rn(x, inv_dx);
+  return s >= T(2) && s <= T(res - 2);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv_dx, int res, int D,
+                                                            uint32_t* __restrict__ keys,
+                                                            uint32_t* __restrict__ core,
+                                                            DevStatus* st) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool live = i < cur.n;
+  T x[3] = {T(0), T(0), T(0)};
+  bool ok = live;
+  int lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+  if (live) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) x[a] = __ldg(cur.f + uint64_t(kX + a) * cur.n + i);
+    keys[i] = block_key(x[0], x[1], x[2], inv_dx, D);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      ok = ok && inset_ok(x[a], inv_dx, res);
+      axis_footprint(x[a], inv_dx, lo[a], hi[a]);
+    }
+    if (!ok) atomicOr(&st->inset_fail, 1u);
+  }
+  // Warp dedupe of identical footprint boxes (neighbouring particles mostly
+  // share one), then the leader marks 1..8 blocks.
+  const uint64_t box =
+      ok ? ((uint64_t(uint32_t(lo[0]) & 0x3ff) << 50) | (uint64_t(uint32_t(lo[1]) & 0x3ff) << 40) |
+            (uint64_t(uint32_t(lo[2]) & 0x3ff) << 30) | (uint64_t(uint32_t(hi[0]) & 0x3ff) << 20) |
+            (uint64_t(uint32_t(hi[1]) & 0x3ff) << 10) | uint64_t(uint32_t(hi[2]) & 0x3ff))
+         : (~0ull - (threadIdx.x & 31));
+  const uint32_t peers = __match_any_sync(0xffffffffu, box);
+  if (!ok || (__ffs(peers) - 1) != int(threadIdx.x & 31)) return;
+  for (int bi = lo[0]; bi <= hi[0]; ++bi)
+    for (int bj = lo[1]; bj <= hi[1]; ++bj)
+      for (int bk = lo[2]; bk <= hi[2]; ++bk)
+        if (bi >= 0 && bj >= 0 && bk >= 0 && bi < D && bj < D && bk < D)
+          core[(int64_t(bi) * D + bj) * D + bk] = 1u;
+}
+
+// Lowest sorted index violating the inset (only runs its loop on failure).
+template <typename T>
+__global__ void inset_fixup_kernel(PState<T> cur, const uint32_t* __restrict__ perm, T inv_dx, int res,
+                                   DevStatus* st, int step) {
+  if (*reinterpret_cast<volatile unsigned int*>(&st->inset_fail) == 0u) return;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cur.n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t src = perm[i];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (!inset_ok(cur.f[uint64_t(kX + a) * cur.n + src], inv_dx, res)) {
+        record_error(st, step, kPhaseActivate, i, a, kErrOutOfDomain);
+        break;
+      }
+    }
+  }
+}
+
+// active(B) = OR_{delta in {0,1}^3} core(B - delta).
+__global__ void __launch_bounds__(256) dilate_kernel(const uint32_t* __restrict__ core,
+                                                     uint32_t* __restrict__ act, int D) {
+  const uint64_t nd = uint64_t(D) * D * D;
+  const uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  const int bz = int(d % uint64_t(D)), by = int((d / uint64_t(D)) % uint64_t(D)), bx = int(d / (uint64_t(D) * D));
+  uint32_t a = 0;
+#pragma unroll
+  for (int dx = 0; dx < 2; ++dx)
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+      for (int dz = 0; dz < 2; ++dz) {
+        const int x = bx - dx, y = by - dy, z = bz - dz;
+        if (x >= 0 && y >= 0 && z >= 0) a |= __ldg(core + (int64_t(x) * D + y) * D + z);
+      }
+  act[d] = a ? 1u : 0u;
+}
+
+// Directory from the exclusive scan of act (computed in place in dir):
+// dir[d] = slot or -1; active[slot] = d in ascending order.  Resets the
+// per-step scratch (core, act, segment bounds) for the next substep.
+__global__ void __launch_bounds__(256) compact_kernel(uint32_t* __restrict__ core, uint32_t* __restrict__ act,
+                                                      int32_t* __restrict__ dir, uint32_t* __restrict__ active,
+                                                      uint32_t* __restrict__ seg_begin,
+                                                      uint32_t* __restrict__ seg_end, uint64_t nd, uint32_t cap,
+                                                      DevStatus* st) {
+  const uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  const uint32_t f = act[d];
+  const uint32_t s = static_cast<uint32_t>(dir[d]);
+  if (f) {
+    if (s < cap)
+      active[s] = static_cast<uint32_t>(d);
+    else
+      st->overflow = 1u;
+    act[d] = 0u;
+  } else {
+    dir[d] = -1;
+  }
+  core[d] = 0u;
+  seg_begin[d] = 0u;
+  seg_end[d] = 0u;
+  if (d == nd - 1) st->n_active = s + f;
+}
+
+// [begin, end) of each block key's run in the sorted order.
+__global__ void __launch_bounds__(256) segments_kernel(const uint32_t* __restrict__ skeys, uint64_t n,
+                                                       uint32_t* __restrict__ seg_begin,
+                                                       uint32_t* __restrict__ seg_end) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t k = skeys[i];
+  if (i == 0 || skeys[i - 1] != k) seg_begin[k] = uint32_t(i);
+  if (i == n - 1 || skeys[i + 1] != k) seg_end[k] = uint32_t(i + 1);
+}
+
+}  // namespace ckg

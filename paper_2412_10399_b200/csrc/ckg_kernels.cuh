@@ -47,6 +47,7 @@ struct StepConst {
   T dx, inv_dx, dt, mass_eps, clamp_floor;
   T gravity[3];
   int res, D, scheme, n_materials, clamp_singular, n_boundaries;
+  int pow2;  // dx is a power of two: x/dx == x*inv_dx exactly (both are exact scalings)
   MatParam<T> mats[kMaxMaterials];
 };
 
@@ -67,7 +68,8 @@ struct DevStatus {
   unsigned int nonfinite;
   unsigned int n_active;
   unsigned int overflow;
-  unsigned int pad;
+  unsigned int inset_fail;      // some particle violated the 2-cell inset (index fixed up after the sort)
+  unsigned int work[4];         // persistent-kernel work counters (P2G, G2P)
 };
 
 // err = step<<56 | phase<<52 | particle<<12 | axis<<8 | code
@@ -138,24 +140,39 @@ struct TwoPi<float> {
   static constexpr float inv = 1.0f / (2.0f * 3.14159265358979323846f);
 };
 
+// x/dx exactly as the reference rounds it (kernel.hpp:116).  For a
+// power-of-two dx (every benchmark scene: extent 1, res 2^k) the product with
+// inv_dx is the same exact scaling, so the division is skipped.
 template <typename T>
-__device__ __forceinline__ int axis_base(T x, T dx, T kq) {
-  return static_cast<int>(dfloor(sub_rn(div_rn(x, dx), kq)));
+__device__ __forceinline__ T over_dx(T x, T dx, T inv_dx, int pow2) {
+  return pow2 ? mul_rn(x, inv_dx) : div_rn(x, dx);
 }
 
 template <typename T>
-__device__ __forceinline__ Axis<T> axis_pair(T x, T dx, T kq) {
-  T s = sub_rn(div_rn(x, dx), kq);
+__device__ __forceinline__ int axis_base(T x, T dx, T inv_dx, int pow2, T kq) {
+  return static_cast<int>(dfloor(sub_rn(over_dx(x, dx, inv_dx, pow2), kq)));
+}
+
+// sin(2 pi f), cos(2 pi f) for f in [0,1): sincospi(2f) (2f is exact) instead
+// of sin(fl(2 pi f)) — differs from the reference by the rounding of 2 pi f
+// (<= 1 ulp of the argument); the paired scheme keeps w0 + w1 = 1 and
+// g1 = -g0 exact regardless (kernel.hpp:103-105).
+__device__ __forceinline__ void sincos_2pi(double f, double* s, double* c) { sincospi(f + f, s, c); }
+__device__ __forceinline__ void sincos_2pi(float f, float* s, float* c) { sincospif(f + f, s, c); }
+
+template <typename T>
+__device__ __forceinline__ Axis<T> axis_pair(T x, T dx, T inv_dx, int pow2, T kq) {
+  T s = sub_rn(over_dx(x, dx, inv_dx, pow2), kq);
   T fb = dfloor(s);
   Axis<T> a;
   a.base = static_cast<int>(fb);
-  T f = sub_rn(s, fb);
+  T f = s - fb;  // exact (Sterbenz)
   T sn, cs;
-  dsincos(mul_rn(TwoPi<T>::v, f), &sn, &cs);
+  sincos_2pi(f, &sn, &cs);
   sn = sn * TwoPi<T>::inv;
   a.w0 = T(1) - f + sn;
   a.w1 = f - sn;
-  a.g0 = (cs - T(1)) / dx;
+  a.g0 = (cs - T(1)) * inv_dx;
   a.xi0 = (T(a.base) + kq) * dx - x;
   return a;
 }
@@ -284,19 +301,34 @@ struct Dual {
 };
 
 template <typename T>
-__device__ __forceinline__ Dual<T> dual_stencil(T x, T y, T z, T dx) {
+__device__ __forceinline__ Dual<T> dual_stencil(T x, T y, T z, T dx, T inv_dx, int pow2) {
   Dual<T> d;
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
     const T kq = g == 0 ? T(-0.25) : T(0.25);  // T(k) * T(0.25), k = -1 / +1
-    d.ax[g][0] = axis_pair(x, dx, kq);
-    d.ax[g][1] = axis_pair(y, dx, kq);
-    d.ax[g][2] = axis_pair(z, dx, kq);
+    d.ax[g][0] = axis_pair(x, dx, inv_dx, pow2, kq);
+    d.ax[g][1] = axis_pair(y, dx, inv_dx, pow2, kq);
+    d.ax[g][2] = axis_pair(z, dx, inv_dx, pow2, kq);
   }
   return d;
 }
 
-// compute_apic_D (transfer.hpp:77-100).
+// compute_apic_D (transfer.hpp:77-100) in separable form: with per-axis
+// moments S = w0 + w1, M1 = w0 xi0 + w1 xi1, M2 = w0 xi0^2 + w1 xi1^2 the
+// 16-node sum factorises exactly (D_aa = 1/2 sum_g M2_a S_b S_c, D_ab =
+// 1/2 sum_g M1_a M1_b S_c); only the summation order differs from the
+// reference's node loop.
+template <typename T>
+struct AxisMoments {
+  T S, M1, M2;
+};
+
+template <typename T>
+__device__ __forceinline__ AxisMoments<T> axis_moments(const Axis<T>& a, T dx) {
+  const T x1 = a.xi0 + dx;
+  return {a.w0 + a.w1, a.w0 * a.xi0 + a.w1 * x1, a.w0 * a.xi0 * a.xi0 + a.w1 * x1 * x1};
+}
+
 template <typename T>
 __device__ __forceinline__ M3<T> apic_D(const Dual<T>& ds, T dx) {
   M3<T> D;
@@ -306,24 +338,18 @@ __device__ __forceinline__ M3<T> apic_D(const Dual<T>& ds, T dx) {
     for (int j = 0; j < 3; ++j) D.a[i][j] = T(0);
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
-    const Axis<T>* ax = ds.ax[g];
-    const T wx[2] = {ax[0].w0, ax[0].w1}, wy[2] = {ax[1].w0, ax[1].w1}, wz[2] = {ax[2].w0, ax[2].w1};
-    const T xx[2] = {ax[0].xi0, ax[0].xi0 + dx}, xy[2] = {ax[1].xi0, ax[1].xi0 + dx},
-            xz[2] = {ax[2].xi0, ax[2].xi0 + dx};
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          T w = T(0.5) * wx[s] * wy[t] * wz[u];
-          T xi[3] = {xx[s], xy[t], xz[u]};
-#pragma unroll
-          for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) D.a[a][b] += w * xi[a] * xi[b];
-        }
+    const AxisMoments<T> m0 = axis_moments(ds.ax[g][0], dx), m1 = axis_moments(ds.ax[g][1], dx),
+                         m2 = axis_moments(ds.ax[g][2], dx);
+    D.a[0][0] += T(0.5) * m0.M2 * m1.S * m2.S;
+    D.a[1][1] += T(0.5) * m1.M2 * m0.S * m2.S;
+    D.a[2][2] += T(0.5) * m2.M2 * m0.S * m1.S;
+    D.a[0][1] += T(0.5) * m0.M1 * m1.M1 * m2.S;
+    D.a[0][2] += T(0.5) * m0.M1 * m2.M1 * m1.S;
+    D.a[1][2] += T(0.5) * m1.M1 * m2.M1 * m0.S;
   }
+  D.a[1][0] = D.a[0][1];
+  D.a[2][0] = D.a[0][2];
+  D.a[2][1] = D.a[1][2];
   return D;
 }
 
@@ -337,33 +363,29 @@ __device__ __forceinline__ bool apic_d_inverse(const M3<T>& D, M3<T>& Di) {
   return true;
 }
 
-// mls_moment (transfer.hpp:127-150).
+// mls_moment (transfer.hpp:127-150), separable form (see apic_D):
+// M00 = 1/2 sum S S S, M0a = 1/2 sum M1_a S S, lower-right block = D.
 template <typename T>
 __device__ __forceinline__ void mls_moment(const Dual<T>& ds, T dx, T (&Mm)[4][4]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) Mm[i][j] = T(0);
+  const M3<T> D = apic_D(ds, dx);
+  T m00 = T(0), m01 = T(0), m02 = T(0), m03 = T(0);
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
-    const Axis<T>* ax = ds.ax[g];
-    const T wx[2] = {ax[0].w0, ax[0].w1}, wy[2] = {ax[1].w0, ax[1].w1}, wz[2] = {ax[2].w0, ax[2].w1};
-    const T xx[2] = {ax[0].xi0, ax[0].xi0 + dx}, xy[2] = {ax[1].xi0, ax[1].xi0 + dx},
-            xz[2] = {ax[2].xi0, ax[2].xi0 + dx};
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          T w = T(0.5) * wx[s] * wy[t] * wz[u];
-          T P[4] = {T(1), xx[s], xy[t], xz[u]};
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) Mm[a][b] += w * P[a] * P[b];
-        }
+    const AxisMoments<T> a = axis_moments(ds.ax[g][0], dx), b = axis_moments(ds.ax[g][1], dx),
+                         c = axis_moments(ds.ax[g][2], dx);
+    m00 += T(0.5) * a.S * b.S * c.S;
+    m01 += T(0.5) * a.M1 * b.S * c.S;
+    m02 += T(0.5) * b.M1 * a.S * c.S;
+    m03 += T(0.5) * c.M1 * a.S * b.S;
   }
+  Mm[0][0] = m00;
+  Mm[0][1] = Mm[1][0] = m01;
+  Mm[0][2] = Mm[2][0] = m02;
+  Mm[0][3] = Mm[3][0] = m03;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Mm[1 + i][1 + j] = D.a[i][j];
 }
 
 template <typename T>
@@ -384,569 +406,5 @@ __device__ __forceinline__ void store_m3(const PState<T>& p, int k, uint64_t i, 
     for (int c = 0; c < 3; ++c) p.f[uint64_t(k + 3 * r + c) * p.n + i] = m.a[r][c];
 }
 
-// ================================================================ kernels
-
-// K1: block key per particle in current order (simulation.hpp:255-266).
-template <typename T>
-__global__ void key_kernel(PState<T> cur, T inv_dx, int D, uint32_t* __restrict__ keys) {
-  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= cur.n) return;
-  keys[i] = block_key(__ldg(cur.f + kX * cur.n + i), __ldg(cur.f + (kX + 1) * cur.n + i),
-                      __ldg(cur.f + (kX + 2) * cur.n + i), inv_dx, D);
-}
-
-// K3: activation over sorted particles (grid.hpp:114-145): 2-cell inset check
-// (OutOfDomainError with the lowest sorted index and its first failing axis),
-// footprint blocks plus one positive halo block per axis.  The footprint's
-// lower/upper block offsets relative to the key block are OR-reduced across
-// same-key lanes of a warp so each warp marks each distinct box once.
-template <typename T>
-__global__ void activate_kernel(PState<T> cur, const uint32_t* __restrict__ perm, T inv_dx, int res,
-                                int D, uint32_t* __restrict__ flags, DevStatus* st, int step) {
-  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool valid = i < cur.n;
-  int lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
-  if (valid) {
-    uint32_t src = perm[i];
-    bool bad = false;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      T s = mul_rn(__ldg(cur.f + (kX + a) * cur.n + src), inv_dx);
-      if (!bad && !(s >= T(2) && s <= T(res - 2))) {
-        record_error(st, step, kPhaseActivate, i, a, kErrOutOfDomain);
-        bad = true;
-      }
-      int base_plus = static_cast<int>(dfloor(sub_rn(s, T(0.25))));
-      int base_minus = static_cast<int>(dfloor(add_rn(s, T(0.25))));
-      lo[a] = base_plus >> 2;
-      hi[a] = ((base_minus + 1) >> 2) + 1;
-    }
-    if (bad) {
-      valid = false;
-      hi[0] = -1;
-    }
-  }
-  // Warp dedupe: lanes with identical boxes mark once.
-  uint64_t boxkey = valid ? ((uint64_t(uint32_t(lo[0]) & 0xfff) << 48) | (uint64_t(uint32_t(lo[1]) & 0xfff) << 36) |
-                             (uint64_t(uint32_t(lo[2]) & 0xfff) << 24) | (uint64_t(uint32_t(hi[0]) & 0xff) << 16) |
-                             (uint64_t(uint32_t(hi[1]) & 0xff) << 8) | uint64_t(uint32_t(hi[2]) & 0xff))
-                          : ~0ull;
-  uint32_t peers = __match_any_sync(0xffffffffu, boxkey);
-  bool leader = (__ffs(peers) - 1) == int(threadIdx.x & 31);
-  if (!valid || !leader) return;
-  for (int bi = lo[0]; bi <= hi[0]; ++bi)
-    for (int bj = lo[1]; bj <= hi[1]; ++bj)
-      for (int bk = lo[2]; bk <= hi[2]; ++bk)
-        if (bi >= 0 && bj >= 0 && bk >= 0 && bi < D && bj < D && bk < D)
-          flags[(int64_t(bi) * D + bj) * D + bk] = 1u;
-}
-
-// K3b: directory from the exclusive scan of flags (in place in dir), active
-// list in ascending directory order, flags reset for the next substep.
-__global__ void compact_kernel(uint32_t* __restrict__ flags, int32_t* __restrict__ dir,
-                               uint32_t* __restrict__ active, uint64_t nd, uint32_t cap,
-                               DevStatus* st) {
-  uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (d >= nd) return;
-  uint32_t f = flags[d];
-  uint32_t s = static_cast<uint32_t>(dir[d]);
-  if (f) {
-    if (s < cap) {
-      active[s] = static_cast<uint32_t>(d);
-    } else {
-      st->overflow = 1u;
-    }
-    flags[d] = 0u;
-  } else {
-    dir[d] = -1;
-  }
-  if (d == nd - 1) st->n_active = s + f;
-}
-
-// K4: clear the active part of the pool (grid.hpp:148-151).
-template <typename T>
-__global__ void clear_kernel(T* __restrict__ pool, const DevStatus* st, uint32_t cap) {
-  uint32_t na = st->n_active;
-  if (na > cap) na = cap;
-  uint64_t total = uint64_t(na) * kBlockVals;
-  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
-       k += uint64_t(gridDim.x) * blockDim.x)
-    pool[k] = T(0);
-}
-
-__device__ __forceinline__ void red_add(double* a, double v) { atomicAdd(a, v); }
-__device__ __forceinline__ void red_add(float* a, float v) { atomicAdd(a, v); }
-
-// K5: P2G (scatter_all, simulation.hpp:279-337; scatter_one, transfer.hpp:235-283;
-// MLS force scatter, transfer.hpp:335-369).  One thread per sorted particle,
-// 16 nodes x 4 values into the block pool.
-template <typename T, int SCHEME>
-__global__ void __launch_bounds__(128) p2g_kernel(PState<T> cur, const uint32_t* __restrict__ perm,
-                                                  StepConst<T> c, const int32_t* __restrict__ dir,
-                                                  T* __restrict__ pool, uint32_t cap, DevStatus* st,
-                                                  int step) {
-  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= cur.n) return;
-  const uint32_t src = __ldg(perm + i);
-  const uint64_t n = cur.n;
-  const T x = __ldg(cur.f + kX * n + src), y = __ldg(cur.f + (kX + 1) * n + src),
-          z = __ldg(cur.f + (kX + 2) * n + src);
-  const T vx = __ldg(cur.f + kV * n + src), vy = __ldg(cur.f + (kV + 1) * n + src),
-          vz = __ldg(cur.f + (kV + 2) * n + src);
-  const T m = __ldg(cur.f + kMass * n + src);
-  const T vol0 = __ldg(cur.f + kVol * n + src);
-  const T J = __ldg(cur.f + kJ * n + src);
-  const uint32_t mi = __ldg(cur.mat + src);
-  const M3<T> F = load_m3(cur, kF, src);
-  M3<T> A;
-  int e = force_matrix(F, J, vol0, c.mats[mi < kMaxMaterials ? mi : 0], A);
-  if (e) {
-    record_error(st, step, kPhaseP2G, i, 0, e);
-    return;
-  }
-  const T dx = c.dx, dt = c.dt;
-  const Dual<T> ds = dual_stencil(x, y, z, dx);
-  M3<T> Cm;
-  if (SCHEME != kSchemePic) {
-    M3<T> Dm = apic_D(ds, dx), Di;
-    if (!apic_d_inverse(Dm, Di)) {
-      record_error(st, step, kPhaseP2G, i, 0, kErrNearSingularD);
-      return;
-    }
-    Cm = mul(load_m3(cur, kB, src), Di);
-  }
-  T Minv[4][4];
-  if (SCHEME == kSchemeMls) {
-    T Mm[4][4];
-    mls_moment(ds, dx, Mm);
-    if (!gauss_inverse4(Mm, Minv)) {
-      record_error(st, step, kPhaseP2G, i, 0, kErrSingularMls);
-      return;
-    }
-  }
-  const int D = c.D;
-#pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    const Axis<T>* ax = ds.ax[g];
-    const T wx[2] = {ax[0].w0, ax[0].w1}, wy[2] = {ax[1].w0, ax[1].w1}, wz[2] = {ax[2].w0, ax[2].w1};
-    const T gx[2] = {ax[0].g0, -ax[0].g0}, gy[2] = {ax[1].g0, -ax[1].g0}, gz[2] = {ax[2].g0, -ax[2].g0};
-    const T xx[2] = {ax[0].xi0, ax[0].xi0 + dx}, xy[2] = {ax[1].xi0, ax[1].xi0 + dx},
-            xz[2] = {ax[2].xi0, ax[2].xi0 + dx};
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int ni = ax[0].base + s, nj = ax[1].base + t, nk = ax[2].base + u;
-          const int32_t slot = dir_lookup(dir, D, ni >> 2, nj >> 2, nk >> 2);
-          if (slot < 0 || uint32_t(slot) >= cap) {
-            record_error(st, step, kPhaseP2G, i, 0, kErrInactive);
-            continue;
-          }
-          const T w = wx[s] * wy[t] * wz[u];
-          const T wm = w * m;
-          T mx = vx * wm, my = vy * wm, mz = vz * wm;
-          if (SCHEME != kSchemePic) {
-            const V3<T> cx = mul(Cm, V3<T>{xx[s], xy[t], xz[u]});
-            mx += cx.x * wm;
-            my += cx.y * wm;
-            mz += cx.z * wm;
-          }
-          if (SCHEME != kSchemeMls) {
-            const V3<T> gw = {gx[s] * wy[t] * wz[u], wx[s] * gy[t] * wz[u], wx[s] * wy[t] * gz[u]};
-            const V3<T> ag = mul(A, gw);
-            mx -= ag.x * dt;
-            my -= ag.y * dt;
-            mz -= ag.z * dt;
-          } else {
-            T q[4];
-            const T P[4] = {T(1), xx[s], xy[t], xz[u]};
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-              q[a] = Minv[a][0] * P[0] + Minv[a][1] * P[1] + Minv[a][2] * P[2] + Minv[a][3] * P[3];
-            const V3<T> ag = mul(A, V3<T>{w * q[1], w * q[2], w * q[3]});
-            mx -= ag.x * dt;
-            my -= ag.y * dt;
-            mz -= ag.z * dt;
-          }
-          T* nd = pool + node_off(slot, g, ni, nj, nk);
-          red_add(nd, wm);
-          red_add(nd + 64, mx);
-          red_add(nd + 128, my);
-          red_add(nd + 192, mz);
-        }
-  }
-}
-
-// K6: grid update on both grids (grid_update_block, transfer.hpp:419-440;
-// BoundaryCondition::contains/apply, grid.hpp:34-55).
-template <typename T>
-__global__ void grid_update_kernel(T* __restrict__ pool, const uint32_t* __restrict__ active,
-                                   const DevStatus* st, uint32_t cap, StepConst<T> c,
-                                   const BcParam<T>* __restrict__ bcs) {
-  uint32_t na = st->n_active;
-  if (na > cap) na = cap;
-  const uint64_t total = uint64_t(na) * 128;
-  const int D = c.D;
-  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
-       k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t slot = uint32_t(k >> 7);
-    const int g = int(k >> 6) & 1;
-    const int l = int(k & 63);
-    T* base = pool + uint64_t(slot) * kBlockVals + g * 256 + l;
-    const T mass = base[0];
-    if (mass > c.mass_eps) {
-      const T inv = T(1) / mass;
-      T v[3] = {base[64] * inv + c.gravity[0] * c.dt, base[128] * inv + c.gravity[1] * c.dt,
-                base[192] * inv + c.gravity[2] * c.dt};
-      if (c.n_boundaries > 0) {
-        const uint32_t d = __ldg(active + slot);
-        const int bz = int(d % uint32_t(D)), by = int((d / uint32_t(D)) % uint32_t(D)),
-                  bx = int(d / (uint32_t(D) * uint32_t(D)));
-        const T off = (g == 0 ? T(-0.25) : T(0.25)) * c.dx;
-        const T xp[3] = {T(bx * 4 + ((l >> 4) & 3)) * c.dx + off, T(by * 4 + ((l >> 2) & 3)) * c.dx + off,
-                         T(bz * 4 + (l & 3)) * c.dx + off};
-        for (int b = 0; b < c.n_boundaries; ++b) {
-          const BcParam<T>& bc = bcs[b];
-          if (!(xp[0] >= bc.lo[0] && xp[0] <= bc.hi[0] && xp[1] >= bc.lo[1] && xp[1] <= bc.hi[1] &&
-                xp[2] >= bc.lo[2] && xp[2] <= bc.hi[2]))
-            continue;
-          if (bc.kind == 0) {  // sticky: v0 + omega x (x - c)
-            const T r0 = xp[0] - bc.center[0], r1 = xp[1] - bc.center[1], r2 = xp[2] - bc.center[2];
-            v[0] = bc.velocity[0] + (bc.omega[1] * r2 - bc.omega[2] * r1);
-            v[1] = bc.velocity[1] + (bc.omega[2] * r0 - bc.omega[0] * r2);
-            v[2] = bc.velocity[2] + (bc.omega[0] * r1 - bc.omega[1] * r0);
-          } else {
-            const T vn = v[0] * bc.normal[0] + v[1] * bc.normal[1] + v[2] * bc.normal[2];
-            if (bc.kind == 1 || vn < T(0)) {
-              v[0] -= bc.normal[0] * vn;
-              v[1] -= bc.normal[1] * vn;
-              v[2] -= bc.normal[2] * vn;
-            }
-          }
-        }
-      }
-      base[64] = v[0];
-      base[128] = v[1];
-      base[192] = v[2];
-    } else {
-      base[0] = T(0);
-      base[64] = T(0);
-      base[128] = T(0);
-      base[192] = T(0);
-    }
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ unsigned long long as_ordered_bits(T v) {
-  return static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(v)));
-}
-
-// K7: G2P gather + state update + advection + reductions
-// (gather_all, simulation.hpp:339-396; gather_one, transfer.hpp:465-510;
-// update_particle_state, transfer.hpp:594-627).  Reads cur at perm[i],
-// writes nxt at i (sorted order).
-template <typename T, int SCHEME>
-__global__ void __launch_bounds__(128) g2p_kernel(PState<T> cur, PState<T> nxt,
-                                                  const uint32_t* __restrict__ perm, StepConst<T> c,
-                                                  const int32_t* __restrict__ dir,
-                                                  const T* __restrict__ pool, uint32_t cap,
-                                                  DevStatus* st, int step) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool live = i < cur.n;
-  T s2 = T(0);
-  bool fluid = false;
-  T Jout = T(1);
-  uint32_t mi = 0;
-  bool bad = false;
-  if (live) {
-    const uint32_t src = __ldg(perm + i);
-    const uint64_t n = cur.n;
-    T x = __ldg(cur.f + kX * n + src), y = __ldg(cur.f + (kX + 1) * n + src),
-      z = __ldg(cur.f + (kX + 2) * n + src);
-    const T m = __ldg(cur.f + kMass * n + src);
-    const T vol0 = __ldg(cur.f + kVol * n + src);
-    T J = __ldg(cur.f + kJ * n + src);
-    mi = __ldg(cur.mat + src);
-    const MatParam<T>& mp = c.mats[mi < kMaxMaterials ? mi : 0];
-    const T dx = c.dx, dt = c.dt;
-    const Dual<T> ds = dual_stencil(x, y, z, dx);
-    // gather: v = 1/2 sum w v~, B = 1/2 sum w v~ xi^T, gradv = 1/2 sum v~ gw^T
-    T v[3] = {T(0), T(0), T(0)};
-    M3<T> Bn, G;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        Bn.a[a][b] = T(0);
-        G.a[a][b] = T(0);
-      }
-    const int D = c.D;
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      const Axis<T>* ax = ds.ax[g];
-      const T wx[2] = {ax[0].w0, ax[0].w1}, wy[2] = {ax[1].w0, ax[1].w1}, wz[2] = {ax[2].w0, ax[2].w1};
-      const T gx[2] = {ax[0].g0, -ax[0].g0}, gy[2] = {ax[1].g0, -ax[1].g0}, gz[2] = {ax[2].g0, -ax[2].g0};
-      const T xx[2] = {ax[0].xi0, ax[0].xi0 + dx}, xy[2] = {ax[1].xi0, ax[1].xi0 + dx},
-              xz[2] = {ax[2].xi0, ax[2].xi0 + dx};
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int ni = ax[0].base + s, nj = ax[1].base + t, nk = ax[2].base + u;
-            const int32_t slot = dir_lookup(dir, D, ni >> 2, nj >> 2, nk >> 2);
-            if (slot < 0 || uint32_t(slot) >= cap) {
-              record_error(st, step, kPhaseG2P, i, 0, kErrInactive);
-              continue;
-            }
-            const T* nd = pool + node_off(slot, g, ni, nj, nk);
-            const T vn[3] = {__ldg(nd + 64), __ldg(nd + 128), __ldg(nd + 192)};
-            const T hw = T(0.5) * (wx[s] * wy[t] * wz[u]);
-            const T xi[3] = {xx[s], xy[t], xz[u]};
-            const T gw[3] = {gx[s] * wy[t] * wz[u], wx[s] * gy[t] * wz[u], wx[s] * wy[t] * gz[u]};
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              v[a] += vn[a] * hw;
-#pragma unroll
-              for (int b = 0; b < 3; ++b) {
-                Bn.a[a][b] += hw * vn[a] * xi[b];
-                G.a[a][b] += T(0.5) * vn[a] * gw[b];
-              }
-            }
-          }
-    }
-    // update_particle_state
-    M3<T> L = G;
-    if (SCHEME == kSchemeMls) {
-      M3<T> Dm = apic_D(ds, dx), Di;
-      if (!apic_d_inverse(Dm, Di)) {
-        record_error(st, step, kPhaseG2P, i, 0, kErrNearSingularD);
-        bad = true;
-      }
-      L = mul(Bn, Di);
-    }
-    M3<T> Bout = SCHEME == kSchemePic ? load_m3(cur, kB, src) : Bn;
-    M3<T> Fout = load_m3(cur, kF, src);
-    if (mp.model == kModelFluid) {
-      fluid = true;
-      if (mp.viscosity > T(0) && SCHEME != kSchemePic) {
-        const T f = dexp(-mp.viscosity * dt / (mp.density * dx * dx));
-        const T tb = trace(Bout) / T(3);
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) Bout.a[a][b] = (a == b ? tb : T(0)) + (Bout.a[a][b] - (a == b ? tb : T(0))) * f;
-      }
-      J *= T(1) + dt * trace(L);
-      if (!(J > T(0))) {
-        record_error(st, step, kPhaseG2P, i, 0, kErrFluidJ);
-        bad = true;
-      }
-    } else {
-      M3<T> Ld;
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) Ld.a[a][b] = (a == b ? T(1) : T(0)) + L.a[a][b] * dt;
-      M3<T> Fn = mul(Ld, Fout);
-      if (c.clamp_singular) clamp_singular_values(Fn, c.clamp_floor);
-      if (mp.model == kModelDP) {
-        int e = return_map_dp(Fn, mp.dp_alpha, mp.mu, mp.lambda);
-        if (e) {
-          record_error(st, step, kPhaseG2P, i, 0, e);
-          bad = true;
-        }
-      } else if (!(det(Fn) > T(0))) {
-        record_error(st, step, kPhaseG2P, i, 0, kErrFInverted);
-        bad = true;
-      }
-      Fout = Fn;
-    }
-    x += v[0] * dt;
-    y += v[1] * dt;
-    z += v[2] * dt;
-    // write the new state in sorted order
-    nxt.f[kX * n + i] = x;
-    nxt.f[(kX + 1) * n + i] = y;
-    nxt.f[(kX + 2) * n + i] = z;
-    nxt.f[kV * n + i] = v[0];
-    nxt.f[(kV + 1) * n + i] = v[1];
-    nxt.f[(kV + 2) * n + i] = v[2];
-    store_m3(nxt, kF, i, Fout);
-    store_m3(nxt, kB, i, Bout);
-    nxt.f[kJ * n + i] = J;
-    nxt.f[kMass * n + i] = m;
-    nxt.f[kVol * n + i] = vol0;
-    nxt.mat[i] = mi;
-    s2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
-    Jout = J;
-    if (!dfinite(s2) || !dfinite(x * x + y * y + z * z)) atomicOr(&st->nonfinite, 1u);
-    (void)bad;
-  }
-  // vmax^2 reduction (NaN never wins, like std::max(vm, s2)).
-  T vm = (s2 > T(0)) ? s2 : T(0);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    T other = __shfl_xor_sync(0xffffffffu, vm, o);
-    vm = (vm < other) ? other : vm;
-  }
-  __shared__ T wmax[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) wmax[wid] = vm;
-  __syncthreads();
-  if (wid == 0) {
-    T b = lane < int(blockDim.x >> 5) ? wmax[lane] : T(0);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      T other = __shfl_xor_sync(0xffffffffu, b, o);
-      b = (b < other) ? other : b;
-    }
-    if (lane == 0 && b > T(0)) atomicMax(&st->vmax2, as_ordered_bits(b));
-  }
-  // per-material min J over fluid particles
-  uint32_t todo = __ballot_sync(0xffffffffu, live && fluid);
-  while (todo) {
-    const uint32_t lead_mat = __shfl_sync(0xffffffffu, mi, __ffs(todo) - 1);
-    const bool mine = live && fluid && mi == lead_mat;
-    T jv = mine ? Jout : T(INFINITY);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      T other = __shfl_xor_sync(0xffffffffu, jv, o);
-      jv = (other < jv) ? other : jv;
-    }
-    if (lane == __ffs(todo) - 1 && lead_mat < kMaxMaterials && jv > T(0))
-      atomicMin(&st->minj[lead_mat], as_ordered_bits(jv));
-    todo &= ~__ballot_sync(0xffffffffu, mine);
-  }
-}
-
-// Status reset before a substep.
-__global__ void status_reset_kernel(DevStatus* st, int reset_err) {
-  if (threadIdx.x == 0) {
-    if (reset_err) st->err = ~0ull;
-    st->vmax2 = 0ull;
-    st->nonfinite = 0u;
-    st->n_active = 0u;
-    st->overflow = 0u;
-  }
-  if (threadIdx.x < kMaxMaterials) st->minj[threadIdx.x] = 0x7ff0000000000000ull;  // +inf
-}
-
-// AoS <-> SoA transposes for the C-ABI (Particle<T> layout, transfer.hpp:19-28).
-// One thread per (particle, field) word so both sides stay coalesced enough.
-template <typename T>
-__global__ void aos_to_soa_kernel(const T* __restrict__ aos, PState<T> p) {
-  constexpr int W = kNumFields + 1;  // 27 fields + material word(s)
-  const uint64_t total = p.n * W;
-  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
-       k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t i = k / W;
-    const int f = int(k - i * W);
-    if (f < kNumFields)
-      p.f[uint64_t(f) * p.n + i] = aos[k];
-    else
-      p.mat[i] = *reinterpret_cast<const uint32_t*>(aos + k);
-  }
-}
-
-template <typename T>
-__global__ void soa_to_aos_kernel(PState<T> p, T* __restrict__ aos) {
-  constexpr int W = kNumFields + 1;
-  const uint64_t total = p.n * W;
-  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
-       k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t i = k / W;
-    const int f = int(k - i * W);
-    if (f < kNumFields) {
-      aos[k] = p.f[uint64_t(f) * p.n + i];
-    } else {
-      T word = T(0);
-      *reinterpret_cast<uint32_t*>(&word) = p.mat[i];
-      aos[k] = word;
-    }
-  }
-}
-
-// Per-particle dual-stencil bases (binning parity hook).
-template <typename T>
-__global__ void bases_kernel(PState<T> p, T dx, int32_t* __restrict__ out) {
-  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= p.n) return;
-#pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    const T kq = g == 0 ? T(-0.25) : T(0.25);
-#pragma unroll
-    for (int a = 0; a < 3; ++a) out[(i * 2 + g) * 3 + a] = axis_base(p.f[uint64_t(kX + a) * p.n + i], dx, kq);
-  }
-}
-
-// Grid pool -> reference Block::nodes order for the grid facade.
-template <typename T>
-__global__ void grid_export_kernel(const T* __restrict__ pool, const uint32_t* __restrict__ active,
-                                   uint64_t nb, int D, int32_t* __restrict__ coords,
-                                   double* __restrict__ nodes) {
-  const uint64_t total = nb * 128;
-  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
-       k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t b = k >> 7;
-    const int nn = int(k & 127);
-    const int g = nn >> 6, l = nn & 63;
-    const T* base = pool + b * kBlockVals + g * 256 + l;
-    if (nodes) {
-      double* o = nodes + k * 4;
-      o[0] = double(base[0]);
-      o[1] = double(base[64]);
-      o[2] = double(base[128]);
-      o[3] = double(base[192]);
-    }
-    if (coords && nn == 0) {
-      const uint32_t d = active[b];
-      coords[b * 3 + 2] = int(d % uint32_t(D));
-      coords[b * 3 + 1] = int((d / uint32_t(D)) % uint32_t(D));
-      coords[b * 3 + 0] = int(d / (uint32_t(D) * uint32_t(D)));
-    }
-  }
-}
-
-// compute_diagnostics on the device (simulation.hpp:55-69): 11 sums/max.
-template <typename T>
-__global__ void diagnostics_kernel(PState<T> p, double* __restrict__ acc /* 10 sums */,
-                                   unsigned long long* __restrict__ vmax_bits) {
-  double s[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  double vm = 0;
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const double m = double(p.f[kMass * p.n + i]);
-    const double x[3] = {double(p.f[kX * p.n + i]), double(p.f[(kX + 1) * p.n + i]), double(p.f[(kX + 2) * p.n + i])};
-    const double v[3] = {double(p.f[kV * p.n + i]), double(p.f[(kV + 1) * p.n + i]), double(p.f[(kV + 2) * p.n + i])};
-    s[0] += v[0] * m; s[1] += v[1] * m; s[2] += v[2] * m;
-    s[3] += (x[1] * v[2] - x[2] * v[1]) * m;
-    s[4] += (x[2] * v[0] - x[0] * v[2]) * m;
-    s[5] += (x[0] * v[1] - x[1] * v[0]) * m;
-    s[6] += v[0]; s[7] += v[1]; s[8] += v[2];
-    const double n2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
-    s[9] += 0.5 * m * n2;
-    vm = vm < n2 ? n2 : vm;
-  }
-#pragma unroll
-  for (int k = 0; k < 10; ++k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double other = __shfl_xor_sync(0xffffffffu, vm, o);
-    vm = vm < other ? other : vm;
-  }
-  if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int k = 0; k < 10; ++k) atomicAdd(acc + k, s[k]);
-    atomicMax(vmax_bits, static_cast<unsigned long long>(__double_as_longlong(vm)));
-  }
-}
 
 }  // namespace ckg

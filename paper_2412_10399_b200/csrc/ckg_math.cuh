@@ -230,8 +230,11 @@ __device__ __forceinline__ void sym_eigen3(M3<T> A, V3<T>& w_out, M3<T>& V_out) 
 }
 
 // svd3 (math.hpp:249-292): F = U diag(sigma) V^T, det U = det V = +1.
+// Kept out of line: it is called from several cold-or-warm sites (polar
+// fallback, Drucker-Prager stress and return map, singular-value clamp) and
+// inlining each copy would blow the instruction cache of the hot kernels.
 template <typename T>
-__device__ __forceinline__ void svd3(const M3<T>& F, M3<T>& U, V3<T>& sigma, M3<T>& V) {
+__device__ __noinline__ void svd3(const M3<T>& F, M3<T>& U, V3<T>& sigma, M3<T>& V) {
   M3<T> FtF;
 #pragma unroll
   for (int i = 0; i < 3; ++i)

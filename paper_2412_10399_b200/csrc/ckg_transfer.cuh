@@ -1,0 +1,783 @@
+// ckg_transfer.cuh — block-tiled P2G, grid update and G2P kernels (sm_100a).
+//
+// Both transfer kernels are persistent: each CTA pulls the next active block
+// (directory order) from a device work counter and processes that block's
+// particle segment [seg_begin, seg_end) of the sorted order.
+//
+// Tile geometry: a particle whose sort key is block b has
+// stencil bases inside [4b-1, 4b+4] on the +1 grid and [4b, 4b+4] on the -1
+// grid (per axis, nodes up to +1 further), so a 6^3-node tile per grid with
+// origin 4b (grid 0, k=-1) / 4b-1 (grid 1, k=+1) holds the whole footprint.
+// The rare particles outside it (multiply/divide rounding disagreement at
+// non-power-of-two dx) take a direct global path.
+//
+// P2G (scatter_one, transfer.hpp:235-283): each warp accumulates into a
+// private FP64 tile in shared memory (no shared-memory FP64 atomics — on
+// sm_100a those are CAS loops), lanes that hit the same base cell are
+// serialised by match_any rank layers, and the CTA flushes the summed tile
+// once per block with coalesced global REDs (native REDG.ADD.F64).
+//
+// G2P (gather_one + update_particle_state, transfer.hpp:465-627): the CTA
+// stages the block's 2 x 6^3 nodal velocities in shared memory and every
+// particle gathers its 16 nodes with a sum-factorised (separable) contraction.
+#pragma once
+
+#include <type_traits>
+
+#include "ckg_kernels.cuh"
+#include "ckg_scan.cuh"
+
+namespace ckg {
+
+constexpr int kTileN = 6;
+constexpr int kTileNodes = kTileN * kTileN * kTileN;  // 216
+constexpr int kTileVals = 2 * 4 * kTileNodes;         // 1728 (m, px, py, pz on both grids)
+constexpr int kVelVals = 2 * 3 * kTileNodes;          // 1296
+constexpr int kXferThreads = 256;
+constexpr int kXferWarps = kXferThreads / 32;
+constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full lattice block)
+
+template <typename T>
+constexpr size_t p2g_smem_bytes() {
+  return size_t(kXferWarps) * kTileVals * sizeof(T);
+}
+
+__device__ __forceinline__ void decode_key(uint32_t key, int D, int& bx, int& by, int& bz) {
+  bz = int(key % uint32_t(D));
+  by = int((key / uint32_t(D)) % uint32_t(D));
+  bx = int(key / (uint32_t(D) * uint32_t(D)));
+}
+
+// Global pool offset of node (gi, gj, gk) on grid g through the block's 3^3
+// neighbour slots (nbr[(ox*3+oy)*3+oz], o = node block - key block + 1).
+__device__ __forceinline__ int64_t nbr_offset(const int32_t* nbr, int g, int gi, int gj, int gk, int bx, int by,
+                                              int bz) {
+  const int ox = (gi >> 2) - bx + 1, oy = (gj >> 2) - by + 1, oz = (gk >> 2) - bz + 1;
+  if (ox < 0 || oy < 0 || oz < 0 || ox > 2 || oy > 2 || oz > 2) return -1;
+  const int32_t slot = nbr[(ox * 3 + oy) * 3 + oz];
+  if (slot < 0) return -1;
+  return int64_t(slot) * kBlockVals + g * 256 + (((gi & 3) << 4) | ((gj & 3) << 2) | (gk & 3));
+}
+
+template <typename T, int SCHEME>
+__global__ void __launch_bounds__(kXferThreads, 2)
+    p2g_tile_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
+                    const int32_t* __restrict__ dir, const uint32_t* __restrict__ active,
+                    const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_end,
+                    T* __restrict__ pool, uint32_t cap, DevStatus* st, int step) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tiles = reinterpret_cast<T*>(smem_raw);
+  __shared__ int32_t nbr[27];
+  __shared__ uint32_t s_item;
+  __shared__ uint32_t cls_cnt[8], cls_off[8];
+  __shared__ uint16_t cls_list[kP2GChunk];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T* wt = tiles + warp * kTileVals;
+  for (int e = tid; e < kXferWarps * kTileVals; e += kXferThreads) tiles[e] = T(0);
+  const uint32_t na = min(st->n_active, cap);
+  const uint32_t lt = lanemask_lt();
+  const int D = c.D;
+  const T dx = c.dx, dt = c.dt;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_item = atomicAdd(&st->work[0], 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    if (item >= na) break;
+    const uint32_t key = active[item];
+    const uint32_t s0 = seg_begin[key], s1 = seg_end[key];
+    if (s1 <= s0) continue;
+    int bx, by, bz;
+    decode_key(key, D, bx, by, bz);
+    if (tid < 27) nbr[tid] = dir_lookup(dir, D, bx - 1 + tid / 9, by - 1 + (tid / 3) % 3, bz - 1 + tid % 3);
+    __syncthreads();
+    for (uint32_t cb = s0; cb < s1; cb += kP2GChunk) {
+      // ---- bin the chunk by sub-octant class (frac(x/dx - 1/4) >= 1/2 per
+      // axis): particles of one class have distinct -1 and +1 grid bases as
+      // soon as their +1 cells differ, so warp w scatters class w with (for
+      // lattice-like layouts) a single rank layer per grid.
+      const uint32_t len = min(uint32_t(kP2GChunk), s1 - cb);
+      if (tid < 8) cls_cnt[tid] = 0;
+      __syncthreads();
+      uint32_t myq[kP2GChunk / kXferThreads], myslot[kP2GChunk / kXferThreads];
+#pragma unroll
+      for (int r = 0; r < kP2GChunk / kXferThreads; ++r) {
+        const uint32_t j = tid + r * kXferThreads;
+        if (j < len) {
+          const uint32_t src = __ldg(perm + cb + j);
+          uint32_t q = 0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const T sa = sub_rn(over_dx(__ldg(cur.f + uint64_t(kX + a) * cur.n + src), dx, c.inv_dx, c.pow2), T(0.25));
+            q |= ((sa - dfloor(sa)) >= T(0.5) ? 1u : 0u) << a;
+          }
+          myq[r] = q;
+          myslot[r] = atomicAdd(&cls_cnt[q], 1u);
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          cls_off[q] = run;
+          run += cls_cnt[q];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kP2GChunk / kXferThreads; ++r) {
+        const uint32_t j = tid + r * kXferThreads;
+        if (j < len) cls_list[cls_off[myq[r]] + myslot[r]] = uint16_t(j);
+      }
+      __syncthreads();
+      const uint32_t my_cnt = cls_cnt[warp], my_off = cls_off[warp];
+      for (uint32_t rb = 0; rb < my_cnt; rb += 32) {
+      const bool in_round = rb + lane < my_cnt;
+      const uint32_t i = cb + (in_round ? uint32_t(cls_list[my_off + rb + lane]) : 0u);
+      bool valid = in_round;
+      // ---- per-particle state and stress (force_matrix, transfer.hpp:183-216)
+      T x = 0, y = 0, z = 0, m = 0;
+      T mv[3] = {0, 0, 0};
+      M3<T> Ap, Q;  // Ap = dt * V0 * tau, Q = m * C
+      T Minv[4][4];
+      Dual<T> ds;
+      if (valid) {
+        const uint32_t src = __ldg(perm + i);
+        const uint64_t n = cur.n;
+        x = __ldg(cur.f + kX * n + src);
+        y = __ldg(cur.f + (kX + 1) * n + src);
+        z = __ldg(cur.f + (kX + 2) * n + src);
+        m = __ldg(cur.f + kMass * n + src);
+        mv[0] = m * __ldg(cur.f + kV * n + src);
+        mv[1] = m * __ldg(cur.f + (kV + 1) * n + src);
+        mv[2] = m * __ldg(cur.f + (kV + 2) * n + src);
+        const T vol0 = __ldg(cur.f + kVol * n + src);
+        const T J = __ldg(cur.f + kJ * n + src);
+        const uint32_t mi = __ldg(cur.mat + src);
+        M3<T> A;
+        const int e = force_matrix(load_m3(cur, kF, src), J, vol0, c.mats[mi < kMaxMaterials ? mi : 0], A);
+        if (e) {
+          record_error(st, step, kPhaseP2G, i, 0, e);
+          valid = false;
+        }
+        Ap = scale(dt, A);
+        ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
+        if (SCHEME != kSchemePic) {
+          M3<T> Di;
+          if (!apic_d_inverse(apic_D(ds, dx), Di)) {
+            record_error(st, step, kPhaseP2G, i, 0, kErrNearSingularD);
+            valid = false;
+          }
+          Q = scale(m, mul(load_m3(cur, kB, src), Di));  // m * B D^-1
+        }
+        if (SCHEME == kSchemeMls) {
+          T Mm[4][4];
+          mls_moment(ds, dx, Mm);
+          if (!gauss_inverse4(Mm, Minv)) {
+            record_error(st, step, kPhaseP2G, i, 0, kErrSingularMls);
+            valid = false;
+          }
+        }
+      }
+      // ---- scatter, grid by grid
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const Axis<T>* ax = ds.ax[g];
+        const int lx = ax[0].base - (4 * bx - g), ly = ax[1].base - (4 * by - g), lz = ax[2].base - (4 * bz - g);
+        const bool in_tile = valid && lx >= 0 && ly >= 0 && lz >= 0 && lx <= kTileN - 2 && ly <= kTileN - 2 &&
+                             lz <= kTileN - 2;
+        const uint32_t cell = in_tile ? uint32_t((lx * kTileN + ly) * kTileN + lz) : (1024u + lane);
+        const uint32_t peers = __match_any_sync(0xffffffffu, cell);
+        const uint32_t rank = __popc(peers & lt);
+        const uint32_t maxrank = __reduce_max_sync(0xffffffffu, rank);
+        const T wx[2] = {ax[0].w0, ax[0].w1}, wy[2] = {ax[1].w0, ax[1].w1}, wz[2] = {ax[2].w0, ax[2].w1};
+        const T gx[2] = {ax[0].g0, -ax[0].g0}, gy[2] = {ax[1].g0, -ax[1].g0}, gz[2] = {ax[2].g0, -ax[2].g0};
+        // node momentum base b_stu = m v + Q xi_stu = u0 + dx (s Qx + t Qy + u Qz)
+        T u0[3] = {mv[0], mv[1], mv[2]};
+        T dQ[3][3];
+        if (SCHEME != kSchemePic) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            u0[a] += Q.a[a][0] * ax[0].xi0 + Q.a[a][1] * ax[1].xi0 + Q.a[a][2] * ax[2].xi0;
+#pragma unroll
+            for (int b = 0; b < 3; ++b) dQ[a][b] = Q.a[a][b] * dx;
+          }
+        }
+        // Node contribution (m w, w b - A' grad w) or, for MLS, the force
+        // through grad Phi = w M^-1 P(xi) (transfer.hpp:335-369).
+        auto contrib = [&](int s, int t, int u, T (&o)[4]) {
+          const T wyz = wy[t] * wz[u];
+          const T w = wx[s] * wyz;
+          T gw0, gw1, gw2;
+          if (SCHEME != kSchemeMls) {
+            gw0 = gx[s] * wyz;
+            gw1 = wx[s] * (gy[t] * wz[u]);
+            gw2 = wx[s] * (wy[t] * gz[u]);
+          } else {
+            const T P1 = ax[0].xi0 + (s ? dx : T(0)), P2 = ax[1].xi0 + (t ? dx : T(0)),
+                    P3 = ax[2].xi0 + (u ? dx : T(0));
+            gw0 = w * (Minv[1][0] + Minv[1][1] * P1 + Minv[1][2] * P2 + Minv[1][3] * P3);
+            gw1 = w * (Minv[2][0] + Minv[2][1] * P1 + Minv[2][2] * P2 + Minv[2][3] * P3);
+            gw2 = w * (Minv[3][0] + Minv[3][1] * P1 + Minv[3][2] * P2 + Minv[3][3] * P3);
+          }
+          o[0] = w * m;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            T b = u0[a];
+            if (SCHEME != kSchemePic) {
+              if (s) b += dQ[a][0];
+              if (t) b += dQ[a][1];
+              if (u) b += dQ[a][2];
+            }
+            o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
+          }
+        };
+        T* p0 = wt + g * 4 * kTileNodes + (lx * kTileN + ly) * kTileN + lz;
+        if (maxrank == 0) {
+          // fast path: every lane owns a distinct base cell in this warp, so
+          // at a fixed node offset all lanes write distinct nodes
+          {
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+#pragma unroll
+              for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  T o[4];
+                  contrib(s, t, u, o);
+                  T* p = p0 + (s * kTileN + t) * kTileN + u;
+                  if (in_tile) {
+                  p[0] += o[0];
+                  p[kTileNodes] += o[1];
+                  p[2 * kTileNodes] += o[2];
+                  p[3 * kTileNodes] += o[3];
+                  }
+                  // node (s,t,u) of one lane can be node (0,0,0) of its
+                  // neighbour: order the read-modify-writes across lanes
+                  __syncwarp();
+                }
+          }
+        } else {
+          // shared base cells: serialise by rank layers (rolled loop)
+#pragma unroll 1
+          for (int nid = 0; nid < 8; ++nid) {
+            const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
+            T o[4];
+            contrib(s, t, u, o);
+            T* p = p0 + (s * kTileN + t) * kTileN + u;
+            for (uint32_t layer = 0; layer <= maxrank; ++layer) {
+              if (in_tile && rank == layer) {
+                p[0] += o[0];
+                p[kTileNodes] += o[1];
+                p[2 * kTileNodes] += o[2];
+                p[3 * kTileNodes] += o[3];
+              }
+              __syncwarp();
+            }
+          }
+        }
+        if (valid && !in_tile) {
+          // footprint outside the block tile: direct REDs through the directory
+#pragma unroll 1
+          for (int nid = 0; nid < 8; ++nid) {
+            const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
+            T o[4];
+            contrib(s, t, u, o);
+            const int gi = ax[0].base + s, gj = ax[1].base + t, gk = ax[2].base + u;
+            const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
+            if (slot < 0 || uint32_t(slot) >= cap) {
+              record_error(st, step, kPhaseP2G, i, 0, kErrInactive);
+            } else {
+              T* nd = pool + node_off(slot, g, gi, gj, gk);
+              atomicAdd(nd, o[0]);
+              atomicAdd(nd + 64, o[1]);
+              atomicAdd(nd + 128, o[2]);
+              atomicAdd(nd + 192, o[3]);
+            }
+          }
+        }
+      }
+      }  // rounds of this warp's class list
+      __syncthreads();
+    }
+    __syncthreads();
+    // ---- flush: sum the warp tiles, one REDG per non-zero node value
+    for (int e = tid; e < kTileVals; e += kXferThreads) {
+      T sum = T(0);
+#pragma unroll
+      for (int w = 0; w < kXferWarps; ++w) {
+        sum += tiles[w * kTileVals + e];
+        tiles[w * kTileVals + e] = T(0);
+      }
+      if (sum != T(0)) {
+        const int g = e / (4 * kTileNodes);
+        const int v = (e / kTileNodes) & 3;
+        const int node = e % kTileNodes;
+        const int gi = 4 * bx - g + node / (kTileN * kTileN);
+        const int gj = 4 * by - g + (node / kTileN) % kTileN;
+        const int gk = 4 * bz - g + node % kTileN;
+        const int64_t off = nbr_offset(nbr, g, gi, gj, gk, bx, by, bz);
+        if (off < 0 || uint64_t(off) >= uint64_t(cap) * kBlockVals)
+          record_error(st, step, kPhaseP2G, s0, 0, kErrInactive);
+        else
+          atomicAdd(pool + off + v * 64, sum);
+      }
+    }
+  }
+}
+
+// Grid update on both grids (grid_update_block, transfer.hpp:419-440;
+// BoundaryCondition::contains/apply, grid.hpp:34-55).
+template <typename T>
+__global__ void grid_update_kernel(T* __restrict__ pool, const uint32_t* __restrict__ active,
+                                   const DevStatus* st, uint32_t cap, StepConst<T> c,
+                                   const BcParam<T>* __restrict__ bcs) {
+  uint32_t na = st->n_active;
+  if (na > cap) na = cap;
+  const uint64_t total = uint64_t(na) * 128;
+  const int D = c.D;
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t slot = uint32_t(k >> 7);
+    const int g = int(k >> 6) & 1;
+    const int l = int(k & 63);
+    T* base = pool + uint64_t(slot) * kBlockVals + g * 256 + l;
+    const T mass = base[0];
+    if (mass > c.mass_eps) {
+      const T inv = T(1) / mass;
+      T v[3] = {base[64] * inv + c.gravity[0] * c.dt, base[128] * inv + c.gravity[1] * c.dt,
+                base[192] * inv + c.gravity[2] * c.dt};
+      if (c.n_boundaries > 0) {
+        int bx, by, bz;
+        decode_key(__ldg(active + slot), D, bx, by, bz);
+        const T off = (g == 0 ? T(-0.25) : T(0.25)) * c.dx;
+        const T xp[3] = {T(bx * 4 + ((l >> 4) & 3)) * c.dx + off, T(by * 4 + ((l >> 2) & 3)) * c.dx + off,
+                         T(bz * 4 + (l & 3)) * c.dx + off};
+        for (int b = 0; b < c.n_boundaries; ++b) {
+          const BcParam<T>& bc = bcs[b];
+          if (!(xp[0] >= bc.lo[0] && xp[0] <= bc.hi[0] && xp[1] >= bc.lo[1] && xp[1] <= bc.hi[1] &&
+                xp[2] >= bc.lo[2] && xp[2] <= bc.hi[2]))
+            continue;
+          if (bc.kind == 0) {  // sticky: v0 + omega x (x - c)
+            const T r0 = xp[0] - bc.center[0], r1 = xp[1] - bc.center[1], r2 = xp[2] - bc.center[2];
+            v[0] = bc.velocity[0] + (bc.omega[1] * r2 - bc.omega[2] * r1);
+            v[1] = bc.velocity[1] + (bc.omega[2] * r0 - bc.omega[0] * r2);
+            v[2] = bc.velocity[2] + (bc.omega[0] * r1 - bc.omega[1] * r0);
+          } else {
+            const T vn = v[0] * bc.normal[0] + v[1] * bc.normal[1] + v[2] * bc.normal[2];
+            if (bc.kind == 1 || vn < T(0)) {
+              v[0] -= bc.normal[0] * vn;
+              v[1] -= bc.normal[1] * vn;
+              v[2] -= bc.normal[2] * vn;
+            }
+          }
+        }
+      }
+      base[64] = v[0];
+      base[128] = v[1];
+      base[192] = v[2];
+    } else {
+      base[0] = T(0);
+      base[64] = T(0);
+      base[128] = T(0);
+      base[192] = T(0);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ unsigned long long as_ordered_bits(T v) {
+  return static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(v)));
+}
+
+// One grid's contribution to gather_one (transfer.hpp:465-510), separable
+// (sum-factorised over z, then y, then x).  V(s,t,u,c) yields the nodal
+// velocity component c of stencil node (s,t,u).
+template <typename T, typename VelFn>
+__device__ __forceinline__ void gather_grid(const Axis<T>* ax, T dx, VelFn V, T (&v)[3], M3<T>& Bm, M3<T>& G) {
+  const T wx0 = ax[0].w0, wx1 = ax[0].w1, wy0 = ax[1].w0, wy1 = ax[1].w1, wz0 = ax[2].w0, wz1 = ax[2].w1;
+  const T gx0 = ax[0].g0, gy0 = ax[1].g0, gz0 = ax[2].g0;
+  const T xx0 = ax[0].xi0, xx1 = ax[0].xi0 + dx, xy0 = ax[1].xi0, xy1 = ax[1].xi0 + dx;
+  const T xz0 = ax[2].xi0, xz1 = ax[2].xi0 + dx;
+#pragma unroll
+  for (int cc = 0; cc < 3; ++cc) {
+    T Y[2], Yg[2], Yz[2], Yx[2], Yzx[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      T Z[2], Zg[2], Zx[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const T a0 = V(s, t, 0, cc), a1 = V(s, t, 1, cc);
+        Z[t] = wz0 * a0 + wz1 * a1;
+        Zg[t] = gz0 * (a0 - a1);
+        Zx[t] = wz0 * xz0 * a0 + wz1 * xz1 * a1;
+      }
+      Y[s] = wy0 * Z[0] + wy1 * Z[1];
+      Yg[s] = gy0 * (Z[0] - Z[1]);
+      Yz[s] = wy0 * Zg[0] + wy1 * Zg[1];
+      Yx[s] = wy0 * xy0 * Z[0] + wy1 * xy1 * Z[1];
+      Yzx[s] = wy0 * Zx[0] + wy1 * Zx[1];
+    }
+    v[cc] += T(0.5) * (wx0 * Y[0] + wx1 * Y[1]);
+    G.a[cc][0] += T(0.5) * (gx0 * (Y[0] - Y[1]));
+    G.a[cc][1] += T(0.5) * (wx0 * Yg[0] + wx1 * Yg[1]);
+    G.a[cc][2] += T(0.5) * (wx0 * Yz[0] + wx1 * Yz[1]);
+    Bm.a[cc][0] += T(0.5) * (wx0 * xx0 * Y[0] + wx1 * xx1 * Y[1]);
+    Bm.a[cc][1] += T(0.5) * (wx0 * Yx[0] + wx1 * Yx[1]);
+    Bm.a[cc][2] += T(0.5) * (wx0 * Yzx[0] + wx1 * Yzx[1]);
+  }
+}
+
+template <typename T, int SCHEME>
+__global__ void __launch_bounds__(kXferThreads, 2)
+    g2p_tile_kernel(PState<T> cur, PState<T> nxt, const uint32_t* __restrict__ perm, StepConst<T> c,
+                    const int32_t* __restrict__ dir, const uint32_t* __restrict__ active,
+                    const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_end,
+                    const T* __restrict__ pool, uint32_t cap, DevStatus* st, int step) {
+  __shared__ T vt[kVelVals];
+  __shared__ int32_t nbr[27];
+  __shared__ uint32_t s_item;
+  __shared__ T wmax[kXferWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t na = min(st->n_active, cap);
+  const int D = c.D;
+  const T dx = c.dx, dt = c.dt;
+  T vmax2 = T(0);
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_item = atomicAdd(&st->work[1], 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    if (item >= na) break;
+    const uint32_t key = active[item];
+    const uint32_t s0 = seg_begin[key], s1 = seg_end[key];
+    if (s1 <= s0) continue;
+    int bx, by, bz;
+    decode_key(key, D, bx, by, bz);
+    if (tid < 27) nbr[tid] = dir_lookup(dir, D, bx - 1 + tid / 9, by - 1 + (tid / 3) % 3, bz - 1 + tid % 3);
+    __syncthreads();
+    // stage nodal velocities of both grids' 6^3 tiles
+    for (int e = tid; e < kVelVals; e += kXferThreads) {
+      const int g = e / (3 * kTileNodes);
+      const int cc = (e / kTileNodes) % 3;
+      const int node = e % kTileNodes;
+      const int gi = 4 * bx - g + node / (kTileN * kTileN);
+      const int gj = 4 * by - g + (node / kTileN) % kTileN;
+      const int gk = 4 * bz - g + node % kTileN;
+      const int64_t off = nbr_offset(nbr, g, gi, gj, gk, bx, by, bz);
+      vt[e] = (off >= 0 && uint64_t(off) < uint64_t(cap) * kBlockVals) ? __ldg(pool + off + (1 + cc) * 64) : T(0);
+    }
+    __syncthreads();
+    for (uint32_t cb = s0; cb < s1; cb += kXferThreads) {
+      const uint32_t i = cb + tid;
+      const bool live = i < s1;
+      bool fluid = false;
+      T Jout = T(1);
+      uint32_t mi = 0;
+      if (live) {
+        const uint32_t src = __ldg(perm + i);
+        const uint64_t n = cur.n;
+        T x = __ldg(cur.f + kX * n + src), y = __ldg(cur.f + (kX + 1) * n + src),
+          z = __ldg(cur.f + (kX + 2) * n + src);
+        T v[3] = {T(0), T(0), T(0)};
+        M3<T> Bn, G;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            Bn.a[a][b] = T(0);
+            G.a[a][b] = T(0);
+          }
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const T kq = g == 0 ? T(-0.25) : T(0.25);
+          Axis<T> ax[3] = {axis_pair(x, dx, c.inv_dx, c.pow2, kq), axis_pair(y, dx, c.inv_dx, c.pow2, kq),
+                           axis_pair(z, dx, c.inv_dx, c.pow2, kq)};
+          const int lx = ax[0].base - (4 * bx - g), ly = ax[1].base - (4 * by - g), lz = ax[2].base - (4 * bz - g);
+          const bool in_tile =
+              lx >= 0 && ly >= 0 && lz >= 0 && lx <= kTileN - 2 && ly <= kTileN - 2 && lz <= kTileN - 2;
+          if (in_tile) {
+            const T* vg = vt + g * 3 * kTileNodes + (lx * kTileN + ly) * kTileN + lz;
+            gather_grid<T>(
+                ax, dx,
+                [&](int s, int t, int u, int cc) { return vg[cc * kTileNodes + (s * kTileN + t) * kTileN + u]; },
+                v, Bn, G);
+          } else {
+            // rare: footprint outside the block tile -> stage the 8 nodes via
+            // the directory into the same registers layout
+            T V[2][2][2][3];
+#pragma unroll 1
+            for (int nid = 0; nid < 8; ++nid) {
+              const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
+              const int gi = ax[0].base + s, gj = ax[1].base + t, gk = ax[2].base + u;
+              const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
+              T a0 = T(0), a1 = T(0), a2 = T(0);
+              if (slot < 0 || uint32_t(slot) >= cap) {
+                record_error(st, step, kPhaseG2P, i, 0, kErrInactive);
+              } else {
+                const T* nd = pool + node_off(slot, g, gi, gj, gk);
+                a0 = __ldg(nd + 64);
+                a1 = __ldg(nd + 128);
+                a2 = __ldg(nd + 192);
+              }
+#pragma unroll
+              for (int ss = 0; ss < 2; ++ss)
+#pragma unroll
+                for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+                  for (int uu = 0; uu < 2; ++uu)
+                    if (ss == s && tt == t && uu == u) {
+                      V[ss][tt][uu][0] = a0;
+                      V[ss][tt][uu][1] = a1;
+                      V[ss][tt][uu][2] = a2;
+                    }
+            }
+            gather_grid<T>(ax, dx, [&](int s, int t, int u, int cc) { return V[s][t][u][cc]; }, v, Bn, G);
+          }
+        }
+        const T m = __ldg(cur.f + kMass * n + src);
+        const T vol0 = __ldg(cur.f + kVol * n + src);
+        T J = __ldg(cur.f + kJ * n + src);
+        mi = __ldg(cur.mat + src);
+        const MatParam<T>& mp = c.mats[mi < kMaxMaterials ? mi : 0];
+        // update_particle_state (transfer.hpp:594-627)
+        M3<T> L = G;
+        if (SCHEME == kSchemeMls) {
+          const Dual<T> ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
+          M3<T> Di;
+          if (!apic_d_inverse(apic_D(ds, dx), Di)) record_error(st, step, kPhaseG2P, i, 0, kErrNearSingularD);
+          L = mul(Bn, Di);
+        }
+        M3<T> Bout = SCHEME == kSchemePic ? load_m3(cur, kB, src) : Bn;
+        M3<T> Fout = load_m3(cur, kF, src);
+        if (mp.model == kModelFluid) {
+          fluid = true;
+          if (mp.viscosity > T(0) && SCHEME != kSchemePic) {
+            const T f = dexp(-mp.viscosity * dt / (mp.density * dx * dx));
+            const T tb = trace(Bout) / T(3);
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int b = 0; b < 3; ++b)
+                Bout.a[a][b] = (a == b ? tb : T(0)) + (Bout.a[a][b] - (a == b ? tb : T(0))) * f;
+          }
+          J *= T(1) + dt * trace(L);
+          if (!(J > T(0))) record_error(st, step, kPhaseG2P, i, 0, kErrFluidJ);
+        } else {
+          M3<T> Ld;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) Ld.a[a][b] = (a == b ? T(1) : T(0)) + L.a[a][b] * dt;
+          M3<T> Fn = mul(Ld, Fout);
+          if (c.clamp_singular) clamp_singular_values(Fn, c.clamp_floor);
+          if (mp.model == kModelDP) {
+            const int e = return_map_dp(Fn, mp.dp_alpha, mp.mu, mp.lambda);
+            if (e) record_error(st, step, kPhaseG2P, i, 0, e);
+          } else if (!(det(Fn) > T(0))) {
+            record_error(st, step, kPhaseG2P, i, 0, kErrFInverted);
+          }
+          Fout = Fn;
+        }
+        x += v[0] * dt;
+        y += v[1] * dt;
+        z += v[2] * dt;
+        nxt.f[kX * n + i] = x;
+        nxt.f[(kX + 1) * n + i] = y;
+        nxt.f[(kX + 2) * n + i] = z;
+        nxt.f[kV * n + i] = v[0];
+        nxt.f[(kV + 1) * n + i] = v[1];
+        nxt.f[(kV + 2) * n + i] = v[2];
+        store_m3(nxt, kF, i, Fout);
+        store_m3(nxt, kB, i, Bout);
+        nxt.f[kJ * n + i] = J;
+        nxt.f[kMass * n + i] = m;
+        nxt.f[kVol * n + i] = vol0;
+        nxt.mat[i] = mi;
+        const T s2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+        Jout = J;
+        if (!dfinite(s2) || !dfinite(x * x + y * y + z * z)) atomicOr(&st->nonfinite, 1u);
+        if (s2 > vmax2) vmax2 = s2;  // NaN never wins (std::max(vm, s2) semantics)
+      }
+      // per-material min J over fluid particles (gather_all, simulation.hpp:371-372)
+      uint32_t todo = __ballot_sync(0xffffffffu, live && fluid);
+      while (todo) {
+        const int leader = __ffs(todo) - 1;
+        const uint32_t lead_mat = __shfl_sync(0xffffffffu, mi, leader);
+        const bool mine = live && fluid && mi == lead_mat;
+        T jv = mine ? Jout : T(INFINITY);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const T other = __shfl_xor_sync(0xffffffffu, jv, o);
+          jv = (other < jv) ? other : jv;
+        }
+        if (lane == leader && lead_mat < kMaxMaterials && jv > T(0))
+          atomicMin(&st->minj[lead_mat], as_ordered_bits(jv));
+        todo &= ~__ballot_sync(0xffffffffu, mine);
+      }
+    }
+  }
+  // vmax^2: warp, CTA, then one atomic per CTA
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T other = __shfl_xor_sync(0xffffffffu, vmax2, o);
+    vmax2 = (vmax2 < other) ? other : vmax2;
+  }
+  if (lane == 0) wmax[warp] = vmax2;
+  __syncthreads();
+  if (tid == 0) {
+    T b = T(0);
+    for (int w = 0; w < kXferWarps; ++w) b = (b < wmax[w]) ? wmax[w] : b;
+    if (b > T(0)) atomicMax(&st->vmax2, as_ordered_bits(b));
+  }
+}
+
+// K4: clear the active part of the pool (grid.hpp:148-151).
+template <typename T>
+__global__ void clear_kernel(T* __restrict__ pool, const DevStatus* st, uint32_t cap) {
+  uint32_t na = st->n_active;
+  if (na > cap) na = cap;
+  const uint64_t total = uint64_t(na) * kBlockVals / 2;  // in 16-byte words (double2 / float4-ish)
+  using W = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  W* p = reinterpret_cast<W*>(pool);
+  W zero;
+  zero.x = T(0);
+  zero.y = T(0);
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total; k += uint64_t(gridDim.x) * blockDim.x)
+    p[k] = zero;
+}
+
+// Status reset before a substep.
+__global__ void status_reset_kernel(DevStatus* st, int reset_err) {
+  if (threadIdx.x == 0) {
+    if (reset_err) st->err = ~0ull;
+    st->vmax2 = 0ull;
+    st->nonfinite = 0u;
+    st->n_active = 0u;
+    st->overflow = 0u;
+    st->inset_fail = 0u;
+  }
+  if (threadIdx.x < 4) st->work[threadIdx.x] = 0u;
+  if (threadIdx.x < kMaxMaterials) st->minj[threadIdx.x] = 0x7ff0000000000000ull;  // +inf
+}
+
+// AoS <-> SoA transposes for the C-ABI (Particle<T> layout, transfer.hpp:19-28).
+template <typename T>
+__global__ void aos_to_soa_kernel(const T* __restrict__ aos, PState<T> p) {
+  constexpr int W = kNumFields + 1;  // 27 fields + material word(s)
+  const uint64_t total = p.n * W;
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = k / W;
+    const int f = int(k - i * W);
+    if (f < kNumFields)
+      p.f[uint64_t(f) * p.n + i] = aos[k];
+    else
+      p.mat[i] = *reinterpret_cast<const uint32_t*>(aos + k);
+  }
+}
+
+template <typename T>
+__global__ void soa_to_aos_kernel(PState<T> p, T* __restrict__ aos) {
+  constexpr int W = kNumFields + 1;
+  const uint64_t total = p.n * W;
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = k / W;
+    const int f = int(k - i * W);
+    if (f < kNumFields) {
+      aos[k] = p.f[uint64_t(f) * p.n + i];
+    } else {
+      T word = T(0);
+      *reinterpret_cast<uint32_t*>(&word) = p.mat[i];
+      aos[k] = word;
+    }
+  }
+}
+
+// Per-particle dual-stencil bases (binning parity hook).
+template <typename T>
+__global__ void bases_kernel(PState<T> p, T dx, T inv_dx, int pow2, int32_t* __restrict__ out) {
+  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const T kq = g == 0 ? T(-0.25) : T(0.25);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      out[(i * 2 + g) * 3 + a] = axis_base(p.f[uint64_t(kX + a) * p.n + i], dx, inv_dx, pow2, kq);
+  }
+}
+
+// Grid pool -> reference Block::nodes order for the grid facade.
+template <typename T>
+__global__ void grid_export_kernel(const T* __restrict__ pool, const uint32_t* __restrict__ active,
+                                   uint64_t nb, int D, int32_t* __restrict__ coords,
+                                   double* __restrict__ nodes) {
+  const uint64_t total = nb * 128;
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t b = k >> 7;
+    const int nn = int(k & 127);
+    const int g = nn >> 6, l = nn & 63;
+    const T* base = pool + b * kBlockVals + g * 256 + l;
+    if (nodes) {
+      double* o = nodes + k * 4;
+      o[0] = double(base[0]);
+      o[1] = double(base[64]);
+      o[2] = double(base[128]);
+      o[3] = double(base[192]);
+    }
+    if (coords && nn == 0) {
+      int bx, by, bz;
+      decode_key(active[b], D, bx, by, bz);
+      coords[b * 3 + 0] = bx;
+      coords[b * 3 + 1] = by;
+      coords[b * 3 + 2] = bz;
+    }
+  }
+}
+
+// compute_diagnostics on the device (simulation.hpp:55-69).
+template <typename T>
+__global__ void diagnostics_kernel(PState<T> p, double* __restrict__ acc /* 10 sums */,
+                                   unsigned long long* __restrict__ vmax_bits) {
+  double s[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double vm = 0;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const double m = double(p.f[kMass * p.n + i]);
+    const double x[3] = {double(p.f[kX * p.n + i]), double(p.f[(kX + 1) * p.n + i]), double(p.f[(kX + 2) * p.n + i])};
+    const double v[3] = {double(p.f[kV * p.n + i]), double(p.f[(kV + 1) * p.n + i]), double(p.f[(kV + 2) * p.n + i])};
+    s[0] += v[0] * m;
+    s[1] += v[1] * m;
+    s[2] += v[2] * m;
+    s[3] += (x[1] * v[2] - x[2] * v[1]) * m;
+    s[4] += (x[2] * v[0] - x[0] * v[2]) * m;
+    s[5] += (x[0] * v[1] - x[1] * v[0]) * m;
+    s[6] += v[0];
+    s[7] += v[1];
+    s[8] += v[2];
+    const double n2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+    s[9] += 0.5 * m * n2;
+    vm = vm < n2 ? n2 : vm;
+  }
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double other = __shfl_xor_sync(0xffffffffu, vm, o);
+    vm = vm < other ? other : vm;
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) atomicAdd(acc + k, s[k]);
+    atomicMax(vmax_bits, static_cast<unsigned long long>(__double_as_longlong(vm)));
+  }
+}
+
+}  // namespace ckg
