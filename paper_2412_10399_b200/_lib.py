@@ -12,7 +12,7 @@ import os
 from . import abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libckmpm_b200.so")
+LIB_PATH = os.environ.get("CKMPM_B200_LIB") or os.path.join(_HERE, "libckmpm_b200.so")
 
 _lib = None
 

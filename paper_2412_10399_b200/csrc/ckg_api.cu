@@ -111,6 +111,8 @@ struct Context final : CtxBase {
   // particles (double-buffered SoA)
   T* fbuf[2] = {nullptr, nullptr};
   uint32_t* mbuf[2] = {nullptr, nullptr};
+  T* tbuf[2] = {nullptr, nullptr};  // stress cache (6 x n) per state buffer
+  bool stress_valid = false;
   int cur = 0;
   // staging for AoS transfers
   T* staging = nullptr;
@@ -196,6 +198,7 @@ struct Context final : CtxBase {
     for (int b = 0; b < 2; ++b) {
       dfree(fbuf[b]);
       dfree(mbuf[b]);
+      dfree(tbuf[b]);
     }
     dfree(staging);
     dfree(keys);
@@ -231,7 +234,7 @@ struct Context final : CtxBase {
     active = dalloc<uint32_t>(cap);
   }
 
-  PState<T> state(int b) const { return PState<T>{fbuf[b], mbuf[b], n}; }
+  PState<T> state(int b) const { return PState<T>{fbuf[b], mbuf[b], tbuf[b], n}; }
 
   template <int S>
   void occupancy_for() {
@@ -256,6 +259,7 @@ struct Context final : CtxBase {
     for (int b = 0; b < 2; ++b) {
       dfree(fbuf[b]);
       dfree(mbuf[b]);
+      dfree(tbuf[b]);
     }
     dfree(keys);
     dfree(vals);
@@ -267,6 +271,7 @@ struct Context final : CtxBase {
     for (int b = 0; b < 2; ++b) {
       fbuf[b] = dalloc<T>(uint64_t(kNumFields) * std::max<uint64_t>(n, 1));
       mbuf[b] = dalloc<uint32_t>(std::max<uint64_t>(n, 1));
+      tbuf[b] = dalloc<T>(6 * std::max<uint64_t>(n, 1));
     }
     keys = dalloc<uint32_t>(n);
     vals = dalloc<uint32_t>(n);
@@ -296,6 +301,7 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaGetLastError());
     CKG_CUDA(cudaStreamSynchronize(st));
     grid_valid = false;
+    stress_valid = false;
     return CKG_OK;
   }
 
@@ -410,6 +416,11 @@ struct Context final : CtxBase {
     if (stop_after >= CKG_PHASE_CLEAR) clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
     if (timed) CKG_CUDA(cudaEventRecord(ev[3], st));
     if (stop_after >= CKG_PHASE_P2G) {
+      if (!stress_valid) {
+        stress_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), c, dstat, step_idx);
+        stress_valid = true;
+        launches += 1;
+      }
       if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, step_idx);
       else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_p2g<kSchemeApic>(c, step_idx);
       else enqueue_p2g<kSchemeMls>(c, step_idx);

@@ -29,6 +29,7 @@ template <typename T>
 struct PState {
   T* f;           // kNumFields * n
   uint32_t* mat;  // n
+  T* tau;         // 6 * n: V0 * Kirchhoff stress of the current F (symmetric, xx xy xz yy yz zz)
   uint64_t n;
   __device__ __forceinline__ T& at(int k, uint64_t i) const { return f[uint64_t(k) * n + i]; }
 };
@@ -201,7 +202,7 @@ __device__ __forceinline__ int force_matrix(const M3<T>& F, T J, T vol0, const M
   if (m.model == kModelFC) {
     T dJ = det(F);
     if (!(dJ > T(0))) return kErrFcStress;
-    M3<T> R = polar_rotation(F);
+    M3<T> R = polar_rotation_fast(F);
     M3<T> FmR;
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -244,15 +245,35 @@ __device__ __forceinline__ int force_matrix(const M3<T>& F, T J, T vol0, const M
   return 0;
 }
 
-// return_map_drucker_prager (material.hpp:157-175).
+// V0 * Kirchhoff stress as 6 symmetric components (force_matrix,
+// transfer.hpp:183-216; tau is symmetric for all three models).
 template <typename T>
-__device__ __forceinline__ int return_map_dp(M3<T>& F, T alpha, T mu, T lambda) {
+__device__ __forceinline__ int stress_tau6(const M3<T>& F, T J, T vol0, const MatParam<T>& m, T (&t6)[6]) {
+  M3<T> A;
+  const int e = force_matrix(F, J, vol0, m, A);
+  t6[0] = A.a[0][0];
+  t6[1] = T(0.5) * (A.a[0][1] + A.a[1][0]);
+  t6[2] = T(0.5) * (A.a[0][2] + A.a[2][0]);
+  t6[3] = A.a[1][1];
+  t6[4] = T(0.5) * (A.a[1][2] + A.a[2][1]);
+  t6[5] = A.a[2][2];
+  return e;
+}
+
+// return_map_drucker_prager (material.hpp:157-175).  Also returns the
+// Kirchhoff stress of the projected F (what force_matrix would compute from
+// it at the next P2G, transfer.hpp:197-208): the projected F has singular
+// vectors U, V and singular values exp(eps), so tau = U diag(2 mu eps +
+// lambda tr eps) U^T with no second SVD.
+template <typename T>
+__device__ __forceinline__ int return_map_dp(M3<T>& F, T alpha, T mu, T lambda, T (&tau6)[6]) {
   if (!(det(F) > T(0))) return kErrReturnMap;
   M3<T> U, V;
   V3<T> sg;
   svd3(F, U, sg, V);
   T e0 = dlog(sg.x), e1 = dlog(sg.y), e2 = dlog(sg.z);
   T tr = e0 + e1 + e2;
+  bool project = true;
   if (tr > T(0)) {
     e0 = e1 = e2 = T(0);
   } else {
@@ -260,18 +281,31 @@ __device__ __forceinline__ int return_map_dp(M3<T>& F, T alpha, T mu, T lambda) 
     T d0 = e0 - t3, d1 = e1 - t3, d2 = e2 - t3;
     T dn = dsqrt(d0 * d0 + d1 * d1 + d2 * d2);
     T dgamma = dn + alpha * (T(3) * lambda + T(2) * mu) / (T(2) * mu) * tr;
-    if (dgamma <= T(0)) return 0;
-    T f = dgamma / dn;
-    e0 -= d0 * f;
-    e1 -= d1 * f;
-    e2 -= d2 * f;
+    if (dgamma <= T(0)) {
+      project = false;
+    } else {
+      T f = dgamma / dn;
+      e0 -= d0 * f;
+      e1 -= d1 * f;
+      e2 -= d2 * f;
+    }
   }
-  T s0 = dexp(e0), s1 = dexp(e1), s2 = dexp(e2);
+  if (project) {
+    T s0 = dexp(e0), s1 = dexp(e1), s2 = dexp(e2);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        F.a[i][j] = U.a[i][0] * s0 * V.a[j][0] + U.a[i][1] * s1 * V.a[j][1] + U.a[i][2] * s2 * V.a[j][2];
+  }
+  const T te = e0 + e1 + e2;
+  const T t0 = T(2) * mu * e0 + lambda * te, t1 = T(2) * mu * e1 + lambda * te, t2 = T(2) * mu * e2 + lambda * te;
+  int k = 0;
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
-      F.a[i][j] = U.a[i][0] * s0 * V.a[j][0] + U.a[i][1] * s1 * V.a[j][1] + U.a[i][2] * s2 * V.a[j][2];
+    for (int j = i; j < 3; ++j)
+      tau6[k++] = U.a[i][0] * t0 * U.a[j][0] + U.a[i][1] * t1 * U.a[j][1] + U.a[i][2] * t2 * U.a[j][2];
   return 0;
 }
 
@@ -300,16 +334,45 @@ struct Dual {
   Axis<T> ax[2][3];
 };
 
+// Both grids' slices of one axis from a single sincos: the -1 and +1 grid
+// fractions of the same coordinate differ by exactly 1/2 (mod 1) whenever
+// x/dx +- 1/4 round exactly (always, away from powers of two), and
+// sin/cos(2 pi (f + 1/2)) = -sin/cos(2 pi f).  Otherwise both are evaluated.
+template <typename T>
+__device__ __forceinline__ void axis_pair_dual(T x, T dx, T inv_dx, int pow2, Axis<T>& am, Axis<T>& ap) {
+  const T xd = over_dx(x, dx, inv_dx, pow2);
+  const T sm = sub_rn(xd, T(-0.25)), sp = sub_rn(xd, T(0.25));
+  const T fbm = dfloor(sm), fbp = dfloor(sp);
+  const T fm = sm - fbm, fp = sp - fbp;
+  T snp, csp, snm, csm;
+  sincos_2pi(fp, &snp, &csp);
+  const T d = fm - fp;
+  if (d == T(0.5) || d == T(-0.5)) {
+    snm = -snp;
+    csm = -csp;
+  } else {
+    sincos_2pi(fm, &snm, &csm);
+  }
+  snp *= TwoPi<T>::inv;
+  snm *= TwoPi<T>::inv;
+  am.base = static_cast<int>(fbm);
+  am.w0 = T(1) - fm + snm;
+  am.w1 = fm - snm;
+  am.g0 = (csm - T(1)) * inv_dx;
+  am.xi0 = (T(am.base) + T(-0.25)) * dx - x;
+  ap.base = static_cast<int>(fbp);
+  ap.w0 = T(1) - fp + snp;
+  ap.w1 = fp - snp;
+  ap.g0 = (csp - T(1)) * inv_dx;
+  ap.xi0 = (T(ap.base) + T(0.25)) * dx - x;
+}
+
 template <typename T>
 __device__ __forceinline__ Dual<T> dual_stencil(T x, T y, T z, T dx, T inv_dx, int pow2) {
   Dual<T> d;
-#pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    const T kq = g == 0 ? T(-0.25) : T(0.25);  // T(k) * T(0.25), k = -1 / +1
-    d.ax[g][0] = axis_pair(x, dx, inv_dx, pow2, kq);
-    d.ax[g][1] = axis_pair(y, dx, inv_dx, pow2, kq);
-    d.ax[g][2] = axis_pair(z, dx, inv_dx, pow2, kq);
-  }
+  axis_pair_dual(x, dx, inv_dx, pow2, d.ax[0][0], d.ax[1][0]);
+  axis_pair_dual(y, dx, inv_dx, pow2, d.ax[0][1], d.ax[1][1]);
+  axis_pair_dual(z, dx, inv_dx, pow2, d.ax[0][2], d.ax[1][2]);
   return d;
 }
 

@@ -29,11 +29,13 @@ template <>
 struct Lim<double> {
   static constexpr double eps = DBL_EPSILON;
   static constexpr double tiny = DBL_MIN;
+  static constexpr double ns_done = 1e-17;  // ||X^T X - I||^2 after which one more Newton-Schulz step is exact
 };
 template <>
 struct Lim<float> {
   static constexpr float eps = FLT_EPSILON;
   static constexpr float tiny = FLT_MIN;
+  static constexpr float ns_done = 1e-8f;
 };
 
 __device__ __forceinline__ double dsqrt(double x) { return sqrt(x); }
@@ -321,6 +323,43 @@ __device__ __forceinline__ M3<T> polar_rotation(const M3<T>& F) {
     prev = diff;
   }
   return R;
+}
+
+// Same rotation factor as polar_rotation, cheaper near rotations: the
+// Newton-Schulz iteration X <- X (3I - X^T X)/2 needs no inverse, square root
+// or division and converges quadratically to the orthogonal polar factor while
+// ||X^T X - I|| < 1 (every elastic state F = R(I + small strain)).  The final
+// factor agrees with the reference's scaled Newton result to round-off; far
+// from a rotation (or on non-convergence) the reference algorithm runs.
+template <typename T>
+__device__ __forceinline__ M3<T> polar_rotation_fast(const M3<T>& F) {
+  M3<T> X = F;
+  for (int it = 0; it < 8; ++it) {
+    // E = X^T X - I (symmetric)
+    M3<T> E;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = i; j < 3; ++j) {
+        T v = X.a[0][i] * X.a[0][j] + X.a[1][i] * X.a[1][j] + X.a[2][i] * X.a[2][j];
+        if (i == j) v -= T(1);
+        E.a[i][j] = v;
+        E.a[j][i] = v;
+      }
+    const T e2 = frob2(E);
+    if (!(e2 < T(0.25))) break;  // outside the comfortable convergence region
+    // X <- X (I - E/2)
+    M3<T> Y;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        Y.a[i][j] = X.a[i][j] - T(0.5) * (X.a[i][0] * E.a[0][j] + X.a[i][1] * E.a[1][j] + X.a[i][2] * E.a[2][j]);
+    X = Y;
+    // ||E|| ~ 1e-8 -> the step just taken leaves ~1.5e-16: converged.
+    if (e2 < Lim<T>::ns_done) return X;
+  }
+  return polar_rotation(F);
 }
 
 // gauss_inverse4 with partial pivoting (math.hpp:360-385).  Returns false on

@@ -35,6 +35,9 @@ constexpr int kTileVals = 2 * 4 * kTileNodes;         // 1728 (m, px, py, pz on 
 constexpr int kVelVals = 2 * 3 * kTileNodes;          // 1296
 constexpr int kXferThreads = 256;
 constexpr int kXferWarps = kXferThreads / 32;
+#ifndef CKG_G2P_MINB
+#define CKG_G2P_MINB 2
+#endif
 constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full lattice block)
 
 template <typename T>
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(kXferThreads, 2)
       const bool in_round = rb + lane < my_cnt;
       const uint32_t i = cb + (in_round ? uint32_t(cls_list[my_off + rb + lane]) : 0u);
       bool valid = in_round;
-      // ---- per-particle state and stress (force_matrix, transfer.hpp:183-216)
+      // ---- per-particle state (scatter_all, simulation.hpp:289-324)
       T x = 0, y = 0, z = 0, m = 0;
       T mv[3] = {0, 0, 0};
       M3<T> Ap, Q;  // Ap = dt * V0 * tau, Q = m * C
@@ -152,16 +155,19 @@ __global__ void __launch_bounds__(kXferThreads, 2)
         mv[0] = m * __ldg(cur.f + kV * n + src);
         mv[1] = m * __ldg(cur.f + (kV + 1) * n + src);
         mv[2] = m * __ldg(cur.f + (kV + 2) * n + src);
-        const T vol0 = __ldg(cur.f + kVol * n + src);
-        const T J = __ldg(cur.f + kJ * n + src);
-        const uint32_t mi = __ldg(cur.mat + src);
-        M3<T> A;
-        const int e = force_matrix(load_m3(cur, kF, src), J, vol0, c.mats[mi < kMaxMaterials ? mi : 0], A);
-        if (e) {
-          record_error(st, step, kPhaseP2G, i, 0, e);
-          valid = false;
+        // dt * V0 * tau from the stress cache written by the previous G2P
+        // (or the initial stress pass): P2G runs no constitutive model.
+        {
+          T t6[6];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) t6[k] = dt * __ldg(cur.tau + uint64_t(k) * n + src);
+          Ap.a[0][0] = t6[0];
+          Ap.a[0][1] = Ap.a[1][0] = t6[1];
+          Ap.a[0][2] = Ap.a[2][0] = t6[2];
+          Ap.a[1][1] = t6[3];
+          Ap.a[1][2] = Ap.a[2][1] = t6[4];
+          Ap.a[2][2] = t6[5];
         }
-        Ap = scale(dt, A);
         ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
         if (SCHEME != kSchemePic) {
           M3<T> Di;
@@ -430,7 +436,7 @@ __device__ __forceinline__ void gather_grid(const Axis<T>* ax, T dx, VelFn V, T 
 }
 
 template <typename T, int SCHEME>
-__global__ void __launch_bounds__(kXferThreads, 2)
+__global__ void __launch_bounds__(kXferThreads, CKG_G2P_MINB)
     g2p_tile_kernel(PState<T> cur, PState<T> nxt, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ active,
                     const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_end,
@@ -536,12 +542,11 @@ __global__ void __launch_bounds__(kXferThreads, 2)
             gather_grid<T>(ax, dx, [&](int s, int t, int u, int cc) { return V[s][t][u][cc]; }, v, Bn, G);
           }
         }
-        const T m = __ldg(cur.f + kMass * n + src);
-        const T vol0 = __ldg(cur.f + kVol * n + src);
-        T J = __ldg(cur.f + kJ * n + src);
+        // update_particle_state (transfer.hpp:594-627).  Outputs are stored
+        // as soon as they are final so the stress evaluation at the end runs
+        // with only F live (register pressure).
         mi = __ldg(cur.mat + src);
         const MatParam<T>& mp = c.mats[mi < kMaxMaterials ? mi : 0];
-        // update_particle_state (transfer.hpp:594-627)
         M3<T> L = G;
         if (SCHEME == kSchemeMls) {
           const Dual<T> ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
@@ -549,11 +554,9 @@ __global__ void __launch_bounds__(kXferThreads, 2)
           if (!apic_d_inverse(apic_D(ds, dx), Di)) record_error(st, step, kPhaseG2P, i, 0, kErrNearSingularD);
           L = mul(Bn, Di);
         }
-        M3<T> Bout = SCHEME == kSchemePic ? load_m3(cur, kB, src) : Bn;
-        M3<T> Fout = load_m3(cur, kF, src);
-        if (mp.model == kModelFluid) {
-          fluid = true;
-          if (mp.viscosity > T(0) && SCHEME != kSchemePic) {
+        {
+          M3<T> Bout = SCHEME == kSchemePic ? load_m3(cur, kB, src) : Bn;
+          if (mp.model == kModelFluid && mp.viscosity > T(0) && SCHEME != kSchemePic) {
             const T f = dexp(-mp.viscosity * dt / (mp.density * dx * dx));
             const T tb = trace(Bout) / T(3);
 #pragma unroll
@@ -562,23 +565,7 @@ __global__ void __launch_bounds__(kXferThreads, 2)
               for (int b = 0; b < 3; ++b)
                 Bout.a[a][b] = (a == b ? tb : T(0)) + (Bout.a[a][b] - (a == b ? tb : T(0))) * f;
           }
-          J *= T(1) + dt * trace(L);
-          if (!(J > T(0))) record_error(st, step, kPhaseG2P, i, 0, kErrFluidJ);
-        } else {
-          M3<T> Ld;
-#pragma unroll
-          for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) Ld.a[a][b] = (a == b ? T(1) : T(0)) + L.a[a][b] * dt;
-          M3<T> Fn = mul(Ld, Fout);
-          if (c.clamp_singular) clamp_singular_values(Fn, c.clamp_floor);
-          if (mp.model == kModelDP) {
-            const int e = return_map_dp(Fn, mp.dp_alpha, mp.mu, mp.lambda);
-            if (e) record_error(st, step, kPhaseG2P, i, 0, e);
-          } else if (!(det(Fn) > T(0))) {
-            record_error(st, step, kPhaseG2P, i, 0, kErrFInverted);
-          }
-          Fout = Fn;
+          store_m3(nxt, kB, i, Bout);
         }
         x += v[0] * dt;
         y += v[1] * dt;
@@ -589,16 +576,51 @@ __global__ void __launch_bounds__(kXferThreads, 2)
         nxt.f[kV * n + i] = v[0];
         nxt.f[(kV + 1) * n + i] = v[1];
         nxt.f[(kV + 2) * n + i] = v[2];
-        store_m3(nxt, kF, i, Fout);
-        store_m3(nxt, kB, i, Bout);
-        nxt.f[kJ * n + i] = J;
-        nxt.f[kMass * n + i] = m;
+        const T vol0 = __ldg(cur.f + kVol * n + src);
+        nxt.f[kMass * n + i] = __ldg(cur.f + kMass * n + src);
         nxt.f[kVol * n + i] = vol0;
         nxt.mat[i] = mi;
-        const T s2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+        {
+          const T s2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+          if (!dfinite(s2) || !dfinite(x * x + y * y + z * z)) atomicOr(&st->nonfinite, 1u);
+          if (s2 > vmax2) vmax2 = s2;  // NaN never wins (std::max(vm, s2) semantics)
+        }
+        T J = __ldg(cur.f + kJ * n + src);
+        M3<T> Fout = load_m3(cur, kF, src);
+        T t6[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};  // V0 tau of the new state
+        if (mp.model == kModelFluid) {
+          fluid = true;
+          store_m3(nxt, kF, i, Fout);  // fluids carry F unchanged (transfer.hpp:609-617)
+          J *= T(1) + dt * trace(L);
+          if (!(J > T(0))) {
+            record_error(st, step, kPhaseG2P, i, 0, kErrFluidJ);
+          } else {
+            stress_tau6(Fout, J, vol0, mp, t6);
+          }
+        } else {
+          M3<T> Ld;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) Ld.a[a][b] = (a == b ? T(1) : T(0)) + L.a[a][b] * dt;
+          M3<T> Fn = mul(Ld, Fout);
+          if (c.clamp_singular) clamp_singular_values(Fn, c.clamp_floor);
+          if (mp.model == kModelDP) {
+            const int e = return_map_dp(Fn, mp.dp_alpha, mp.mu, mp.lambda, t6);
+            if (e) record_error(st, step, kPhaseG2P, i, 0, e);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) t6[k] *= vol0;
+          } else if (!(det(Fn) > T(0))) {
+            record_error(st, step, kPhaseG2P, i, 0, kErrFInverted);
+          }
+          store_m3(nxt, kF, i, Fn);
+          if (mp.model == kModelFC && det(Fn) > T(0)) stress_tau6(Fn, J, vol0, mp, t6);
+        }
+        nxt.f[kJ * n + i] = J;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) nxt.tau[uint64_t(k) * n + i] = t6[k];
         Jout = J;
-        if (!dfinite(s2) || !dfinite(x * x + y * y + z * z)) atomicOr(&st->nonfinite, 1u);
-        if (s2 > vmax2) vmax2 = s2;  // NaN never wins (std::max(vm, s2) semantics)
+
       }
       // per-material min J over fluid particles (gather_all, simulation.hpp:371-372)
       uint32_t todo = __ballot_sync(0xffffffffu, live && fluid);
@@ -631,6 +653,22 @@ __global__ void __launch_bounds__(kXferThreads, 2)
     for (int w = 0; w < kXferWarps; ++w) b = (b < wmax[w]) ? wmax[w] : b;
     if (b > T(0)) atomicMax(&st->vmax2, as_ordered_bits(b));
   }
+}
+
+// Initial stress cache for a freshly uploaded state (force_matrix of every
+// particle, transfer.hpp:183-216); errors surface as P2G-phase errors exactly
+// where the reference's scatter would throw them.
+template <typename T>
+__global__ void __launch_bounds__(256) stress_kernel(PState<T> cur, StepConst<T> c, DevStatus* st, int step) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= cur.n) return;
+  const uint32_t mi = cur.mat[i];
+  T t6[6];
+  const int e = stress_tau6(load_m3(cur, kF, i), cur.f[kJ * cur.n + i], cur.f[kVol * cur.n + i],
+                            c.mats[mi < kMaxMaterials ? mi : 0], t6);
+  if (e) record_error(st, step, kPhaseP2G, i, 0, e);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) cur.tau[uint64_t(k) * cur.n + i] = e ? T(0) : t6[k];
 }
 
 // K4: clear the active part of the pool (grid.hpp:148-151).
