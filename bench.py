@@ -252,11 +252,16 @@ def main():
     time.sleep(0.3)
     L.ckg_timer_mark(ctx, 0)
     p2g_ms, g2p_ms = [], []
+    phase_acc = [0.0] * 6
+    sort_kinds = []
     total_launch = 0
     for _ in range(args.steps):
         step_once()
         p2g_ms.append(out.phase_ms[3])
         g2p_ms.append(out.phase_ms[5])
+        for k in range(6):
+            phase_acc[k] += out.phase_ms[k] / args.steps
+        sort_kinds.append(int(out.sort_kind))
         total_launch += int(out.kernel_launches)
     L.ckg_timer_mark(ctx, 1)
     el_ms = C.c_double()
@@ -337,7 +342,9 @@ def main():
                         "p2g_gbs": p2g_bytes / (p2g_avg * 1e-3) / 1e9,
                         "g2p_gbs": g2p_bytes / (g2p_avg * 1e-3) / 1e9,
                         "combined_frac": (p2g_bytes + g2p_bytes) / ((p2g_avg + g2p_avg) * 1e-3) / 1e9 / peak},
-            "phase_ms": dict(zip(abi.PHASE_NAMES, phase_ms)),
+            "phase_ms": dict(zip(abi.PHASE_NAMES, phase_acc)),
+            "sort_kinds": {"full_radix": sort_kinds.count(0), "identity": sort_kinds.count(1),
+                           "incremental": sort_kinds.count(2)},
             "cpu_baseline": cb,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                     "steps": e2e_steps, "path": "ckg_upload(pinned AoS) + ckg_step + ckg_download per step"},

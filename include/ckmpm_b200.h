@@ -146,6 +146,9 @@ typedef struct ckg_step_out {
   uint64_t error_particle;            /* sorted particle index (OutOfDomainError::particle_index) */
   uint64_t active_blocks;             /* BlockSparseGrid::active_block_count after activate */
   uint64_t kernel_launches;           /* device kernels this call enqueued */
+  uint64_t sort_changed;              /* particles whose block key changed since the last sort */
+  int32_t sort_kind;                  /* 0 full radix, 1 identity, 2 incremental merge */
+  int32_t _pad2;
 } ckg_step_out;
 
 /* DiagnosticsRow<T> (simulation.hpp:44-53), computed on the device

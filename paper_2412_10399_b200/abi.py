@@ -89,6 +89,8 @@ class StepOut(C.Structure):
         ("error_particle", C.c_uint64),
         ("active_blocks", C.c_uint64),
         ("kernel_launches", C.c_uint64),
+        ("sort_changed", C.c_uint64),
+        ("sort_kind", C.c_int32), ("_pad2", C.c_int32),
     ]
 
 

@@ -233,6 +233,10 @@ class Simulation:
     def reset_counters(self):
         self._counters = TransferCounters()
 
+    def last_sort_kind(self) -> int:
+        """0 full radix sort, 1 identity (no key changed), 2 incremental merge."""
+        return getattr(self, "_last_sort_kind", 0)
+
     def particle_count(self) -> int:
         return self._n
 
@@ -254,6 +258,7 @@ class Simulation:
         self._vmax = float(out.vmax)
         self._min_j = [float(out.min_j[m]) for m in range(len(self.cfg.materials))]
         self.last_active_blocks = int(out.active_blocks)
+        self._last_sort_kind = int(out.sort_kind)
 
     def step(self, dt: float) -> abi.StepOut:
         """Simulation::step (simulation.hpp:150-188) on the device."""

@@ -16,6 +16,7 @@
 
 #include "../../include/ckmpm_b200.h"
 #include "ckg_bin.cuh"
+#include "ckg_isort.cuh"
 #include "ckg_kernels.cuh"
 #include "ckg_scan.cuh"
 #include "ckg_transfer.cuh"
@@ -121,8 +122,16 @@ struct Context final : CtxBase {
   uint32_t* keys = nullptr;
   uint32_t* vals = nullptr;
   RadixScratch rs;
-  uint32_t* perm = nullptr;  // points into vals or rs.vals_alt after a sort
-  uint32_t* skeys = nullptr;
+  uint32_t* perm = nullptr;  // sorted position -> current index (result of the last sort)
+  uint32_t* skeys = nullptr; // sorted keys
+  // incremental sort state (ckg_isort.cuh)
+  uint32_t* ko = nullptr;    // sorted keys of the stored order (valid after a completed step)
+  bool ko_valid = false;
+  uint32_t *chg = nullptr, *cpre = nullptr, *ck = nullptr, *ci = nullptr, *iota = nullptr;
+  uint32_t *perm_buf = nullptr, *skeys_tmp = nullptr, *ncount = nullptr;
+  uint32_t* hcount = nullptr;  // pinned
+  uint64_t last_changed = 0;
+  int last_sort_kind = 0;    // 0 full radix, 1 identity, 2 incremental
   // grid
   uint32_t* core = nullptr;   // footprint blocks (D^3)
   uint32_t* flags = nullptr;  // active = dilated core (D^3)
@@ -132,6 +141,7 @@ struct Context final : CtxBase {
   int32_t* dir = nullptr;
   uint32_t* active = nullptr;
   uint32_t* scan_partials = nullptr;
+  uint32_t* scan_partials_n = nullptr;  // scan scratch sized for n
   T* pool = nullptr;
   uint32_t pool_cap = 0;
   // status
@@ -207,6 +217,8 @@ struct Context final : CtxBase {
     dfree(rs.vals_alt);
     dfree(rs.hist);
     dfree(rs.partials);
+    for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount}) dfree(*b);
+    if (hcount) cudaFreeHost(hcount);
     dfree(flags);
     dfree(core);
     dfree(seg_begin);
@@ -214,6 +226,7 @@ struct Context final : CtxBase {
     dfree(dir);
     dfree(active);
     dfree(scan_partials);
+    dfree(scan_partials_n);
     dfree(pool);
     dfree(dstat);
     dfree(dbcs);
@@ -267,6 +280,7 @@ struct Context final : CtxBase {
     dfree(rs.vals_alt);
     dfree(rs.hist);
     dfree(rs.partials);
+    for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount}) dfree(*b);
     n = count;
     for (int b = 0; b < 2; ++b) {
       fbuf[b] = dalloc<T>(uint64_t(kNumFields) * std::max<uint64_t>(n, 1));
@@ -280,6 +294,13 @@ struct Context final : CtxBase {
     uint64_t nh = uint64_t(kRadix) * sort_tiles(std::max<uint64_t>(n, 1));
     rs.hist = dalloc<uint32_t>(nh);
     rs.partials = dalloc<uint32_t>(scan_tiles(nh) + 1);
+    for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp}) *b = dalloc<uint32_t>(n);
+    ncount = dalloc<uint32_t>(1);
+    dfree(scan_partials_n);
+    scan_partials_n = dalloc<uint32_t>(scan_tiles(std::max<uint64_t>(n, 1)) + 1);
+    if (!hcount) CKG_CUDA(cudaMallocHost(&hcount, sizeof(uint32_t)));
+    if (n) iota_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(iota, n);
+    ko_valid = false;
     cur = 0;
   }
 
@@ -302,6 +323,7 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaStreamSynchronize(st));
     grid_valid = false;
     stress_valid = false;
+    ko_valid = false;
     return CKG_OK;
   }
 
@@ -359,12 +381,53 @@ struct Context final : CtxBase {
   }
 
   // K1 + K2: key/footprint pass then stable sort (perm[i] = source index of
-  // sorted position i, skeys[i] its key).
+  // sorted position i, skeys[i] its key).  With the stored order's sorted
+  // keys at hand the sort is incremental (ckg_isort.cuh); one small host
+  // read-back of the changed count picks identity / merge / full radix.
   void enqueue_sort() {
     PState<T> cs = state(cur);
     key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(cs, T(cfg.inv_dx), cfg.resolution, D, keys,
                                                                          core, dstat);
-    radix_sort_pairs(keys, vals, n, key_bits, rs, st, &skeys, &perm);
+    launches += 1;
+    if (ko_valid) {
+      changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, ko, n, chg);
+      exclusive_scan(chg, cpre, n, scan_partials_n, st);
+      compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci, ncount);
+      launches += 5;
+      CKG_CUDA(cudaMemcpyAsync(hcount, ncount, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CKG_CUDA(cudaStreamSynchronize(st));
+      const uint32_t nc = *hcount;
+      last_changed = nc;
+      if (nc == 0) {
+        perm = iota;
+        skeys = ko;
+        last_sort_kind = 1;
+        return;
+      }
+      if (uint64_t(nc) * 8 <= n) {
+        uint32_t *sck = nullptr, *sci = nullptr;
+        radix_sort_pairs(ck, ci, nc, key_bits, rs, st, &sck, &sci, ci);
+        merge_unchanged_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, sck, sci, nc,
+                                                                          perm_buf, skeys_tmp);
+        merge_changed_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, st>>>(ko, cpre, n, sck, sci, nc, perm_buf,
+                                                                          skeys_tmp);
+        launches += uint64_t((key_bits + kRadixBits - 1) / kRadixBits) * 5 + 2;
+        std::swap(ko, skeys_tmp);
+        perm = perm_buf;
+        skeys = ko;
+        last_sort_kind = 2;
+        return;
+      }
+    }
+    uint32_t *sk = nullptr, *sp = nullptr;
+    radix_sort_pairs(keys, vals, n, key_bits, rs, st, &sk, &sp);
+    launches += uint64_t((key_bits + kRadixBits - 1) / kRadixBits) * 5;
+    CKG_CUDA(cudaMemcpyAsync(ko, sk, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    perm = sp;
+    skeys = ko;
+    ko_valid = true;
+    last_sort_kind = 0;
+    last_changed = n;
   }
 
   // K3-K6: inset error in sorted order, halo dilation, directory, segments.
@@ -393,8 +456,7 @@ struct Context final : CtxBase {
   // pass, inset fix-up, dilate, 3-kernel scan, compact, segments, clear,
   // P2G, grid, G2P).
   uint64_t launches_per_step(int stop_after) const {
-    int passes = (key_bits + kRadixBits - 1) / kRadixBits;
-    uint64_t k = 2 + uint64_t(passes) * 5;
+    uint64_t k = 1;  // status reset; sort kernels are counted by enqueue_sort
     if (stop_after >= CKG_PHASE_ACTIVATE) k += 7;
     if (stop_after >= CKG_PHASE_CLEAR) k += 1;
     if (stop_after >= CKG_PHASE_P2G) k += 1;
@@ -527,6 +589,7 @@ struct Context final : CtxBase {
       CKG_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
       CKG_CUDA(cudaStreamSynchronize(st));
       if (hstat->overflow && count_steps == 1) {
+        ko_valid = false;
         // grow the pool (state untouched: G2P writes the other buffer)
         uint64_t want = std::min<uint64_t>(nd, uint64_t(hstat->n_active) * 5 / 4 + 64);
         set_pool_cap(uint32_t(want));
@@ -536,6 +599,8 @@ struct Context final : CtxBase {
     }
     fill_out(out, timed, count_steps == 1 ? stop_after : CKG_PHASE_G2P);
     out->kernel_launches = launches;
+    out->sort_changed = last_changed;
+    out->sort_kind = last_sort_kind;
     grid_valid = true;
     last_active = hstat->n_active;
     if (hstat->overflow) {
@@ -548,9 +613,14 @@ struct Context final : CtxBase {
       if (rc == CKG_OK && stop_after >= CKG_PHASE_G2P) {
         cur ^= 1;
         step_count += 1;
+      } else {
+        ko_valid = false;  // stored order unchanged: the new sorted keys do not describe it
       }
+      if (stop_after < CKG_PHASE_ACTIVATE) CKG_CUDA(cudaMemsetAsync(core, 0, nd * sizeof(uint32_t), st));
     } else if (rc == CKG_OK) {
       step_count += uint64_t(count_steps);
+    } else {
+      ko_valid = false;
     }
     out->status = rc;
     return rc;
@@ -560,10 +630,13 @@ struct Context final : CtxBase {
     if (count != n) return CKG_ERR_CONFIG;
     if (n == 0) return CKG_OK;
     CKG_CUDA(cudaSetDevice(device));
+    status_reset_kernel<<<1, 32, 0, st>>>(dstat, 1);
     enqueue_sort();
     CKG_CUDA(cudaMemcpyAsync(hkeys, skeys, n * 4, cudaMemcpyDeviceToHost, st));
     CKG_CUDA(cudaMemcpyAsync(horder, perm, n * 4, cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaMemsetAsync(core, 0, nd * sizeof(uint32_t), st));
     CKG_CUDA(cudaStreamSynchronize(st));
+    ko_valid = false;  // the stored order was not permuted
     return CKG_OK;
   }
 

@@ -212,10 +212,12 @@ inline uint32_t sort_tiles(uint64_t n) { return uint32_t((n + kSortTile - 1) / k
 // Stable sort of keys[0..n) (only the low `bits` bits are significant).
 // On return *keys_res / *vals_res point at the sorted keys and the permutation
 // (either the caller's buffers or the scratch ones).
+// vals_init == nullptr: the values are the input indices (a permutation).
 inline void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint64_t n, int bits, RadixScratch& s,
-                             cudaStream_t st, uint32_t** keys_res, uint32_t** vals_res) {
+                             cudaStream_t st, uint32_t** keys_res, uint32_t** vals_res,
+                             uint32_t* vals_init = nullptr) {
   uint32_t ntiles = sort_tiles(n);
-  uint32_t *kin = keys, *vin = nullptr, *kout = s.keys_alt, *vout = s.vals_alt;
+  uint32_t *kin = keys, *vin = vals_init, *kout = s.keys_alt, *vout = s.vals_alt;
   int passes = (bits + kRadixBits - 1) / kRadixBits;
   if (passes < 1) passes = 1;
   for (int p = 0; p < passes; ++p) {
