@@ -386,18 +386,19 @@ struct Context final : CtxBase {
   // read-back of the changed count picks identity / merge / full radix.
   void enqueue_sort() {
     PState<T> cs = state(cur);
-    key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(cs, T(cfg.inv_dx), cfg.resolution, D, keys,
-                                                                         core, dstat);
+    key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
+        cs, T(cfg.inv_dx), cfg.resolution, D, keys, core, ko_valid ? ko : nullptr, chg, dstat);
     launches += 1;
     if (ko_valid) {
-      changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, ko, n, chg);
-      exclusive_scan(chg, cpre, n, scan_partials_n, st);
-      compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci, ncount);
-      launches += 5;
-      CKG_CUDA(cudaMemcpyAsync(hcount, ncount, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CKG_CUDA(cudaMemcpyAsync(hcount, &dstat->nchanged, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
       CKG_CUDA(cudaStreamSynchronize(st));
       const uint32_t nc = *hcount;
       last_changed = nc;
+      if (nc != 0 && uint64_t(nc) * 8 <= n) {
+        exclusive_scan(chg, cpre, n, scan_partials_n, st);
+        compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci, ncount);
+        launches += 4;
+      }
       if (nc == 0) {
         perm = iota;
         skeys = ko;

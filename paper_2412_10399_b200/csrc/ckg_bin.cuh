@@ -39,35 +39,52 @@ template <typename T>
 __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv_dx, int res, int D,
                                                             uint32_t* __restrict__ keys,
                                                             uint32_t* __restrict__ core,
-                                                            DevStatus* st) {
+                                                            const uint32_t* __restrict__ ko,
+                                                            uint32_t* __restrict__ chg, DevStatus* st) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool live = i < cur.n;
-  T x[3] = {T(0), T(0), T(0)};
-  bool ok = live;
-  int lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+  bool ok = live, changed = false;
+  uint32_t key = 0xffffffffu, ext = 0;
+  int kb[3] = {0, 0, 0};
   if (live) {
+    T x[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) x[a] = __ldg(cur.f + uint64_t(kX + a) * cur.n + i);
-    keys[i] = block_key(x[0], x[1], x[2], inv_dx, D);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) kb[a] = key_axis(x[a], inv_dx, D);
+    key = (uint32_t(kb[0]) * uint32_t(D) + uint32_t(kb[1])) * uint32_t(D) + uint32_t(kb[2]);
+    keys[i] = key;
+    if (ko) {
+      changed = key != __ldg(ko + i);
+      chg[i] = changed ? 1u : 0u;
+    }
+    // footprint blocks relative to the key block: lo in {kb-1, kb}, hi in {kb, kb+1}
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       ok = ok && inset_ok(x[a], inv_dx, res);
-      axis_footprint(x[a], inv_dx, lo[a], hi[a]);
+      int lo, hi;
+      axis_footprint(x[a], inv_dx, lo, hi);
+      ok = ok && lo >= kb[a] - 1 && hi <= kb[a] + 1;
+      ext |= (lo < kb[a] ? 1u : 0u) << (2 * a);
+      ext |= (hi > kb[a] ? 1u : 0u) << (2 * a + 1);
     }
     if (!ok) atomicOr(&st->inset_fail, 1u);
   }
-  // Warp dedupe of identical footprint boxes (neighbouring particles mostly
-  // share one), then the leader marks 1..8 blocks.
-  const uint64_t box =
-      ok ? ((uint64_t(uint32_t(lo[0]) & 0x3ff) << 50) | (uint64_t(uint32_t(lo[1]) & 0x3ff) << 40) |
-            (uint64_t(uint32_t(lo[2]) & 0x3ff) << 30) | (uint64_t(uint32_t(hi[0]) & 0x3ff) << 20) |
-            (uint64_t(uint32_t(hi[1]) & 0x3ff) << 10) | uint64_t(uint32_t(hi[2]) & 0x3ff))
-         : (~0ull - (threadIdx.x & 31));
-  const uint32_t peers = __match_any_sync(0xffffffffu, box);
+  if (ko) {
+    const uint32_t cb = __ballot_sync(0xffffffffu, changed);
+    if ((threadIdx.x & 31) == 0 && cb) atomicAdd(&st->nchanged, uint32_t(__popc(cb)));
+  }
+  // Lanes with the same footprint box (same key block and extent bits) mark
+  // it once.  (A bounding box over different boxes would over-activate.)
+  const uint64_t gbox = ok ? ((uint64_t(key) << 8) | ext) : (~0ull - (threadIdx.x & 31));
+  const uint32_t peers = __match_any_sync(0xffffffffu, gbox);
   if (!ok || (__ffs(peers) - 1) != int(threadIdx.x & 31)) return;
-  for (int bi = lo[0]; bi <= hi[0]; ++bi)
-    for (int bj = lo[1]; bj <= hi[1]; ++bj)
-      for (int bk = lo[2]; bk <= hi[2]; ++bk)
+  const int x0 = kb[0] - int(ext & 1u), x1 = kb[0] + int((ext >> 1) & 1u);
+  const int y0 = kb[1] - int((ext >> 2) & 1u), y1 = kb[1] + int((ext >> 3) & 1u);
+  const int z0 = kb[2] - int((ext >> 4) & 1u), z1 = kb[2] + int((ext >> 5) & 1u);
+  for (int bi = x0; bi <= x1; ++bi)
+    for (int bj = y0; bj <= y1; ++bj)
+      for (int bk = z0; bk <= z1; ++bk)
         if (bi >= 0 && bj >= 0 && bk >= 0 && bi < D && bj < D && bk < D)
           core[(int64_t(bi) * D + bj) * D + bk] = 1u;
 }

@@ -70,6 +70,7 @@ struct DevStatus {
   unsigned int n_active;
   unsigned int overflow;
   unsigned int inset_fail;      // some particle violated the 2-cell inset (index fixed up after the sort)
+  unsigned int nchanged;        // particles whose block key differs from the stored sorted key
   unsigned int work[4];         // persistent-kernel work counters (P2G, G2P)
 };
 

@@ -695,6 +695,7 @@ __global__ void status_reset_kernel(DevStatus* st, int reset_err) {
     st->n_active = 0u;
     st->overflow = 0u;
     st->inset_fail = 0u;
+    st->nchanged = 0u;
   }
   if (threadIdx.x < 4) st->work[threadIdx.x] = 0u;
   if (threadIdx.x < kMaxMaterials) st->minj[threadIdx.x] = 0x7ff0000000000000ull;  // +inf
