@@ -9,7 +9,7 @@ PKG = paper_2412_10399_b200
 SRC = $(PKG)/csrc/ckg_api.cu
 HDR = $(wildcard $(PKG)/csrc/*.cuh) include/ckmpm_b200.h
 
-all: $(PKG)/libckmpm_b200.so oracle
+all: $(PKG)/libckmpm_b200.so oracle dropin
 
 $(PKG)/libckmpm_b200.so: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build/ptxas.log || (cat build/ptxas.log; false)
@@ -23,3 +23,16 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
+
+# C++ drop-in test binary (needs the reference headers; built where they exist,
+# the binary travels to the GPU box).
+REF ?= /root/reference
+DROPIN_BIN = tests/cpp/_bin/dropin_test
+dropin: $(PKG)/libckmpm_b200.so
+	@if [ -d $(REF)/proj/include/ckmpm ]; then \
+	  mkdir -p tests/cpp/_bin && g++ -std=gnu++20 -O3 -DNDEBUG -fno-math-errno -pthread \
+	    -I$(REF)/proj/include -Iinclude tests/cpp/dropin_test.cpp -L$(PKG) -lckmpm_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../../$(PKG)' -o $(DROPIN_BIN) ; \
+	else echo "reference tree absent: keeping prebuilt $(DROPIN_BIN)"; fi
+
+.PHONY: dropin

@@ -1,0 +1,46 @@
+"""The C++ drop-in (include/ckmpm_b200/simulation.hpp) driven like the
+reference's ckmpm::Simulation<T>, next to the reference engine, plus the
+reference's acceptance criteria 3, 4 and 10 (proj/tests/acceptance_main.cpp)
+run through the drop-in on the GPU.  The binary is built by `make dropin`
+where /root/reference exists and travels with the repo."""
+import json
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+BIN = os.path.join(os.path.dirname(__file__), "cpp", "_bin", "dropin_test")
+
+
+def run(what, timeout=900):
+    if not os.path.exists(BIN):
+        pytest.skip("dropin_test not built (needs the reference headers at build time)")
+    r = subprocess.run([BIN, what], capture_output=True, text=True, timeout=timeout)
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert line, r.stdout + r.stderr
+    d = json.loads(line[-1])
+    print(d)
+    assert r.returncode == 0 and d["pass"], d
+    return d
+
+
+def test_dropin_parity_with_reference():
+    run("parity")
+
+
+def test_dropin_errors_match_reference():
+    run("errors")
+
+
+def test_acceptance_4_rotating_rod_angular_momentum():
+    d = run("rod")
+    assert abs(d["lz0"] - 4.9639e-3) <= 0.01 * 4.9639e-3
+
+
+def test_acceptance_3_two_spheres_momentum():
+    run("spheres")
+
+
+def test_acceptance_10_stress_scenes_mass():
+    run("stress")
