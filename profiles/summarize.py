@@ -1,0 +1,115 @@
+#!/usr/bin/env python3
+"""Summarise ncu outputs brought back in gpurun_out/ into the committed
+profiles/ files (run in the build container; ncu -i works without a GPU).
+
+  python profiles/summarize.py launches <launch-list.csv> <out.txt>
+      one steady-state substep of the bench command (kernel, device time, share)
+  python profiles/summarize.py full <report.ncu-rep> <out.txt> [--traffic profiles/traffic.json]
+      key metrics per profiled kernel; with --traffic, the measured DRAM bytes
+      per launch of each kernel are recorded for bench.py's roofline.traffic
+"""
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "dram_read"),
+    ("dram__bytes_write.sum", "dram_write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%peak"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64_pipe_%"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy_%"),
+    ("launch__registers_per_thread", "regs"),
+    ("smsp__inst_executed.sum", "warp_instr"),
+    ("lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed", "l2_atomic_%"),
+    ("lts__t_sectors_srcunit_tex_op_red.sum", "l2_red_sectors"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem_ld_bank_conflicts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "smem_st_bank_conflicts"),
+    ("smsp__sass_inst_executed_op_shared_ld.sum", "smem_ld_instr"),
+    ("smsp__sass_inst_executed_op_local_ld.sum", "local_ld_instr"),
+]
+
+
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hdr]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    seq = []
+    for r in rows[hdr + 1:]:
+        if len(r) <= vi:
+            continue
+        try:
+            v = float(r[vi].replace(",", ""))
+        except ValueError:
+            continue
+        seq.append((r[ki].split("(")[0].replace("void ", ""), v))
+    starts = [i for i, (n, _) in enumerate(seq) if "status_reset" in n]
+    # the last complete substep before the e2e loop: second-to-last reset pair
+    s, e = starts[-3], starts[-2]
+    step = seq[s:e]
+    tot = sum(v for _, v in step)
+    with open(out, "w") as f:
+        f.write(f"# one steady-state substep of the bench command, ncu gpu__time_duration.sum\n")
+        f.write(f"# (cold-cache, serialised launches: compare SHARES, not absolutes)\n")
+        f.write(f"# source: {path}\n")
+        for n, v in step:
+            f.write(f"{n:48s} {v / 1e3:10.1f} us  {v / tot * 100:5.1f} %\n")
+        f.write(f"{'substep total':48s} {tot / 1e3:10.1f} us\n")
+        agg = collections.OrderedDict()
+        for n, v in seq:
+            agg.setdefault(n, []).append(v)
+        f.write("\n# all launches of the run, by kernel\n")
+        for n, vs in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+            f.write(f"{n:48s} n={len(vs):4d} avg={sum(vs) / len(vs) / 1e3:10.1f} us\n")
+    print(open(out).read())
+
+
+def full(path, out, traffic=None):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    by_kernel = collections.OrderedDict()
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")].split("(")[0].replace("void ", "")
+        by_kernel.setdefault(name, []).append(r)
+    lines = [f"# ncu --set full summary; source: {path}"]
+    tr = {}
+    for name, rs in by_kernel.items():
+        lines.append(f"\n== {name}  ({len(rs)} launch(es) profiled)")
+        for m, label in METRICS:
+            if m not in h:
+                continue
+            i = h.index(m)
+            vals = []
+            for r in rs:
+                try:
+                    vals.append(float(r[i].replace(",", "")))
+                except ValueError:
+                    pass
+            if vals:
+                lines.append(f"  {label:26s} {sum(vals) / len(vals):14.4f} {units[i]}")
+        short = name.split("::")[-1].split("<")[0]
+        if "dram__bytes_read.sum" in h:
+            ur = units[h.index("dram__bytes_read.sum")]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
+            rd = sum(float(r[h.index("dram__bytes_read.sum")].replace(",", "")) for r in rs) / len(rs)
+            wr = sum(float(r[h.index("dram__bytes_write.sum")].replace(",", "")) for r in rs) / len(rs)
+            tr[short.replace("_tile", "")] = (rd + wr) * scale
+    # stall reasons of the longest kernel
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    if traffic:
+        json.dump(tr, open(traffic, "w"), indent=1)
+        print("traffic:", tr)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        t = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
+        full(sys.argv[2], sys.argv[3], t)
