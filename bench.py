@@ -198,19 +198,93 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_slab(args, ws, rank, local):
+    """N>1: x-slab decomposition (paper_2412_10399_b200/slab.py), one rank
+    per GPU over NCCL.  Weak scaling: the C5 block grows with N so every GPU
+    keeps ~10M particles (cells = 108 * N^(1/3))."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_10399_b200._lib import lib
+    from paper_2412_10399_b200.slab import DistTransport, build_rank_for_box
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = lib()
+    cells = int(round(args.cells * ws ** (1.0 / 3.0)))
+    cfg = block_scene(cells, resolution=args.res, scheme=args.scheme)
+    bounds, rk = build_rank_for_box(cfg, ws, rank, args.precision, local)
+    tr = DistTransport(dist, rank, ws, torch.device("cuda", local))
+    n_local = torch.tensor([rk.n], dtype=torch.int64, device=f"cuda:{local}")
+    dist.all_reduce(n_local)
+    n_total = int(n_local.item())
+    dt = rk.cfl_dt(1.0)
+    for _ in range(args.warmup):
+        tr.step(rk, dt)
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    L.ckg_timer_mark(rk.ctx, 0)
+    launches = 0
+    for _ in range(args.steps):
+        tr.step(rk, dt)
+        launches += int(rk.out.kernel_launches)
+    L.ckg_timer_mark(rk.ctx, 1)
+    el = C.c_double()
+    L.ckg_timer_elapsed(rk.ctx, 0, 1, C.byref(el))
+    clocks = sampler.stop()
+    t = torch.tensor([el.value], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    value = n_total * args.steps / (t_ms * 1e-3)
+    # e2e: each step the rank's state goes host -> device -> host through the ABI
+    e2e_steps = max(1, args.e2e_steps)
+    dist.barrier()
+    L.ckg_timer_mark(rk.ctx, 2)
+    hb = hd = 0
+    for _ in range(e2e_steps):
+        host = rk.particles()
+        hd += host.nbytes
+        L.ckg_upload(rk.ctx, abi.ptr(host), len(host))
+        hb += host.nbytes
+        tr.step(rk, dt)
+    L.ckg_timer_mark(rk.ctx, 3)
+    L.ckg_timer_elapsed(rk.ctx, 2, 3, C.byref(el))
+    t = torch.tensor([el.value], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if args.precision == 8 else "f32", "data": "synthetic",
+            "config": {"workload": f"C5_block_{cells} (weak scaling: ~{args.cells}^3 cells per GPU)",
+                       "particles_total": n_total, "resolution": args.res, "scheme": args.scheme,
+                       "material": "fixed_corotated", "ppc": 8, "dt": dt,
+                       "parallelism": f"x-slab decomposition over {ws} GPUs (NCCL halo reduce/broadcast, migration)",
+                       "slab_bounds": list(map(int, bounds))},
+            "e2e": {"value": n_total * e2e_steps / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": hb // e2e_steps, "d2h_bytes_per_step": hd // e2e_steps,
+                    "steps": e2e_steps, "path": "per rank: ckg_download + ckg_upload + slab substep"},
+            "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    rk.close()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
     ws, rank, local = dist_env()
-    dist = None
     if ws > 1:
-        import torch
-        import torch.distributed as dist_mod
-        torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl")
-        dist = dist_mod
+        run_slab(args, ws, rank, local)
+        return
+    dist = None
     import torch
 
     from paper_2412_10399_b200._lib import lib

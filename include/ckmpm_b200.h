@@ -220,6 +220,33 @@ int32_t ckg_grid_totals(ckg_ctx* ctx, double mass[2], double momentum[6]);
 /* compute_diagnostics on the device (simulation.hpp:55-69). */
 int32_t ckg_diagnostics_compute(ckg_ctx* ctx, ckg_diagnostics* out);
 
+/* ---- x-slab decomposition (net-new, the reference has none).
+ * One context per GPU/rank owning block planes bx in [bx_lo, bx_hi); the
+ * substep is split into stages and the host moves the exchange buffers
+ * (device pointers) between them with NCCL (paper_2412_10399_b200/slab.py):
+ *   ckg_slab_bin      key/sort of own particles; footprint flags (D^3 u32) -> core_out
+ *   (host: MAX-allreduce core over ranks)
+ *   ckg_slab_p2g      global activation from the reduced flags, clear, P2G;
+ *                     block counts of planes {bx_lo-1, bx_lo, bx_hi-1, bx_hi}
+ *   ckg_slab_halo     op 0 pack a plane, 1 add into it, 2 overwrite it
+ *                     (block = 2 grids x 4 values x 64 nodes of T)
+ *   ckg_slab_grid     grid update of own planes
+ *   ckg_slab_g2p      G2P; counts of particles leaving left / right
+ *   ckg_slab_pack     survivors compacted after nl_in incoming; migrant records
+ *                     (ckg_slab_record_words() T words each) into left/right
+ *   ckg_slab_finish   incoming records appended [left][survivors][right]
+ * Must be called before ckg_upload. */
+int32_t ckg_slab_set(ckg_ctx* ctx, int32_t rank, int32_t world, int32_t bx_lo, int32_t bx_hi);
+int32_t ckg_slab_bin(ckg_ctx* ctx, double dt, void* core_out);
+int32_t ckg_slab_p2g(ckg_ctx* ctx, const void* core_in, uint64_t plane_blocks[4]);
+int32_t ckg_slab_halo(ckg_ctx* ctx, int32_t op, int32_t plane, void* buf);
+int32_t ckg_slab_grid(ckg_ctx* ctx);
+int32_t ckg_slab_g2p(ckg_ctx* ctx, uint64_t counts[2]);
+int32_t ckg_slab_pack(ckg_ctx* ctx, uint64_t nl_in, void* left, void* right);
+int32_t ckg_slab_finish(ckg_ctx* ctx, const void* left, uint64_t nl, const void* right, uint64_t nr,
+                        ckg_step_out* out);
+int32_t ckg_slab_record_words(void);
+
 /* Device-side timing on the context's stream (the stream every kernel of
  * this context is launched on): record marker `slot` (0..15); elapsed ms
  * between two recorded markers (synchronises on `b`). */

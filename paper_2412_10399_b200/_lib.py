@@ -64,6 +64,23 @@ def _declare(lib: C.CDLL) -> None:
     lib.ckg_timer_mark.restype = i32
     lib.ckg_timer_elapsed.argtypes = [vp, i32, i32, P(C.c_double)]
     lib.ckg_timer_elapsed.restype = i32
+    lib.ckg_slab_set.argtypes = [vp, i32, i32, i32, i32]
+    lib.ckg_slab_set.restype = i32
+    lib.ckg_slab_bin.argtypes = [vp, C.c_double, vp]
+    lib.ckg_slab_bin.restype = i32
+    lib.ckg_slab_p2g.argtypes = [vp, vp, P(u64)]
+    lib.ckg_slab_p2g.restype = i32
+    lib.ckg_slab_halo.argtypes = [vp, i32, i32, vp]
+    lib.ckg_slab_halo.restype = i32
+    lib.ckg_slab_grid.argtypes = [vp]
+    lib.ckg_slab_grid.restype = i32
+    lib.ckg_slab_g2p.argtypes = [vp, P(u64)]
+    lib.ckg_slab_g2p.restype = i32
+    lib.ckg_slab_pack.argtypes = [vp, u64, vp, vp]
+    lib.ckg_slab_pack.restype = i32
+    lib.ckg_slab_finish.argtypes = [vp, vp, u64, vp, u64, P(abi.StepOut)]
+    lib.ckg_slab_finish.restype = i32
+    lib.ckg_slab_record_words.restype = i32
     lib.ckg_last_error_message.argtypes = [vp, C.c_char_p, u64]
     lib.ckg_last_error_message.restype = i32
 
@@ -74,6 +91,8 @@ EXPORTED = (
     "ckg_step_many", "ckg_step_phases", "ckg_debug_sort", "ckg_debug_bases",
     "ckg_grid_active_block_count", "ckg_grid_download", "ckg_grid_totals",
     "ckg_diagnostics_compute", "ckg_timer_mark", "ckg_timer_elapsed", "ckg_last_error_message",
+    "ckg_slab_set", "ckg_slab_bin", "ckg_slab_p2g", "ckg_slab_halo", "ckg_slab_grid", "ckg_slab_g2p",
+    "ckg_slab_pack", "ckg_slab_finish", "ckg_slab_record_words",
 )
 
 

@@ -19,6 +19,7 @@
 #include "ckg_isort.cuh"
 #include "ckg_kernels.cuh"
 #include "ckg_scan.cuh"
+#include "ckg_slab.cuh"
 #include "ckg_transfer.cuh"
 
 namespace ckg {
@@ -94,6 +95,14 @@ struct CtxBase {
   virtual int grid_download(int32_t* coords, double* nodes, uint64_t nb) = 0;
   virtual int grid_totals(double* mass, double* mom) = 0;
   virtual int diagnostics(ckg_diagnostics* out) = 0;
+  virtual int slab_set(int rank, int world, int lo, int hi) = 0;
+  virtual int slab_bin(double dt, void* core_out) = 0;
+  virtual int slab_p2g(const void* core_in, uint64_t* plane_blocks) = 0;
+  virtual int slab_halo(int op, int plane, void* buf) = 0;
+  virtual int slab_grid() = 0;
+  virtual int slab_g2p(uint64_t* counts) = 0;
+  virtual int slab_pack(uint64_t nl_in, void* left, void* right) = 0;
+  virtual int slab_finish(const void* left, uint64_t nl, const void* right, uint64_t nr, ckg_step_out* out) = 0;
   virtual int timer_mark(int slot) = 0;
   virtual int timer_elapsed(int a, int b, double* ms) = 0;
 };
@@ -115,6 +124,15 @@ struct Context final : CtxBase {
   T* tbuf[2] = {nullptr, nullptr};  // stress cache (6 x n) per state buffer
   bool stress_valid = false;
   int cur = 0;
+  uint64_t cap = 0;  // particle buffer capacity (field stride)
+  // x-slab decomposition (ckg_slab.cuh)
+  bool slab = false;
+  int srank = 0, sworld = 1, bx_lo = 0, bx_hi = 0;
+  uint32_t* plane_start = nullptr;
+  uint32_t *fl_stay = nullptr, *fl_left = nullptr, *fl_right = nullptr;
+  uint32_t *pos_stay = nullptr, *pos_left = nullptr, *pos_right = nullptr;
+  uint64_t mig_left = 0, mig_right = 0, n_stay = 0;
+  double slab_dt = 0;
   // staging for AoS transfers
   T* staging = nullptr;
   uint64_t staging_words = 0;
@@ -218,6 +236,7 @@ struct Context final : CtxBase {
     dfree(rs.hist);
     dfree(rs.partials);
     for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount}) dfree(*b);
+    for (uint32_t** b : {&plane_start, &fl_stay, &fl_left, &fl_right, &pos_stay, &pos_left, &pos_right}) dfree(*b);
     if (hcount) cudaFreeHost(hcount);
     dfree(flags);
     dfree(core);
@@ -247,7 +266,7 @@ struct Context final : CtxBase {
     active = dalloc<uint32_t>(cap);
   }
 
-  PState<T> state(int b) const { return PState<T>{fbuf[b], mbuf[b], tbuf[b], n}; }
+  PState<T> state(int b) const { return PState<T>{fbuf[b], mbuf[b], tbuf[b], n, cap}; }
 
   template <int S>
   void occupancy_for() {
@@ -268,7 +287,12 @@ struct Context final : CtxBase {
   }
 
   void ensure_particles(uint64_t count) {
-    if (count == n && fbuf[0]) return;
+    // slab mode keeps headroom for migrants (the particle count of a rank changes)
+    const uint64_t want = slab ? count + std::max<uint64_t>(count / 2, 1u << 20) : count;
+    if (fbuf[0] && want <= cap && (slab || count == cap)) {
+      n = count;
+      return;
+    }
     for (int b = 0; b < 2; ++b) {
       dfree(fbuf[b]);
       dfree(mbuf[b]);
@@ -282,24 +306,31 @@ struct Context final : CtxBase {
     dfree(rs.partials);
     for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount}) dfree(*b);
     n = count;
+    cap = std::max<uint64_t>(want, 1);
     for (int b = 0; b < 2; ++b) {
-      fbuf[b] = dalloc<T>(uint64_t(kNumFields) * std::max<uint64_t>(n, 1));
-      mbuf[b] = dalloc<uint32_t>(std::max<uint64_t>(n, 1));
-      tbuf[b] = dalloc<T>(6 * std::max<uint64_t>(n, 1));
+      fbuf[b] = dalloc<T>(uint64_t(kNumFields) * cap);
+      mbuf[b] = dalloc<uint32_t>(cap);
+      tbuf[b] = dalloc<T>(6 * cap);
     }
-    keys = dalloc<uint32_t>(n);
-    vals = dalloc<uint32_t>(n);
-    rs.keys_alt = dalloc<uint32_t>(n);
-    rs.vals_alt = dalloc<uint32_t>(n);
-    uint64_t nh = uint64_t(kRadix) * sort_tiles(std::max<uint64_t>(n, 1));
+    keys = dalloc<uint32_t>(cap);
+    vals = dalloc<uint32_t>(cap);
+    rs.keys_alt = dalloc<uint32_t>(cap);
+    rs.vals_alt = dalloc<uint32_t>(cap);
+    uint64_t nh = uint64_t(kRadix) * sort_tiles(cap);
     rs.hist = dalloc<uint32_t>(nh);
     rs.partials = dalloc<uint32_t>(scan_tiles(nh) + 1);
-    for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp}) *b = dalloc<uint32_t>(n);
+    for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp}) *b = dalloc<uint32_t>(cap);
     ncount = dalloc<uint32_t>(1);
     dfree(scan_partials_n);
-    scan_partials_n = dalloc<uint32_t>(scan_tiles(std::max<uint64_t>(n, 1)) + 1);
+    scan_partials_n = dalloc<uint32_t>(scan_tiles(cap) + 1);
     if (!hcount) CKG_CUDA(cudaMallocHost(&hcount, sizeof(uint32_t)));
-    if (n) iota_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(iota, n);
+    iota_kernel<<<grid_for(cap, 256, 1 << 30), 256, 0, st>>>(iota, cap);
+    if (slab) {
+      for (uint32_t** b : {&fl_stay, &fl_left, &fl_right, &pos_stay, &pos_left, &pos_right}) {
+        dfree(*b);
+        *b = dalloc<uint32_t>(cap);
+      }
+    }
     ko_valid = false;
     cur = 0;
   }
@@ -437,8 +468,12 @@ struct Context final : CtxBase {
     inset_fixup_kernel<T><<<148, 256, 0, st>>>(cs, perm, T(cfg.inv_dx), cfg.resolution, dstat, step_idx);
     dilate_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(core, flags, D);
     exclusive_scan(flags, reinterpret_cast<uint32_t*>(dir), nd, scan_partials, st);
+    if (slab)
+      plane_start_kernel<<<(D + 1 + 127) / 128, 128, 0, st>>>(reinterpret_cast<const uint32_t*>(dir), flags, D,
+                                                             plane_start);
     compact_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(core, flags, dir, active, seg_begin, seg_end, nd,
                                                                pool_cap, dstat);
+    if (slab) slab_ranges_kernel<<<1, 1, 0, st>>>(plane_start, D, bx_lo, bx_hi, dstat);
     segments_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(skeys, n, seg_begin, seg_end);
   }
 
@@ -694,6 +729,172 @@ struct Context final : CtxBase {
     return CKG_OK;
   }
 
+  // ---------------------------------------------------------------- slabs
+  // Staged substep for the x-slab decomposition; the host moves the
+  // exchange buffers between stages (paper_2412_10399_b200/slab.py).
+  int slab_set(int rank, int world, int lo, int hi) override {
+    if (lo < 0 || hi > D || lo >= hi || rank < 0 || rank >= world) return CKG_ERR_CONFIG;
+    slab = true;
+    srank = rank;
+    sworld = world;
+    bx_lo = lo;
+    bx_hi = hi;
+    CKG_CUDA(cudaSetDevice(device));
+    dfree(plane_start);
+    plane_start = dalloc<uint32_t>(uint64_t(D) + 1);
+    return CKG_OK;
+  }
+
+  int plane_bx(int sel) const {
+    return sel == 0 ? bx_lo - 1 : sel == 1 ? bx_lo : sel == 2 ? bx_hi - 1 : bx_hi;
+  }
+
+  int slab_bin(double dt, void* core_out) override {
+    if (!slab) return CKG_ERR_CONFIG;
+    CKG_CUDA(cudaSetDevice(device));
+    launches = 0;
+    slab_dt = dt;
+    status_reset_kernel<<<1, 32, 0, st>>>(dstat, 1);
+    CKG_CUDA(cudaEventRecord(ev[0], st));
+    enqueue_sort();
+    CKG_CUDA(cudaMemcpyAsync(core_out, core, nd * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    return CKG_OK;
+  }
+
+  int slab_p2g(const void* core_in, uint64_t* plane_blocks) override {
+    CKG_CUDA(cudaSetDevice(device));
+    const StepConst<T> c = make_const(slab_dt);
+    CKG_CUDA(cudaMemcpyAsync(core, core_in, nd * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    CKG_CUDA(cudaEventRecord(ev[1], st));
+    enqueue_activate(0);
+    CKG_CUDA(cudaEventRecord(ev[2], st));
+    clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
+    CKG_CUDA(cudaEventRecord(ev[3], st));
+    if (!stress_valid) {
+      stress_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), c, dstat, 0);
+      stress_valid = true;
+    }
+    if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, 0);
+    else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_p2g<kSchemeApic>(c, 0);
+    else enqueue_p2g<kSchemeMls>(c, 0);
+    CKG_CUDA(cudaEventRecord(ev[4], st));
+    launches += 12;
+    std::vector<uint32_t> ps(uint64_t(D) + 1);
+    CKG_CUDA(cudaMemcpyAsync(ps.data(), plane_start, ps.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    for (int sel = 0; sel < 4; ++sel) {
+      const int bx = plane_bx(sel);
+      plane_blocks[sel] = (bx < 0 || bx >= D) ? 0 : uint64_t(ps[bx + 1] - ps[bx]);
+    }
+    return CKG_OK;
+  }
+
+  // op 0: pack plane -> buf, 1: add buf into plane, 2: copy buf into plane
+  int slab_halo(int op, int sel, void* buf) override {
+    const int bx = plane_bx(sel);
+    if (bx < 0 || bx >= D) return CKG_OK;
+    CKG_CUDA(cudaSetDevice(device));
+    halo_kernel<T><<<148 * 4, 256, 0, st>>>(pool, plane_start, bx, op, static_cast<T*>(buf));
+    launches += 1;
+    CKG_CUDA(cudaStreamSynchronize(st));
+    return CKG_OK;
+  }
+
+  int slab_grid() override {
+    CKG_CUDA(cudaSetDevice(device));
+    const StepConst<T> c = make_const(slab_dt);
+    grid_update_kernel<T><<<148 * 8, 256, 0, st>>>(pool, active, dstat, pool_cap, c, dbcs);
+    CKG_CUDA(cudaEventRecord(ev[5], st));
+    launches += 1;
+    return CKG_OK;
+  }
+
+  int slab_g2p(uint64_t* counts) override {
+    CKG_CUDA(cudaSetDevice(device));
+    const StepConst<T> c = make_const(slab_dt);
+    if (cfg.scheme == CKG_SCHEME_PIC) enqueue_g2p<kSchemePic>(c, 0);
+    else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_g2p<kSchemeApic>(c, 0);
+    else enqueue_g2p<kSchemeMls>(c, 0);
+    CKG_CUDA(cudaEventRecord(ev[6], st));
+    PState<T> nx = state(cur ^ 1);
+    classify_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(nx, T(cfg.inv_dx), D, bx_lo, bx_hi, fl_stay,
+                                                                   fl_left, fl_right);
+    exclusive_scan(fl_stay, pos_stay, n, scan_partials_n, st);
+    exclusive_scan(fl_left, pos_left, n, scan_partials_n, st);
+    exclusive_scan(fl_right, pos_right, n, scan_partials_n, st);
+    launches += 11;
+    uint32_t tail[6] = {0, 0, 0, 0, 0, 0};
+    if (n) {
+      CKG_CUDA(cudaMemcpyAsync(&tail[0], pos_stay + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CKG_CUDA(cudaMemcpyAsync(&tail[1], fl_stay + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CKG_CUDA(cudaMemcpyAsync(&tail[2], pos_left + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CKG_CUDA(cudaMemcpyAsync(&tail[3], fl_left + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CKG_CUDA(cudaMemcpyAsync(&tail[4], pos_right + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CKG_CUDA(cudaMemcpyAsync(&tail[5], fl_right + n - 1, 4, cudaMemcpyDeviceToHost, st));
+    }
+    CKG_CUDA(cudaStreamSynchronize(st));
+    n_stay = uint64_t(tail[0]) + tail[1];
+    mig_left = uint64_t(tail[2]) + tail[3];
+    mig_right = uint64_t(tail[4]) + tail[5];
+    counts[0] = mig_left;
+    counts[1] = mig_right;
+    return CKG_OK;
+  }
+
+  int slab_pack(uint64_t nl_in, void* left, void* right) override {
+    CKG_CUDA(cudaSetDevice(device));
+    if (nl_in + n_stay > cap) {
+      last_error = "slab: particle capacity of this rank exceeded";
+      return CKG_ERR_DEVICE;
+    }
+    // survivors -> the cur buffer at [nl_in, nl_in + n_stay) with their
+    // sorted keys of this substep (the next substep's ko); migrants -> records
+    PState<T> nx = state(cur ^ 1);
+    PState<T> dst = state(cur);
+    migrate_out_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
+        nx, skeys, fl_stay, pos_stay, fl_left, pos_left, fl_right, pos_right, dst, skeys_tmp, nl_in,
+        static_cast<T*>(left), static_cast<T*>(right));
+    launches += 1;
+    CKG_CUDA(cudaStreamSynchronize(st));
+    return CKG_OK;
+  }
+
+  int slab_finish(const void* left, uint64_t nl, const void* right, uint64_t nr, ckg_step_out* out) override {
+    CKG_CUDA(cudaSetDevice(device));
+    const uint64_t total = nl + n_stay + nr;
+    if (total > cap) {
+      last_error = "slab: particle capacity of this rank exceeded";
+      return CKG_ERR_DEVICE;
+    }
+    PState<T> dst = state(cur);
+    dst.n = total;
+    if (nl)
+      migrate_in_kernel<T><<<grid_for(nl, 256, 1 << 30), 256, 0, st>>>(static_cast<const T*>(left), nl, dst,
+                                                                       skeys_tmp, 0);
+    if (nr)
+      migrate_in_kernel<T><<<grid_for(nr, 256, 1 << 30), 256, 0, st>>>(static_cast<const T*>(right), nr, dst,
+                                                                       skeys_tmp, nl + n_stay);
+    launches += 2;
+    std::swap(ko, skeys_tmp);
+    ko_valid = true;  // [left keys][survivor keys][right keys] is non-decreasing
+    n = total;
+    CKG_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    ckg_step_out local;
+    if (!out) out = &local;
+    fill_out(out, true, CKG_PHASE_G2P);
+    out->kernel_launches = launches;
+    out->sort_changed = last_changed;
+    out->sort_kind = last_sort_kind;
+    grid_valid = true;
+    last_active = hstat->n_active;
+    int rc = decode_status(out, CKG_PHASE_G2P);
+    if (rc == CKG_OK) step_count += 1;
+    out->status = rc;
+    return rc;
+  }
+
   int timer_mark(int slot) override {
     if (slot < 0 || slot >= 16) return CKG_ERR_CONFIG;
     CKG_CUDA(cudaEventRecord(tev[slot], st));
@@ -884,6 +1085,41 @@ int32_t ckg_diagnostics_compute(ckg_ctx* ctx, ckg_diagnostics* out) {
   if (!ctx || !out) return CKG_ERR_CONFIG;
   return guard(ctx, "ckg_diagnostics_compute", [&] { return ctx->impl->diagnostics(out); });
 }
+
+int32_t ckg_slab_set(ckg_ctx* ctx, int32_t rank, int32_t world, int32_t bx_lo, int32_t bx_hi) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_set", [&] { return ctx->impl->slab_set(rank, world, bx_lo, bx_hi); });
+}
+int32_t ckg_slab_bin(ckg_ctx* ctx, double dt, void* core_out) {
+  if (!ctx || !core_out) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_bin", [&] { return ctx->impl->slab_bin(dt, core_out); });
+}
+int32_t ckg_slab_p2g(ckg_ctx* ctx, const void* core_in, uint64_t plane_blocks[4]) {
+  if (!ctx || !core_in || !plane_blocks) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_p2g", [&] { return ctx->impl->slab_p2g(core_in, plane_blocks); });
+}
+int32_t ckg_slab_halo(ckg_ctx* ctx, int32_t op, int32_t plane, void* buf) {
+  if (!ctx || op < 0 || op > 2 || plane < 0 || plane > 3) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_halo", [&] { return ctx->impl->slab_halo(op, plane, buf); });
+}
+int32_t ckg_slab_grid(ckg_ctx* ctx) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_grid", [&] { return ctx->impl->slab_grid(); });
+}
+int32_t ckg_slab_g2p(ckg_ctx* ctx, uint64_t counts[2]) {
+  if (!ctx || !counts) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_g2p", [&] { return ctx->impl->slab_g2p(counts); });
+}
+int32_t ckg_slab_pack(ckg_ctx* ctx, uint64_t nl_in, void* left, void* right) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_pack", [&] { return ctx->impl->slab_pack(nl_in, left, right); });
+}
+int32_t ckg_slab_finish(ckg_ctx* ctx, const void* left, uint64_t nl, const void* right, uint64_t nr,
+                        ckg_step_out* out) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_finish", [&] { return ctx->impl->slab_finish(left, nl, right, nr, out); });
+}
+int32_t ckg_slab_record_words(void) { return ckg::kMigrantWords; }
 
 int32_t ckg_timer_mark(ckg_ctx* ctx, int32_t slot) {
   if (!ctx) return CKG_ERR_CONFIG;

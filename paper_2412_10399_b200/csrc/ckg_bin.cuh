@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
   if (live) {
     T x[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) x[a] = __ldg(cur.f + uint64_t(kX + a) * cur.n + i);
+    for (int a = 0; a < 3; ++a) x[a] = __ldg(cur.f + uint64_t(kX + a) * cur.stride + i);
 #pragma unroll
     for (int a = 0; a < 3; ++a) kb[a] = key_axis(x[a], inv_dx, D);
     key = (uint32_t(kb[0]) * uint32_t(D) + uint32_t(kb[1])) * uint32_t(D) + uint32_t(kb[2]);
@@ -99,7 +99,7 @@ __global__ void inset_fixup_kernel(PState<T> cur, const uint32_t* __restrict__ p
     const uint32_t src = perm[i];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      if (!inset_ok(cur.f[uint64_t(kX + a) * cur.n + src], inv_dx, res)) {
+      if (!inset_ok(cur.f[uint64_t(kX + a) * cur.stride + src], inv_dx, res)) {
         record_error(st, step, kPhaseActivate, i, a, kErrOutOfDomain);
         break;
       }
@@ -151,7 +151,11 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t* __restrict__ cor
   core[d] = 0u;
   seg_begin[d] = 0u;
   seg_end[d] = 0u;
-  if (d == nd - 1) st->n_active = s + f;
+  if (d == nd - 1) {
+    st->n_active = s + f;
+    st->item_lo = st->grid_lo = st->clear_lo = 0u;
+    st->item_hi = st->grid_hi = st->clear_hi = s + f;
+  }
 }
 
 // [begin, end) of each block key's run in the sorted order.

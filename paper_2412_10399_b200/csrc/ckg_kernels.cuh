@@ -29,9 +29,10 @@ template <typename T>
 struct PState {
   T* f;           // kNumFields * n
   uint32_t* mat;  // n
-  T* tau;         // 6 * n: V0 * Kirchhoff stress of the current F (symmetric, xx xy xz yy yz zz)
-  uint64_t n;
-  __device__ __forceinline__ T& at(int k, uint64_t i) const { return f[uint64_t(k) * n + i]; }
+  T* tau;         // 6 fields: V0 * Kirchhoff stress of the current F (symmetric, xx xy xz yy yz zz)
+  uint64_t n;       // live particles in this window
+  uint64_t stride;  // distance between fields (buffer capacity); f/mat/tau may be offset into the buffer
+  __device__ __forceinline__ T& at(int k, uint64_t i) const { return f[uint64_t(k) * stride + i]; }
 };
 
 template <typename T>
@@ -72,6 +73,9 @@ struct DevStatus {
   unsigned int inset_fail;      // some particle violated the 2-cell inset (index fixed up after the sort)
   unsigned int nchanged;        // particles whose block key differs from the stored sorted key
   unsigned int work[4];         // persistent-kernel work counters (P2G, G2P)
+  unsigned int item_lo, item_hi;    // active-list range the transfer kernels walk
+  unsigned int grid_lo, grid_hi;    // slot range of the grid update
+  unsigned int clear_lo, clear_hi;  // slot range cleared before P2G
 };
 
 // err = step<<56 | phase<<52 | particle<<12 | axis<<8 | code
@@ -458,7 +462,7 @@ __device__ __forceinline__ M3<T> load_m3(const PState<T>& p, int k, uint64_t i) 
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) m.a[r][c] = __ldg(p.f + uint64_t(k + 3 * r + c) * p.n + i);
+    for (int c = 0; c < 3; ++c) m.a[r][c] = __ldg(p.f + uint64_t(k + 3 * r + c) * p.stride + i);
   return m;
 }
 
@@ -467,7 +471,7 @@ __device__ __forceinline__ void store_m3(const PState<T>& p, int k, uint64_t i, 
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) p.f[uint64_t(k + 3 * r + c) * p.n + i] = m.a[r][c];
+    for (int c = 0; c < 3; ++c) p.f[uint64_t(k + 3 * r + c) * p.stride + i] = m.a[r][c];
 }
 
 

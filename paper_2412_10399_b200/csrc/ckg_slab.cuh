@@ -1,0 +1,145 @@
+// ckg_slab.cuh — x-slab decomposition kernels.
+//
+// Each rank owns block planes bx in [bx_lo, bx_hi) and the particles whose
+// sort key lies there.  The block directory is global and identical on every
+// rank (the footprint flags are MAX-all-reduced before activation), and the
+// active list is in directory order, so every block plane bx occupies the
+// contiguous slot range [plane_start[bx], plane_start[bx+1]) on all ranks:
+// halo exchanges are contiguous slices of the block pool, no coordinate
+// matching.  Per substep:
+//   P2G writes ghost planes bx_lo-1 and bx_hi  -> sent to the owners, added
+//   grid update on owned planes                -> boundary planes sent back
+//   G2P on owned particles                     -> migrants (new key outside
+//   [bx_lo, bx_hi)) packed in order and sent; the receiver builds
+//   [left migrants][survivors][right migrants], which the next substep's
+//   stable sort turns into the global stable order restricted to the slab.
+#pragma once
+
+#include <cstdint>
+
+#include "ckg_kernels.cuh"
+
+namespace ckg {
+
+// plane_start[bx] = first slot of block plane bx: the exclusive scan of the
+// active flags at directory index (bx, 0, 0) (read before compaction).
+__global__ void plane_start_kernel(const uint32_t* __restrict__ scan_of_act, const uint32_t* __restrict__ act,
+                                   int D, uint32_t* __restrict__ plane_start) {
+  const int bx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bx > D) return;
+  if (bx == D) {
+    const uint64_t last = uint64_t(D) * D * D - 1;
+    plane_start[D] = scan_of_act[last] + act[last];
+    return;
+  }
+  plane_start[bx] = scan_of_act[uint64_t(bx) * D * D];
+}
+
+// Work ranges of this rank after compaction: transfer items (own planes),
+// grid update (own planes), clear (own planes and both ghost planes).
+__global__ void slab_ranges_kernel(const uint32_t* __restrict__ plane_start, int D, int bx_lo, int bx_hi,
+                                   DevStatus* st) {
+  const int g0 = bx_lo > 0 ? bx_lo - 1 : 0, g1 = bx_hi < D ? bx_hi + 1 : D;
+  st->item_lo = plane_start[bx_lo];
+  st->item_hi = plane_start[bx_hi];
+  st->grid_lo = plane_start[bx_lo];
+  st->grid_hi = plane_start[bx_hi];
+  st->clear_lo = plane_start[g0];
+  st->clear_hi = plane_start[g1];
+}
+
+// op 0: dst[...] = pool plane; op 1: pool plane += src; op 2: pool plane = src.
+template <typename T>
+__global__ void halo_kernel(T* __restrict__ pool, const uint32_t* __restrict__ plane_start, int bx, int op,
+                            T* __restrict__ buf) {
+  const uint64_t s0 = plane_start[bx], s1 = plane_start[bx + 1];
+  const uint64_t total = (s1 - s0) * kBlockVals;
+  T* p = pool + s0 * kBlockVals;
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total; k += uint64_t(gridDim.x) * blockDim.x) {
+    if (op == 0)
+      buf[k] = p[k];
+    else if (op == 1)
+      p[k] += buf[k];
+    else
+      p[k] = buf[k];
+  }
+}
+
+// Migration class of each particle of the new state: 0 stays, 1 left, 2 right.
+template <typename T>
+__global__ void classify_kernel(PState<T> st_new, T inv_dx, int D, int bx_lo, int bx_hi,
+                                uint32_t* __restrict__ stay, uint32_t* __restrict__ left,
+                                uint32_t* __restrict__ right) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= st_new.n) return;
+  const int bx = key_axis(st_new.f[uint64_t(kX) * st_new.stride + i], inv_dx, D);
+  const uint32_t l = bx < bx_lo, r = bx >= bx_hi;
+  left[i] = l;
+  right[i] = r;
+  stay[i] = (l | r) ? 0u : 1u;
+}
+
+// Migrant record: 27 state fields, material (bit pattern in a T word), the 6
+// stress-cache values and the particle's previous sorted key (a T word).
+constexpr int kMigrantWords = kNumFields + 1 + 6 + 1;
+
+template <typename T>
+__device__ __forceinline__ T word_of(uint32_t v) {
+  T w = T(0);
+  *reinterpret_cast<uint32_t*>(&w) = v;
+  return w;
+}
+template <typename T>
+__device__ __forceinline__ uint32_t word_to_u32(T w) {
+  return *reinterpret_cast<const uint32_t*>(&w);
+}
+
+// Survivors -> dst (at pos_stay + offset, with their old keys), migrants of
+// the chosen sides -> records at their scanned positions.
+template <typename T>
+__global__ void migrate_out_kernel(PState<T> src, const uint32_t* __restrict__ src_oldkey,
+                                   const uint32_t* __restrict__ stay, const uint32_t* __restrict__ pos_stay,
+                                   const uint32_t* __restrict__ left, const uint32_t* __restrict__ pos_left,
+                                   const uint32_t* __restrict__ right, const uint32_t* __restrict__ pos_right,
+                                   PState<T> dst, uint32_t* __restrict__ dst_oldkey, uint64_t offset,
+                                   T* __restrict__ rec_left, T* __restrict__ rec_right) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= src.n) return;
+  if (stay[i]) {
+    const uint64_t j = pos_stay[i] + offset;
+#pragma unroll 4
+    for (int k = 0; k < kNumFields; ++k) dst.f[uint64_t(k) * dst.stride + j] = src.f[uint64_t(k) * src.stride + i];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) dst.tau[uint64_t(k) * dst.stride + j] = src.tau[uint64_t(k) * src.stride + i];
+    dst.mat[j] = src.mat[i];
+    dst_oldkey[j] = src_oldkey[i];
+    return;
+  }
+  T* rec = left[i] ? rec_left + uint64_t(pos_left[i]) * kMigrantWords
+                   : rec_right + uint64_t(pos_right[i]) * kMigrantWords;
+  (void)right;
+#pragma unroll 4
+  for (int k = 0; k < kNumFields; ++k) rec[k] = src.f[uint64_t(k) * src.stride + i];
+  rec[kNumFields] = word_of<T>(src.mat[i]);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) rec[kNumFields + 1 + k] = src.tau[uint64_t(k) * src.stride + i];
+  rec[kNumFields + 7] = word_of<T>(src_oldkey[i]);
+}
+
+// Received records -> dst positions [offset, offset + count).
+template <typename T>
+__global__ void migrate_in_kernel(const T* __restrict__ rec, uint64_t count, PState<T> dst,
+                                  uint32_t* __restrict__ dst_oldkey, uint64_t offset) {
+  const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= count) return;
+  const T* p = rec + r * kMigrantWords;
+  const uint64_t j = offset + r;
+#pragma unroll 4
+  for (int k = 0; k < kNumFields; ++k) dst.f[uint64_t(k) * dst.stride + j] = p[k];
+  dst.mat[j] = word_to_u32(p[kNumFields]);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) dst.tau[uint64_t(k) * dst.stride + j] = p[kNumFields + 1 + k];
+  dst_oldkey[j] = word_to_u32(p[kNumFields + 7]);
+}
+
+}  // namespace ckg

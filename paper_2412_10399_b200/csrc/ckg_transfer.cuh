@@ -77,13 +77,13 @@ __global__ void __launch_bounds__(kXferThreads, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   T* wt = tiles + warp * kTileVals;
   for (int e = tid; e < kXferWarps * kTileVals; e += kXferThreads) tiles[e] = T(0);
-  const uint32_t na = min(st->n_active, cap);
+  const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const uint32_t lt = lanemask_lt();
   const int D = c.D;
   const T dx = c.dx, dt = c.dt;
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_item = atomicAdd(&st->work[0], 1u);
+    if (tid == 0) s_item = item0 + atomicAdd(&st->work[0], 1u);
     __syncthreads();
     const uint32_t item = s_item;
     if (item >= na) break;
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kXferThreads, 2)
           uint32_t q = 0;
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
-            const T sa = sub_rn(over_dx(__ldg(cur.f + uint64_t(kX + a) * cur.n + src), dx, c.inv_dx, c.pow2), T(0.25));
+            const T sa = sub_rn(over_dx(__ldg(cur.f + uint64_t(kX + a) * cur.stride + src), dx, c.inv_dx, c.pow2), T(0.25));
             q |= ((sa - dfloor(sa)) >= T(0.5) ? 1u : 0u) << a;
           }
           myq[r] = q;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kXferThreads, 2)
       Dual<T> ds;
       if (valid) {
         const uint32_t src = __ldg(perm + i);
-        const uint64_t n = cur.n;
+        const uint64_t n = cur.stride;  // field stride (buffer capacity)
         x = __ldg(cur.f + kX * n + src);
         y = __ldg(cur.f + (kX + 1) * n + src);
         z = __ldg(cur.f + (kX + 2) * n + src);
@@ -339,13 +339,14 @@ template <typename T>
 __global__ void grid_update_kernel(T* __restrict__ pool, const uint32_t* __restrict__ active,
                                    const DevStatus* st, uint32_t cap, StepConst<T> c,
                                    const BcParam<T>* __restrict__ bcs) {
-  uint32_t na = st->n_active;
-  if (na > cap) na = cap;
-  const uint64_t total = uint64_t(na) * 128;
+  const uint32_t g0 = st->grid_lo;
+  uint32_t g1 = st->grid_hi;
+  if (g1 > cap) g1 = cap;
+  const uint64_t total = g1 > g0 ? uint64_t(g1 - g0) * 128 : 0;
   const int D = c.D;
   for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
        k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t slot = uint32_t(k >> 7);
+    const uint32_t slot = g0 + uint32_t(k >> 7);
     const int g = int(k >> 6) & 1;
     const int l = int(k & 63);
     T* base = pool + uint64_t(slot) * kBlockVals + g * 256 + l;
@@ -446,13 +447,13 @@ __global__ void __launch_bounds__(kXferThreads, CKG_G2P_MINB)
   __shared__ uint32_t s_item;
   __shared__ T wmax[kXferWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t na = min(st->n_active, cap);
+  const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const int D = c.D;
   const T dx = c.dx, dt = c.dt;
   T vmax2 = T(0);
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_item = atomicAdd(&st->work[1], 1u);
+    if (tid == 0) s_item = item0 + atomicAdd(&st->work[1], 1u);
     __syncthreads();
     const uint32_t item = s_item;
     if (item >= na) break;
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_G2P_MINB)
       uint32_t mi = 0;
       if (live) {
         const uint32_t src = __ldg(perm + i);
-        const uint64_t n = cur.n;
+        const uint64_t n = cur.stride;  // field stride (buffer capacity)
         T x = __ldg(cur.f + kX * n + src), y = __ldg(cur.f + (kX + 1) * n + src),
           z = __ldg(cur.f + (kX + 2) * n + src);
         T v[3] = {T(0), T(0), T(0)};
@@ -664,21 +665,22 @@ __global__ void __launch_bounds__(256) stress_kernel(PState<T> cur, StepConst<T>
   if (i >= cur.n) return;
   const uint32_t mi = cur.mat[i];
   T t6[6];
-  const int e = stress_tau6(load_m3(cur, kF, i), cur.f[kJ * cur.n + i], cur.f[kVol * cur.n + i],
+  const int e = stress_tau6(load_m3(cur, kF, i), cur.f[kJ * cur.stride + i], cur.f[kVol * cur.stride + i],
                             c.mats[mi < kMaxMaterials ? mi : 0], t6);
   if (e) record_error(st, step, kPhaseP2G, i, 0, e);
 #pragma unroll
-  for (int k = 0; k < 6; ++k) cur.tau[uint64_t(k) * cur.n + i] = e ? T(0) : t6[k];
+  for (int k = 0; k < 6; ++k) cur.tau[uint64_t(k) * cur.stride + i] = e ? T(0) : t6[k];
 }
 
 // K4: clear the active part of the pool (grid.hpp:148-151).
 template <typename T>
 __global__ void clear_kernel(T* __restrict__ pool, const DevStatus* st, uint32_t cap) {
-  uint32_t na = st->n_active;
-  if (na > cap) na = cap;
-  const uint64_t total = uint64_t(na) * kBlockVals / 2;  // in 16-byte words (double2 / float4-ish)
+  const uint32_t c0 = st->clear_lo;
+  uint32_t c1 = st->clear_hi;
+  if (c1 > cap) c1 = cap;
+  const uint64_t total = c1 > c0 ? uint64_t(c1 - c0) * kBlockVals / 2 : 0;  // in 2-element words
   using W = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
-  W* p = reinterpret_cast<W*>(pool);
+  W* p = reinterpret_cast<W*>(pool + uint64_t(c0) * kBlockVals);
   W zero;
   zero.x = T(0);
   zero.y = T(0);
@@ -711,7 +713,7 @@ __global__ void aos_to_soa_kernel(const T* __restrict__ aos, PState<T> p) {
     const uint64_t i = k / W;
     const int f = int(k - i * W);
     if (f < kNumFields)
-      p.f[uint64_t(f) * p.n + i] = aos[k];
+      p.f[uint64_t(f) * p.stride + i] = aos[k];
     else
       p.mat[i] = *reinterpret_cast<const uint32_t*>(aos + k);
   }
@@ -726,7 +728,7 @@ __global__ void soa_to_aos_kernel(PState<T> p, T* __restrict__ aos) {
     const uint64_t i = k / W;
     const int f = int(k - i * W);
     if (f < kNumFields) {
-      aos[k] = p.f[uint64_t(f) * p.n + i];
+      aos[k] = p.f[uint64_t(f) * p.stride + i];
     } else {
       T word = T(0);
       *reinterpret_cast<uint32_t*>(&word) = p.mat[i];
@@ -745,7 +747,7 @@ __global__ void bases_kernel(PState<T> p, T dx, T inv_dx, int pow2, int32_t* __r
     const T kq = g == 0 ? T(-0.25) : T(0.25);
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-      out[(i * 2 + g) * 3 + a] = axis_base(p.f[uint64_t(kX + a) * p.n + i], dx, inv_dx, pow2, kq);
+      out[(i * 2 + g) * 3 + a] = axis_base(p.f[uint64_t(kX + a) * p.stride + i], dx, inv_dx, pow2, kq);
   }
 }
 
@@ -786,9 +788,9 @@ __global__ void diagnostics_kernel(PState<T> p, double* __restrict__ acc /* 10 s
   double vm = 0;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.n;
        i += uint64_t(gridDim.x) * blockDim.x) {
-    const double m = double(p.f[kMass * p.n + i]);
-    const double x[3] = {double(p.f[kX * p.n + i]), double(p.f[(kX + 1) * p.n + i]), double(p.f[(kX + 2) * p.n + i])};
-    const double v[3] = {double(p.f[kV * p.n + i]), double(p.f[(kV + 1) * p.n + i]), double(p.f[(kV + 2) * p.n + i])};
+    const double m = double(p.f[kMass * p.stride + i]);
+    const double x[3] = {double(p.f[kX * p.stride + i]), double(p.f[(kX + 1) * p.stride + i]), double(p.f[(kX + 2) * p.stride + i])};
+    const double v[3] = {double(p.f[kV * p.stride + i]), double(p.f[(kV + 1) * p.stride + i]), double(p.f[(kV + 2) * p.stride + i])};
     s[0] += v[0] * m;
     s[1] += v[1] * m;
     s[2] += v[2] * m;

@@ -1,0 +1,441 @@
+"""x-slab decomposition of the CK-MPM substep over several GPUs.
+
+One process (rank) per GPU owns the block planes bx in [bx_lo, bx_hi) and
+the particles whose sort key lies there.  The device work of a substep runs in
+the library (libckmpm_b200.so, csrc/ckg_slab.cuh); between its stages this
+module moves the exchange buffers:
+
+  1. footprint flags of every rank, MAX-all-reduced -> identical global block
+     directory, so a block plane is the same contiguous pool slice everywhere;
+  2. after P2G: ghost planes (bx_lo-1, bx_hi) sent to their owners and added
+     (halo reduce-add of mass + momentum, both grids);
+  3. after the grid update: boundary planes sent back into the neighbours'
+     ghost planes (halo broadcast of velocities);
+  4. after G2P: migrant counts, then migrant records; each rank rebuilds
+     [left migrants][survivors][right migrants], which the next substep's
+     stable sort turns into the global stable order restricted to the slab
+     (bit-identical binning and order to a single-domain run);
+  5. vmax / min J all-reduced for the CFL step.
+
+The substep is a generator (`SlabRank.stages`) that yields exchange requests,
+so the same code runs over torch.distributed (NCCL on GPUs, gloo on CPU) or
+in-process over several contexts on one GPU (`run_loopback`, used by the
+tests: no kernel ever waits on another rank's kernel).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from .scene import SceneConfig, mass_epsilon, seed_particles, to_abi_config
+
+
+# ------------------------------------------------------------- partitioning
+
+def block_x_of(particles: np.ndarray, cfg: SceneConfig, precision: int = 8) -> np.ndarray:
+    """Sort-key block x (simulation.hpp:256-261), exact in T."""
+    T = np.float64 if precision == 8 else np.float32
+    dx = cfg.dx(precision)
+    inv_dx = T(1) / dx
+    D = cfg.resolution // 4 + 2
+    x = particles["x"][:, 0].astype(T)
+    b = np.floor(x * inv_dx + T(0.25)).astype(np.int64) >> 2
+    return np.clip(b, 0, D - 1)
+
+
+def partition_planes(plane_counts: np.ndarray, world: int) -> List[int]:
+    """Slab boundaries X_0=0 < X_1 < ... < X_world=D over block planes,
+    balancing particle counts (prefix-sum split); every rank gets >= 1 plane."""
+    D = len(plane_counts)
+    if world > D:
+        raise ValueError("more ranks than block planes")
+    cum = np.concatenate([[0], np.cumsum(plane_counts)])
+    total = cum[-1]
+    bounds = [0]
+    for r in range(1, world):
+        target = total * r / world
+        x = int(np.searchsorted(cum, target, side="left"))
+        x = max(x, bounds[-1] + 1)
+        x = min(x, D - (world - r))
+        bounds.append(x)
+    bounds.append(D)
+    return bounds
+
+
+def split_particles(particles: np.ndarray, cfg: SceneConfig, world: int, precision: int = 8):
+    """Global stable order by key (the reference's sort_particles), then the
+    contiguous slab ranges of it.  Returns (bounds, [per-rank arrays])."""
+    D = cfg.resolution // 4 + 2
+    T = np.float64 if precision == 8 else np.float32
+    dx = cfg.dx(precision)
+    inv_dx = T(1) / dx
+    c = np.clip(np.floor(particles["x"].astype(T) * inv_dx + T(0.25)).astype(np.int64) >> 2, 0, D - 1)
+    key = (c[:, 0] * D + c[:, 1]) * D + c[:, 2]
+    order = np.argsort(key, kind="stable")
+    ps = particles[order]
+    bx = c[order, 0]
+    counts = np.bincount(bx, minlength=D)
+    bounds = partition_planes(counts, world)
+    parts = [ps[(bx >= bounds[r]) & (bx < bounds[r + 1])] for r in range(world)]
+    return bounds, parts
+
+
+# --------------------------------------------------------------- requests
+
+@dataclass
+class AllReduceMax:
+    buf: object           # torch.Tensor (int32, device)
+
+
+@dataclass
+class Neighbor:
+    send_left: Optional[object]
+    send_right: Optional[object]
+    recv_left: Optional[object]
+    recv_right: Optional[object]
+
+
+@dataclass
+class Counts:
+    """Exchange two integers with the neighbours: send (to_left, to_right),
+    receive (from_left, from_right) into `out` (list of 2)."""
+    to_left: int
+    to_right: int
+    out: list
+
+
+@dataclass
+class Scalars:
+    """All-reduce [vmax, -minJ...] by max and error flags by max."""
+    values: np.ndarray
+    out: list
+
+
+def _check(lib, ctx, rc, what):
+    if rc != 0:
+        buf = C.create_string_buffer(512)
+        lib.ckg_last_error_message(ctx, buf, 512)
+        raise RuntimeError(f"{what}: status {rc}: {buf.value.decode()}")
+
+
+class SlabRank:
+    """One rank of the x-slab decomposition (one ckg context, one GPU)."""
+
+    def __init__(self, cfg: SceneConfig, rank: int, world: int, bounds: Sequence[int], particles: np.ndarray,
+                 mass_eps: float, precision: int = 8, device: int = 0):
+        import torch
+
+        from ._lib import lib
+        self.lib = lib()
+        self.torch = torch
+        self.cfg = cfg
+        self.rank, self.world = rank, world
+        self.bx_lo, self.bx_hi = int(bounds[rank]), int(bounds[rank + 1])
+        self.precision = precision
+        self.T = np.float64 if precision == 8 else np.float32
+        self.tdtype = torch.float64 if precision == 8 else torch.float32
+        self.device = torch.device("cuda", device)
+        self._abi_cfg = to_abi_config(cfg, precision, mass_eps, device)
+        ctx = C.c_void_p()
+        rc = self.lib.ckg_create(C.byref(self._abi_cfg), C.byref(ctx))
+        if rc != 0:
+            raise RuntimeError(f"ckg_create failed ({rc})")
+        self.ctx = ctx
+        _check(self.lib, ctx, self.lib.ckg_slab_set(ctx, rank, world, self.bx_lo, self.bx_hi), "ckg_slab_set")
+        p = np.ascontiguousarray(particles, dtype=abi.particle_dtype(precision))
+        _check(self.lib, ctx, self.lib.ckg_upload(ctx, abi.ptr(p), len(p)), "ckg_upload")
+        self.n = len(p)
+        D = cfg.resolution // 4 + 2
+        self.core = torch.zeros(D * D * D, dtype=torch.int32, device=self.device)
+        self.block_words = 512
+        self.rec_words = int(self.lib.ckg_slab_record_words())
+        self.out = abi.StepOut()
+        self.vmax = 0.0
+        self.min_j = [1.0] * len(cfg.materials)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.ckg_destroy(self.ctx)
+            self.ctx = None
+
+    def _buf(self, blocks_or_recs: int, words: int):
+        return self.torch.empty(max(1, blocks_or_recs) * words, dtype=self.tdtype, device=self.device)
+
+    def stages(self, dt: float):
+        """One substep; yields exchange requests (see module docstring)."""
+        lib, ctx = self.lib, self.ctx
+        has_l, has_r = self.rank > 0, self.rank < self.world - 1
+        _check(lib, ctx, lib.ckg_slab_bin(ctx, float(dt), C.c_void_p(self.core.data_ptr())), "ckg_slab_bin")
+        yield AllReduceMax(self.core)
+        planes = (C.c_uint64 * 4)()
+        _check(lib, ctx, lib.ckg_slab_p2g(ctx, C.c_void_p(self.core.data_ptr()), planes), "ckg_slab_p2g")
+        pb = [int(v) for v in planes]  # blocks of planes ghostL, ownL, ownR, ghostR
+        W = self.block_words
+        # halo reduce-add: ghost planes -> owners
+        send_l = self._buf(pb[0], W) if has_l else None
+        send_r = self._buf(pb[3], W) if has_r else None
+        if send_l is not None:
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 0, C.c_void_p(send_l.data_ptr())), "halo pack")
+        if send_r is not None:
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 3, C.c_void_p(send_r.data_ptr())), "halo pack")
+        recv_l = self._buf(pb[1], W) if has_l else None
+        recv_r = self._buf(pb[2], W) if has_r else None
+        yield Neighbor(send_l, send_r, recv_l, recv_r)
+        if recv_l is not None:
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 1, 1, C.c_void_p(recv_l.data_ptr())), "halo add")
+        if recv_r is not None:
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 1, 2, C.c_void_p(recv_r.data_ptr())), "halo add")
+        _check(lib, ctx, lib.ckg_slab_grid(ctx), "ckg_slab_grid")
+        # halo broadcast of velocities: own boundary planes -> neighbours' ghosts
+        send_l = self._buf(pb[1], W) if has_l else None
+        send_r = self._buf(pb[2], W) if has_r else None
+        if send_l is not None:
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 1, C.c_void_p(send_l.data_ptr())), "vel pack")
+        if send_r is not None:
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 2, C.c_void_p(send_r.data_ptr())), "vel pack")
+        recv_l = self._buf(pb[0], W) if has_l else None
+        recv_r = self._buf(pb[3], W) if has_r else None
+        yield Neighbor(send_l, send_r, recv_l, recv_r)
+        if recv_l is not None:
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 2, 0, C.c_void_p(recv_l.data_ptr())), "vel set")
+        if recv_r is not None:
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 2, 3, C.c_void_p(recv_r.data_ptr())), "vel set")
+        # G2P and migration
+        counts = (C.c_uint64 * 2)()
+        _check(lib, ctx, lib.ckg_slab_g2p(ctx, counts), "ckg_slab_g2p")
+        out_l, out_r = int(counts[0]), int(counts[1])
+        if (out_l and not has_l) or (out_r and not has_r):
+            raise RuntimeError("particle left the global domain through a slab edge")
+        got = [0, 0]
+        yield Counts(out_l, out_r, got)
+        nl_in, nr_in = got
+        R = self.rec_words
+        send_l, send_r = self._buf(out_l, R), self._buf(out_r, R)
+        _check(lib, ctx, lib.ckg_slab_pack(ctx, nl_in, C.c_void_p(send_l.data_ptr()), C.c_void_p(send_r.data_ptr())),
+               "ckg_slab_pack")
+        recv_l, recv_r = self._buf(nl_in, R), self._buf(nr_in, R)
+        yield Neighbor(send_l[: out_l * R] if has_l else None, send_r[: out_r * R] if has_r else None,
+                       recv_l[: nl_in * R] if has_l else None, recv_r[: nr_in * R] if has_r else None)
+        rc = lib.ckg_slab_finish(ctx, C.c_void_p(recv_l.data_ptr()), nl_in, C.c_void_p(recv_r.data_ptr()), nr_in,
+                                 C.byref(self.out))
+        # errors travel through the all-reduce below so every rank stops together
+        self.out.status = rc
+        self.n = self.n - out_l - out_r + nl_in + nr_in
+        vals = np.array([self.out.vmax] + [-float(self.out.min_j[m]) for m in range(len(self.cfg.materials))]
+                        + [float(self.out.status)], dtype=np.float64)
+        red = [None]
+        yield Scalars(vals, red)
+        r = red[0]
+        self.vmax = float(r[0])
+        self.min_j = [-float(v) for v in r[1:1 + len(self.cfg.materials)]]
+        if r[-1] != 0:
+            buf = C.create_string_buffer(512)
+            lib.ckg_last_error_message(ctx, buf, 512)
+            raise RuntimeError(f"slab substep failed on some rank (local: {buf.value.decode() or 'ok'})")
+
+    def particles(self) -> np.ndarray:
+        out = np.zeros(self.n, dtype=abi.particle_dtype(self.precision))
+        _check(self.lib, self.ctx, self.lib.ckg_download(self.ctx, abi.ptr(out), self.n), "ckg_download")
+        return out
+
+    def cfl_dt(self, remaining: float) -> float:
+        """cfl_dt (simulation.hpp:134-145) from the all-reduced vmax / min J."""
+        T = self.T
+        cmax = T(0)
+        for mi, m in enumerate(self.cfg.materials):
+            if m.is_fluid:
+                c = T(np.sqrt(T(m.bulk) * T(m.gamma) * T(np.power(T(self.min_j[mi]), T(1) - T(m.gamma)))
+                              / T(m.density)))
+            else:
+                c = T(np.sqrt((T(m.lam) + T(2) * T(m.mu)) / T(m.density)))
+            cmax = c if cmax < c else cmax
+        vmax = T(self.vmax)
+        denom = cmax if vmax < cmax else vmax
+        dt = T(self.cfg.cfl) * self.cfg.dx(self.precision) / denom if denom > 0 else T(remaining)
+        if T(self.cfg.max_dt) > 0:
+            dt = min(dt, T(self.cfg.max_dt))
+        return float(min(dt, T(remaining)))
+
+
+# ------------------------------------------------------------- transports
+
+def run_loopback(ranks: List[SlabRank], dt: float):
+    """Drive all ranks' stages in lock step inside one process (one GPU):
+    exchanges are device-to-device copies between the ranks' buffers."""
+    gens = [r.stages(dt) for r in ranks]
+    world = len(ranks)
+    while True:
+        reqs = []
+        done = False
+        for g in gens:
+            try:
+                reqs.append(next(g))
+            except StopIteration:
+                done = True
+        if done:
+            assert len(reqs) == 0, "ranks out of step"
+            return
+        kind = type(reqs[0])
+        assert all(type(q) is kind for q in reqs), "ranks out of step"
+        if kind is AllReduceMax:
+            acc = reqs[0].buf.clone()
+            for q in reqs[1:]:
+                acc = ranks[0].torch.maximum(acc, q.buf)
+            for q in reqs:
+                q.buf.copy_(acc)
+        elif kind is Neighbor:
+            for r, q in enumerate(reqs):
+                if r > 0 and q.recv_left is not None:
+                    q.recv_left.copy_(reqs[r - 1].send_right)
+                if r < world - 1 and q.recv_right is not None:
+                    q.recv_right.copy_(reqs[r + 1].send_left)
+        elif kind is Counts:
+            for r, q in enumerate(reqs):
+                q.out[0] = reqs[r - 1].to_right if r > 0 else 0
+                q.out[1] = reqs[r + 1].to_left if r < world - 1 else 0
+        elif kind is Scalars:
+            m = np.max(np.stack([q.values for q in reqs]), axis=0)
+            for q in reqs:
+                q.out[0] = m
+        # torch copies run on torch's stream; the library on its own
+        ranks[0].torch.cuda.synchronize()
+
+
+class DistTransport:
+    """torch.distributed transport (NCCL for device buffers; works with gloo
+    for CPU tensors too).  Neighbours are rank-1 / rank+1 (no wrap)."""
+
+    def __init__(self, dist, rank: int, world: int, device):
+        self.dist, self.rank, self.world, self.device = dist, rank, world, device
+        # gloo cannot move CUDA tensors point-to-point: stage through host
+        # memory (used to run several ranks on one GPU in tests)
+        self.host_staged = dist.get_backend() == "gloo" and getattr(device, "type", "cpu") == "cuda"
+        self.comm_device = "cpu" if self.host_staged else device
+
+    def _out(self, t):
+        return t.cpu() if (self.host_staged and t is not None) else t
+
+    def handle(self, req):
+        import torch
+        d = self.dist
+        if isinstance(req, AllReduceMax):
+            buf = self._out(req.buf)
+            d.all_reduce(buf, op=d.ReduceOp.MAX)
+            if buf is not req.buf:
+                req.buf.copy_(buf)
+        elif isinstance(req, Neighbor):
+            sl, sr = self._out(req.send_left), self._out(req.send_right)
+            rl, rr = self._out(req.recv_left), self._out(req.recv_right)
+            ops = []
+            if self.rank > 0:
+                if sl is not None:
+                    ops.append(d.P2POp(d.isend, sl.contiguous(), self.rank - 1))
+                if rl is not None:
+                    ops.append(d.P2POp(d.irecv, rl, self.rank - 1))
+            if self.rank < self.world - 1:
+                if sr is not None:
+                    ops.append(d.P2POp(d.isend, sr.contiguous(), self.rank + 1))
+                if rr is not None:
+                    ops.append(d.P2POp(d.irecv, rr, self.rank + 1))
+            ops = [o for o in ops if o.tensor.numel() > 0]
+            if ops:
+                for w in d.batch_isend_irecv(ops):
+                    w.wait()
+            if rl is not None and rl is not req.recv_left:
+                req.recv_left.copy_(rl)
+            if rr is not None and rr is not req.recv_right:
+                req.recv_right.copy_(rr)
+        elif isinstance(req, Counts):
+            t = torch.tensor([req.to_left, req.to_right], dtype=torch.int64, device=self.comm_device)
+            allc = [torch.zeros(2, dtype=torch.int64, device=self.comm_device) for _ in range(self.world)]
+            d.all_gather(allc, t)
+            req.out[0] = int(allc[self.rank - 1][1]) if self.rank > 0 else 0
+            req.out[1] = int(allc[self.rank + 1][0]) if self.rank < self.world - 1 else 0
+        elif isinstance(req, Scalars):
+            t = torch.tensor(req.values, dtype=torch.float64, device=self.comm_device)
+            d.all_reduce(t, op=d.ReduceOp.MAX)
+            req.out[0] = t.cpu().numpy()
+
+    def step(self, rank_obj: SlabRank, dt: float):
+        import torch
+        for req in rank_obj.stages(dt):
+            self.handle(req)
+            # the library runs on its own (non-blocking) stream: make the
+            # received data visible before handing control back to it
+            if torch.cuda.is_available():
+                torch.cuda.synchronize()
+
+
+def build_ranks(cfg: SceneConfig, world: int, precision: int = 8, particles: Optional[np.ndarray] = None,
+                devices: Optional[Sequence[int]] = None, only_rank: Optional[int] = None):
+    """Seed (or take) the global particle set, split it into slabs and build
+    the rank objects (all of them for loopback, one for a real rank)."""
+    p = seed_particles(cfg, precision) if particles is None else particles
+    me = mass_epsilon(p, precision)  # global median, as the single-domain run
+    bounds, parts = split_particles(p, cfg, world, precision)
+    # refresh_velocity_stats (simulation.hpp:234-243) over the global set
+    T = np.float64 if precision == 8 else np.float32
+    v = p["v"].astype(T)
+    vmax = float(np.max(np.sqrt((v[:, 0] * v[:, 0] + v[:, 1] * v[:, 1]) + v[:, 2] * v[:, 2]))) if len(p) else 0.0
+    min_j = [1.0] * len(cfg.materials)
+    for mi, m in enumerate(cfg.materials):
+        sel = p["J"][p["material"] == mi]
+        if m.is_fluid and len(sel):
+            min_j[mi] = min(1.0, float(np.min(sel)))
+    ranks = []
+    for r in range(world):
+        if only_rank is not None and r != only_rank:
+            continue
+        dev = devices[r] if devices else 0
+        rk = SlabRank(cfg, r, world, bounds, parts[r], me, precision, dev)
+        rk.vmax, rk.min_j = vmax, list(min_j)
+        ranks.append(rk)
+    return bounds, ranks
+
+
+def build_rank_for_box(cfg: SceneConfig, world: int, rank: int, precision: int = 8, device: int = 0):
+    """Rank-local seeding for single-box scenes (the bench's C5 family): the
+    slab bounds come from the x-marginal of the lattice, and each rank seeds
+    only the part of the box whose sort-key plane it owns.  Seeding order is
+    the lattice order restricted to the slab, i.e. exactly the slab's part of
+    the global stable sort (no rank ever holds the whole body)."""
+    import copy
+
+    assert len(cfg.bodies) == 1 and cfg.bodies[0].shape.kind == "box" and cfg.bodies[0].ppc in (8, 27)
+    T = np.float64 if precision == 8 else np.float32
+    dx = cfg.dx(precision)
+    inv_dx = T(1) / dx
+    D = cfg.resolution // 4 + 2
+    body = cfg.bodies[0]
+    lo, hi = [T(v) for v in body.shape.lo], [T(v) for v in body.shape.hi]
+    nsub = 2 if body.ppc == 8 else 3
+    offs = np.array([T(2 * s + 1) / T(2 * nsub) for s in range(nsub)], dtype=T)
+    i0, i1 = int(np.floor(lo[0] / dx)) - 1, int(np.ceil(hi[0] / dx)) + 1
+    ii = np.arange(i0, i1 + 1)
+    xs = ((ii[:, None].astype(T) + offs[None, :]) * dx).ravel()
+    xs = xs[(xs >= lo[0]) & (xs < hi[0])]
+    bx = np.clip(np.floor(xs * inv_dx + T(0.25)).astype(np.int64) >> 2, 0, D - 1)
+    bounds = partition_planes(np.bincount(bx, minlength=D).astype(np.float64), world)
+    # the box restricted to key planes [X_r, X_{r+1}): x in [(4X - 1/4) dx, (4X' - 1/4) dx)
+    xa, xb = (T(4 * bounds[rank]) - T(0.25)) * dx, (T(4 * bounds[rank + 1]) - T(0.25)) * dx
+    sub = copy.deepcopy(cfg)
+    sh = sub.bodies[0].shape
+    sh.lo = (float(max(lo[0], xa)), sh.lo[1], sh.lo[2])
+    sh.hi = (float(min(hi[0], xb)), sh.hi[1], sh.hi[2])
+    if not (sh.lo[0] < sh.hi[0]):
+        part = np.zeros(0, dtype=abi.particle_dtype(precision))
+    else:
+        part = seed_particles(sub, precision)
+        kbx = np.clip(np.floor(part["x"][:, 0] * inv_dx + T(0.25)).astype(np.int64) >> 2, 0, D - 1)
+        part = part[(kbx >= bounds[rank]) & (kbx < bounds[rank + 1])]
+    mat = cfg.materials[body.material]
+    vol = (dx * dx * dx) / T(body.ppc)
+    me = float(T(1e-12) * (T(mat.density) * vol))  # every particle has the same mass
+    rk = SlabRank(cfg, rank, world, bounds, part, me, precision, device)
+    v = np.array(body.velocity, dtype=T)
+    rk.vmax = float(np.sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]))
+    return bounds, rk

@@ -1,0 +1,142 @@
+"""x-slab decomposition on one GPU: 2 and 3 ranks emulated in-process (each
+rank its own context; exchanges are device copies between stages, no kernel
+waits on another rank).  The concatenated rank states must reproduce the
+single-domain run: identical global particle order (bit-exact binning and
+stable sort across slabs) and state within the single-GPU tolerances."""
+import numpy as np
+import pytest
+
+from paper_2412_10399_b200.api import Simulation
+from paper_2412_10399_b200.scene import SceneConfig, seed_particles
+from paper_2412_10399_b200.slab import build_ranks, run_loopback
+from tests.gpu_util import tag_volumes
+from tests.util import perturb
+
+pytestmark = pytest.mark.gpu
+
+
+def scene(scheme="apic", model="fixed_corotated"):
+    mat = {"model": model, "density": 1000.0, "E": 1e5, "nu": 0.3}
+    if model == "drucker_prager":
+        mat.update({"E": 1e4, "friction_angle_deg": 30.0})
+    obj = {"resolution": 48, "scheme": scheme, "gravity": [0, -9.8, 0], "materials": [mat],
+           "bodies": [{"shape": {"kind": "box", "lo": [0.3, 0.3, 0.35], "hi": [0.55, 0.5, 0.6]}, "material": 0,
+                       "velocity": [1.5, 0.0, -0.3]}],
+           "boundaries": [{"kind": "sticky", "lo": [0, 0, 0], "hi": [1, 0.125, 1]}]}
+    return SceneConfig.from_json(obj)
+
+
+def _keys(p, cfg):
+    D = cfg.resolution // 4 + 2
+    c = np.clip(np.floor(p["x"] * float(cfg.resolution) + 0.25).astype(np.int64) >> 2, 0, D - 1)
+    return (c[:, 0] * D + c[:, 1]) * D + c[:, 2]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("scheme,model", [("apic", "fixed_corotated"), ("pic", "drucker_prager")])
+def test_slab_loopback_matches_single_domain(world, scheme, model):
+    cfg = scene(scheme, model)
+    p0 = tag_volumes(perturb(seed_particles(cfg), seed=3, fscale=0.002, vscale=0.05, bscale=0.05, xscale=0.1,
+                             dx=1 / 48))
+    single = Simulation(cfg, particles=p0)
+    bounds, ranks = build_ranks(cfg, world, particles=p0)
+    assert len(ranks) == world
+    migrated = 0
+    for step in range(25):
+        dt = single.cfl_dt(1.0)
+        assert abs(ranks[0].cfl_dt(1.0) - dt) <= 1e-9 * dt
+        single.step(dt)
+        n_before = [r.n for r in ranks]
+        run_loopback(ranks, dt)
+        migrated += sum(abs(a - r.n) for a, r in zip(n_before, ranks))
+        a = single.particles()
+        b = np.concatenate([r.particles() for r in ranks])
+        assert len(a) == len(b)
+        # The stored orders differ by where migrants sit until the next sort;
+        # the stable sort both feed into the next substep must agree: sort both
+        # by the block key of the (single-domain) positions.
+        key_of = dict(zip(a["volume0"].tolist(), _keys(a, cfg).tolist()))
+        ka = np.array([key_of[t] for t in a["volume0"].tolist()])
+        kb = np.array([key_of[t] for t in b["volume0"].tolist()])
+        sa = a["volume0"][np.argsort(ka, kind="stable")]
+        sb = b["volume0"][np.argsort(kb, kind="stable")]
+        assert np.array_equal(sa, sb), f"global sorted order differs at step {step}"
+        ia, ib = np.argsort(a["volume0"]), np.argsort(b["volume0"])
+        a, b = a[ia], b[ib]
+        for f, fl in (("x", 1.0), ("v", 1.0), ("F", 1.0)):
+            x = np.asarray(a[f], dtype=np.float64)
+            y = np.asarray(b[f], dtype=np.float64)
+            assert np.max(np.abs(x - y)) <= 1e-10 * max(np.max(np.abs(x)), fl), (step, f)
+    assert migrated > 0, "no particle crossed a slab boundary; the test would not exercise migration"
+    for r in ranks:
+        r.close()
+    single.close()
+
+
+def _mp_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_10399_b200.scene import block_scene
+    from paper_2412_10399_b200.slab import DistTransport, build_rank_for_box
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = block_scene(24, resolution=128, scheme="apic")
+    cfg.bodies[0].velocity = (2.0, 0.0, 0.0)  # sweep particles across slab boundaries
+    bounds, rk = build_rank_for_box(cfg, world, rank, 8, 0)
+    tr = DistTransport(dist, rank, world, torch.device("cuda", 0))
+    dt = rk.cfl_dt(1.0)
+    for _ in range(12):
+        tr.step(rk, dt)
+    q.put((rank, rk.particles(), dt))
+    rk.close()
+    dist.destroy_process_group()
+
+
+def test_slab_multiprocess_gloo_matches_single_domain():
+    """The bench's multi-process path (one process per rank, DistTransport,
+    rank-local seeding) with 2 processes sharing this GPU through a
+    host-staged gloo transport (exchanges are host-driven: no kernel waits on
+    another process)."""
+    import multiprocessing as mp
+    import socket
+
+    from paper_2412_10399_b200.scene import block_scene
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, (ps, dt)) for r, ps, dt in (q.get(timeout=600) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    cfg = block_scene(24, resolution=128, scheme="apic")
+    cfg.bodies[0].velocity = (2.0, 0.0, 0.0)
+    single = Simulation(cfg)
+    dt = res[0][1]
+    for _ in range(12):
+        single.step(dt)
+    a = single.particles()
+    b = np.concatenate([res[r][0] for r in range(world)])
+    assert len(a) == len(b) and len(res[0][0]) != len(a)
+    # match particles by position quantised far above round-off (lattice
+    # particles stay >= dx/2 apart; the two runs differ by ~1e-16)
+    qa = np.round(a["x"] * 2.0 ** 30).astype(np.int64)
+    qb = np.round(b["x"] * 2.0 ** 30).astype(np.int64)
+    ka = np.lexsort((qa[:, 2], qa[:, 1], qa[:, 0]))
+    kb = np.lexsort((qb[:, 2], qb[:, 1], qb[:, 0]))
+    for f in ("x", "v", "F"):
+        x = np.asarray(a[f][ka], dtype=np.float64)
+        y = np.asarray(b[f][kb], dtype=np.float64)
+        err = float(np.max(np.abs(x - y)) / max(float(np.max(np.abs(x))), 1.0))
+        assert err <= 1e-10, (f, err)
+    single.close()
