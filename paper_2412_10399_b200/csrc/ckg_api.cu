@@ -276,7 +276,7 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kXferThreads, smem));
     if (cfg.scheme == S) p2g_ctas = std::max(1, per) * nsm;
-    CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S>, kXferThreads, 0));
+    CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S>, kG2PThreads, 0));
     if (cfg.scheme == S) g2p_ctas = std::max(1, per) * nsm;
   }
 
@@ -484,7 +484,7 @@ struct Context final : CtxBase {
   }
   template <int S>
   void enqueue_g2p(const StepConst<T>& c, int step_idx) {
-    g2p_tile_kernel<T, S><<<g2p_ctas, kXferThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir, active,
+    g2p_tile_kernel<T, S><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir, active,
                                                               seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
   }
 

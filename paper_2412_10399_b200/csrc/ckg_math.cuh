@@ -283,7 +283,7 @@ __device__ __noinline__ void svd3(const M3<T>& F, M3<T>& U, V3<T>& sigma, M3<T>&
 // polar_rotation (math.hpp:300-321): scaled Newton R <- (gR + (gR)^-T)/2 with
 // the reference's stopping rule; SVD construction for near-singular input.
 template <typename T>
-__device__ __forceinline__ M3<T> polar_rotation(const M3<T>& F) {
+__device__ __noinline__ M3<T> polar_rotation(const M3<T>& F) {  // cold fallback: out of line
   T nf = dsqrt(frob2(F));
   T d = det(F);
   if (!(d > T(1e-10) * nf * nf * nf)) {

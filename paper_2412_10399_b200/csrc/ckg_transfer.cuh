@@ -35,9 +35,17 @@ constexpr int kTileVals = 2 * 4 * kTileNodes;         // 1728 (m, px, py, pz on 
 constexpr int kVelVals = 2 * 3 * kTileNodes;          // 1296
 constexpr int kXferThreads = 256;
 constexpr int kXferWarps = kXferThreads / 32;
-#ifndef CKG_G2P_MINB
-#define CKG_G2P_MINB 2
+// G2P CTA shape: small CTAs keep more of them resident per SM when one
+// stalls at its tile-staging barrier (measured on the 10M bench: 128 x 4 and
+// 64 x 8 beat 256 x 2 by 9%).
+#ifndef CKG_G2P_THREADS
+#define CKG_G2P_THREADS 128
 #endif
+#ifndef CKG_G2P_MINB
+#define CKG_G2P_MINB 4
+#endif
+constexpr int kG2PThreads = CKG_G2P_THREADS;
+constexpr int kG2PWarps = kG2PThreads / 32;
 constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full lattice block)
 
 template <typename T>
@@ -437,7 +445,7 @@ __device__ __forceinline__ void gather_grid(const Axis<T>* ax, T dx, VelFn V, T 
 }
 
 template <typename T, int SCHEME>
-__global__ void __launch_bounds__(kXferThreads, CKG_G2P_MINB)
+__global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
     g2p_tile_kernel(PState<T> cur, PState<T> nxt, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ active,
                     const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_end,
@@ -445,7 +453,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_G2P_MINB)
   __shared__ T vt[kVelVals];
   __shared__ int32_t nbr[27];
   __shared__ uint32_t s_item;
-  __shared__ T wmax[kXferWarps];
+  __shared__ T wmax[kG2PWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const int D = c.D;
@@ -465,7 +473,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_G2P_MINB)
     if (tid < 27) nbr[tid] = dir_lookup(dir, D, bx - 1 + tid / 9, by - 1 + (tid / 3) % 3, bz - 1 + tid % 3);
     __syncthreads();
     // stage nodal velocities of both grids' 6^3 tiles
-    for (int e = tid; e < kVelVals; e += kXferThreads) {
+    for (int e = tid; e < kVelVals; e += kG2PThreads) {
       const int g = e / (3 * kTileNodes);
       const int cc = (e / kTileNodes) % 3;
       const int node = e % kTileNodes;
@@ -476,7 +484,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_G2P_MINB)
       vt[e] = (off >= 0 && uint64_t(off) < uint64_t(cap) * kBlockVals) ? __ldg(pool + off + (1 + cc) * 64) : T(0);
     }
     __syncthreads();
-    for (uint32_t cb = s0; cb < s1; cb += kXferThreads) {
+    for (uint32_t cb = s0; cb < s1; cb += kG2PThreads) {
       const uint32_t i = cb + tid;
       const bool live = i < s1;
       bool fluid = false;
@@ -651,7 +659,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_G2P_MINB)
   __syncthreads();
   if (tid == 0) {
     T b = T(0);
-    for (int w = 0; w < kXferWarps; ++w) b = (b < wmax[w]) ? wmax[w] : b;
+    for (int w = 0; w < kG2PWarps; ++w) b = (b < wmax[w]) ? wmax[w] : b;
     if (b > T(0)) atomicMax(&st->vmax2, as_ordered_bits(b));
   }
 }
