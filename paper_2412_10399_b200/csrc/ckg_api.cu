@@ -274,6 +274,17 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
     const size_t smem = p2g_smem_bytes<T>();
     CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    {
+      // smallest shared-memory carveout holding two P2G CTAs: the rest of
+      // the 256 KB stays L1 for the class-order particle gathers and spills
+      cudaFuncAttributes fa{};
+      CKG_CUDA(cudaFuncGetAttributes(&fa, p2g_tile_kernel<T, S>));
+      int smem_sm = 0;
+      CKG_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+      const size_t need = 2 * (smem + fa.sharedSizeBytes + 1024);
+      const int pct = int(std::min<size_t>(100, (need * 100 + smem_sm - 1) / std::max(smem_sm, 1)));
+      CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kXferThreads, smem));
     if (cfg.scheme == S) p2g_ctas = std::max(1, per) * nsm;
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S>, kG2PThreads, 0));

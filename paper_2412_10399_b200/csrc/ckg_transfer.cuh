@@ -48,9 +48,17 @@ constexpr int kG2PThreads = CKG_G2P_THREADS;
 constexpr int kG2PWarps = kG2PThreads / 32;
 constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full lattice block)
 
+// P2G class tiles: warp w scatters sub-octant class w only, whose bases lie in
+// a 4-wide range per axis on both grids (slot 0 origin 4b, slot 1 origin
+// 4b - c_a with c_a = bit a of w), so each warp-private tile is 5^3 nodes per
+// grid instead of the 6^3 block halo.  8 warps x 2 x 4 x 125 FP64 = 64 KB per
+// CTA, which leaves L1 room for the particle gathers and register spills.
+constexpr int kPT = 5;
+constexpr int kPTNodes = kPT * kPT * kPT;  // 125
+constexpr int kPTVals = 2 * 4 * kPTNodes;  // 1000
 template <typename T>
 constexpr size_t p2g_smem_bytes() {
-  return size_t(kXferWarps) * kTileVals * sizeof(T);
+  return size_t(kXferWarps) * kPTVals * sizeof(T);
 }
 
 __device__ __forceinline__ void decode_key(uint32_t key, int D, int& bx, int& by, int& bz) {
@@ -83,8 +91,9 @@ __global__ void __launch_bounds__(kXferThreads, 2)
   __shared__ uint32_t cls_cnt[8], cls_off[8];
   __shared__ uint16_t cls_list[kP2GChunk];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  T* wt = tiles + warp * kTileVals;
-  for (int e = tid; e < kXferWarps * kTileVals; e += kXferThreads) tiles[e] = T(0);
+  T* wt = tiles + warp * kPTVals;
+  for (int e = tid; e < kXferWarps * kPTVals; e += kXferThreads) tiles[e] = T(0);
+  const int cx = warp & 1, cy = (warp >> 1) & 1, cz = (warp >> 2) & 1;  // class bits
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const uint32_t lt = lanemask_lt();
   const int D = c.D;
@@ -198,36 +207,35 @@ __global__ void __launch_bounds__(kXferThreads, 2)
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
         const Axis<T>* ax = ds.ax[g];
-        const int lx = ax[0].base - (4 * bx - g), ly = ax[1].base - (4 * by - g), lz = ax[2].base - (4 * bz - g);
-        const bool in_tile = valid && lx >= 0 && ly >= 0 && lz >= 0 && lx <= kTileN - 2 && ly <= kTileN - 2 &&
-                             lz <= kTileN - 2;
-        const uint32_t cell = in_tile ? uint32_t((lx * kTileN + ly) * kTileN + lz) : (1024u + lane);
+        const int lx = ax[0].base - (4 * bx - (g ? cx : 0)), ly = ax[1].base - (4 * by - (g ? cy : 0)),
+                  lz = ax[2].base - (4 * bz - (g ? cz : 0));
+        const bool in_tile =
+            valid && lx >= 0 && ly >= 0 && lz >= 0 && lx <= kPT - 2 && ly <= kPT - 2 && lz <= kPT - 2;
+        const uint32_t cell = in_tile ? uint32_t((lx * kPT + ly) * kPT + lz) : (1024u + lane);
         const uint32_t peers = __match_any_sync(0xffffffffu, cell);
         const uint32_t rank = __popc(peers & lt);
         const uint32_t maxrank = __reduce_max_sync(0xffffffffu, rank);
-        const T wx[2] = {ax[0].w0, ax[0].w1}, wy[2] = {ax[1].w0, ax[1].w1}, wz[2] = {ax[2].w0, ax[2].w1};
-        const T gx[2] = {ax[0].g0, -ax[0].g0}, gy[2] = {ax[1].g0, -ax[1].g0}, gz[2] = {ax[2].g0, -ax[2].g0};
         // node momentum base b_stu = m v + Q xi_stu = u0 + dx (s Qx + t Qy + u Qz)
         T u0[3] = {mv[0], mv[1], mv[2]};
-        T dQ[3][3];
         if (SCHEME != kSchemePic) {
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
+          for (int a = 0; a < 3; ++a)
             u0[a] += Q.a[a][0] * ax[0].xi0 + Q.a[a][1] * ax[1].xi0 + Q.a[a][2] * ax[2].xi0;
-#pragma unroll
-            for (int b = 0; b < 3; ++b) dQ[a][b] = Q.a[a][b] * dx;
-          }
         }
         // Node contribution (m w, w b - A' grad w) or, for MLS, the force
         // through grad Phi = w M^-1 P(xi) (transfer.hpp:335-369).
+        // (selects, not arrays indexed by s/t/u: the rolled paths below
+        // would otherwise put the axis weights in local memory)
         auto contrib = [&](int s, int t, int u, T (&o)[4]) {
-          const T wyz = wy[t] * wz[u];
-          const T w = wx[s] * wyz;
+          const T wxs = s ? ax[0].w1 : ax[0].w0, wyt = t ? ax[1].w1 : ax[1].w0, wzu = u ? ax[2].w1 : ax[2].w0;
+          const T wyz = wyt * wzu;
+          const T w = wxs * wyz;
           T gw0, gw1, gw2;
           if (SCHEME != kSchemeMls) {
-            gw0 = gx[s] * wyz;
-            gw1 = wx[s] * (gy[t] * wz[u]);
-            gw2 = wx[s] * (wy[t] * gz[u]);
+            const T gxs = s ? -ax[0].g0 : ax[0].g0, gyt = t ? -ax[1].g0 : ax[1].g0, gzu = u ? -ax[2].g0 : ax[2].g0;
+            gw0 = gxs * wyz;
+            gw1 = wxs * (gyt * wzu);
+            gw2 = wxs * (wyt * gzu);
           } else {
             const T P1 = ax[0].xi0 + (s ? dx : T(0)), P2 = ax[1].xi0 + (t ? dx : T(0)),
                     P3 = ax[2].xi0 + (u ? dx : T(0));
@@ -240,14 +248,15 @@ __global__ void __launch_bounds__(kXferThreads, 2)
           for (int a = 0; a < 3; ++a) {
             T b = u0[a];
             if (SCHEME != kSchemePic) {
-              if (s) b += dQ[a][0];
-              if (t) b += dQ[a][1];
-              if (u) b += dQ[a][2];
+              // + Q (s, t, u) dx, fused (no dx-scaled copy of Q kept live)
+              if (s) b = fma(Q.a[a][0], dx, b);
+              if (t) b = fma(Q.a[a][1], dx, b);
+              if (u) b = fma(Q.a[a][2], dx, b);
             }
             o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
           }
         };
-        T* p0 = wt + g * 4 * kTileNodes + (lx * kTileN + ly) * kTileN + lz;
+        T* p0 = wt + g * 4 * kPTNodes + (lx * kPT + ly) * kPT + lz;
         if (maxrank == 0) {
           // fast path: every lane owns a distinct base cell in this warp, so
           // at a fixed node offset all lanes write distinct nodes
@@ -260,12 +269,12 @@ __global__ void __launch_bounds__(kXferThreads, 2)
                 for (int u = 0; u < 2; ++u) {
                   T o[4];
                   contrib(s, t, u, o);
-                  T* p = p0 + (s * kTileN + t) * kTileN + u;
+                  T* p = p0 + (s * kPT + t) * kPT + u;
                   if (in_tile) {
                   p[0] += o[0];
-                  p[kTileNodes] += o[1];
-                  p[2 * kTileNodes] += o[2];
-                  p[3 * kTileNodes] += o[3];
+                  p[kPTNodes] += o[1];
+                  p[2 * kPTNodes] += o[2];
+                  p[3 * kPTNodes] += o[3];
                   }
                   // node (s,t,u) of one lane can be node (0,0,0) of its
                   // neighbour: order the read-modify-writes across lanes
@@ -279,13 +288,13 @@ __global__ void __launch_bounds__(kXferThreads, 2)
             const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
             T o[4];
             contrib(s, t, u, o);
-            T* p = p0 + (s * kTileN + t) * kTileN + u;
+            T* p = p0 + (s * kPT + t) * kPT + u;
             for (uint32_t layer = 0; layer <= maxrank; ++layer) {
               if (in_tile && rank == layer) {
                 p[0] += o[0];
-                p[kTileNodes] += o[1];
-                p[2 * kTileNodes] += o[2];
-                p[3 * kTileNodes] += o[3];
+                p[kPTNodes] += o[1];
+                p[2 * kPTNodes] += o[2];
+                p[3 * kPTNodes] += o[3];
               }
               __syncwarp();
             }
@@ -316,21 +325,45 @@ __global__ void __launch_bounds__(kXferThreads, 2)
       __syncthreads();
     }
     __syncthreads();
-    // ---- flush: sum the warp tiles, one REDG per non-zero node value
-    for (int e = tid; e < kTileVals; e += kXferThreads) {
+    // ---- flush: sum the warp tiles, one REDG per non-zero node value.
+    // Slot 0: all class tiles share origin 4b (5^3).  Slot 1: the 6^3 halo
+    // from 4b - 1; warp w's tile covers offsets [1 - c, 5 - c] per axis.
+    for (int e = tid; e < 4 * kPTNodes + 4 * kTileNodes; e += kXferThreads) {
       T sum = T(0);
+      int g, v, i, j, k;
+      if (e < 4 * kPTNodes) {
+        g = 0;
+        v = e / kPTNodes;
+        const int node = e % kPTNodes;
+        i = node / (kPT * kPT);
+        j = (node / kPT) % kPT;
+        k = node % kPT;
 #pragma unroll
-      for (int w = 0; w < kXferWarps; ++w) {
-        sum += tiles[w * kTileVals + e];
-        tiles[w * kTileVals + e] = T(0);
+        for (int w = 0; w < kXferWarps; ++w) {
+          T* q = tiles + w * kPTVals + e;
+          sum += *q;
+          *q = T(0);
+        }
+      } else {
+        g = 1;
+        const int e1 = e - 4 * kPTNodes;
+        v = e1 / kTileNodes;
+        const int node = e1 % kTileNodes;
+        i = node / (kTileN * kTileN);
+        j = (node / kTileN) % kTileN;
+        k = node % kTileN;
+#pragma unroll
+        for (int w = 0; w < kXferWarps; ++w) {
+          const int li = i - 1 + (w & 1), lj = j - 1 + ((w >> 1) & 1), lk = k - 1 + ((w >> 2) & 1);
+          if (li >= 0 && lj >= 0 && lk >= 0 && li < kPT && lj < kPT && lk < kPT) {
+            T* q = tiles + w * kPTVals + 4 * kPTNodes + v * kPTNodes + (li * kPT + lj) * kPT + lk;
+            sum += *q;
+            *q = T(0);
+          }
+        }
       }
       if (sum != T(0)) {
-        const int g = e / (4 * kTileNodes);
-        const int v = (e / kTileNodes) & 3;
-        const int node = e % kTileNodes;
-        const int gi = 4 * bx - g + node / (kTileN * kTileN);
-        const int gj = 4 * by - g + (node / kTileN) % kTileN;
-        const int gk = 4 * bz - g + node % kTileN;
+        const int gi = 4 * bx - g + i, gj = 4 * by - g + j, gk = 4 * bz - g + k;
         const int64_t off = nbr_offset(nbr, g, gi, gj, gk, bx, by, bz);
         if (off < 0 || uint64_t(off) >= uint64_t(cap) * kBlockVals)
           record_error(st, step, kPhaseP2G, s0, 0, kErrInactive);
