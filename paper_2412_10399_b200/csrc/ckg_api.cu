@@ -281,8 +281,16 @@ struct Context final : CtxBase {
       CKG_CUDA(cudaFuncGetAttributes(&fa, p2g_tile_kernel<T, S>));
       int smem_sm = 0;
       CKG_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
-      const size_t need = 2 * (smem + fa.sharedSizeBytes + 1024);
-      const int pct = int(std::min<size_t>(100, (need * 100 + smem_sm - 1) / std::max(smem_sm, 1)));
+      const size_t need = 2 * (smem + fa.sharedSizeBytes + 1024);  // + 1 KB reserved per CTA
+      // supported sm_100 carveouts (KB); the driver rounds the percentage up
+      // to the next one, so ask for floor(target) of the smallest that fits
+      size_t target = size_t(smem_sm);
+      for (int kb : {64, 100, 132, 164, 196, 228})
+        if (size_t(kb) * 1024 >= need) {
+          target = std::min<size_t>(size_t(kb) * 1024, size_t(smem_sm));
+          break;
+        }
+      const int pct = int(std::min<size_t>(100, target * 100 / std::max(smem_sm, 1)));
       CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     }
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kXferThreads, smem));

@@ -44,6 +44,12 @@ constexpr int kXferWarps = kXferThreads / 32;
 #ifndef CKG_G2P_MINB
 #define CKG_G2P_MINB 4
 #endif
+#ifndef CKG_G2P_DUAL
+#define CKG_G2P_DUAL 0
+#endif
+#ifndef CKG_P2G_MINB
+#define CKG_P2G_MINB 2
+#endif
 constexpr int kG2PThreads = CKG_G2P_THREADS;
 constexpr int kG2PWarps = kG2PThreads / 32;
 constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full lattice block)
@@ -79,7 +85,7 @@ __device__ __forceinline__ int64_t nbr_offset(const int32_t* nbr, int g, int gi,
 }
 
 template <typename T, int SCHEME>
-__global__ void __launch_bounds__(kXferThreads, 2)
+__global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
     p2g_tile_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ active,
                     const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_end,
@@ -89,7 +95,7 @@ __global__ void __launch_bounds__(kXferThreads, 2)
   __shared__ int32_t nbr[27];
   __shared__ uint32_t s_item;
   __shared__ uint32_t cls_cnt[8], cls_off[8];
-  __shared__ uint16_t cls_list[kP2GChunk];
+  __shared__ uint32_t cls_list[kP2GChunk];  // class order -> state index (perm applied)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   T* wt = tiles + warp * kPTVals;
   for (int e = tid; e < kXferWarps * kPTVals; e += kXferThreads) tiles[e] = T(0);
@@ -119,12 +125,13 @@ __global__ void __launch_bounds__(kXferThreads, 2)
       const uint32_t len = min(uint32_t(kP2GChunk), s1 - cb);
       if (tid < 8) cls_cnt[tid] = 0;
       __syncthreads();
-      uint32_t myq[kP2GChunk / kXferThreads], myslot[kP2GChunk / kXferThreads];
+      uint32_t myq[kP2GChunk / kXferThreads], myslot[kP2GChunk / kXferThreads], mysrc[kP2GChunk / kXferThreads];
 #pragma unroll
       for (int r = 0; r < kP2GChunk / kXferThreads; ++r) {
         const uint32_t j = tid + r * kXferThreads;
         if (j < len) {
           const uint32_t src = __ldg(perm + cb + j);
+          mysrc[r] = src;
           uint32_t q = 0;
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
@@ -148,57 +155,65 @@ __global__ void __launch_bounds__(kXferThreads, 2)
 #pragma unroll
       for (int r = 0; r < kP2GChunk / kXferThreads; ++r) {
         const uint32_t j = tid + r * kXferThreads;
-        if (j < len) cls_list[cls_off[myq[r]] + myslot[r]] = uint16_t(j);
+        if (j < len) cls_list[cls_off[myq[r]] + myslot[r]] = mysrc[r];
       }
       __syncthreads();
       const uint32_t my_cnt = cls_cnt[warp], my_off = cls_off[warp];
       for (uint32_t rb = 0; rb < my_cnt; rb += 32) {
       const bool in_round = rb + lane < my_cnt;
-      const uint32_t i = cb + (in_round ? uint32_t(cls_list[my_off + rb + lane]) : 0u);
+      const uint32_t src = in_round ? cls_list[my_off + rb + lane] : 0u;
+      // sorted index of this particle, for error reports only (rare path)
+      auto sorted_index = [&]() -> uint32_t {
+        for (uint32_t k = cb; k < min(cb + uint32_t(kP2GChunk), s1); ++k)
+          if (__ldg(perm + k) == src) return k;
+        return cb;
+      };
       bool valid = in_round;
       // ---- per-particle state (scatter_all, simulation.hpp:289-324)
       T x = 0, y = 0, z = 0, m = 0;
       T mv[3] = {0, 0, 0};
-      M3<T> Ap, Q;  // Ap = dt * V0 * tau, Q = m * C
+      M3<T> Ap, Q, Bp;  // Ap = dt * V0 * tau, Q = m * C
       T Minv[4][4];
       Dual<T> ds;
       if (valid) {
-        const uint32_t src = __ldg(perm + i);
+        // every field load is issued before the first use
         const uint64_t n = cur.stride;  // field stride (buffer capacity)
         x = __ldg(cur.f + kX * n + src);
         y = __ldg(cur.f + (kX + 1) * n + src);
         z = __ldg(cur.f + (kX + 2) * n + src);
         m = __ldg(cur.f + kMass * n + src);
-        mv[0] = m * __ldg(cur.f + kV * n + src);
-        mv[1] = m * __ldg(cur.f + (kV + 1) * n + src);
-        mv[2] = m * __ldg(cur.f + (kV + 2) * n + src);
+        T v3[3], t6[6];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v3[k] = __ldg(cur.f + (kV + k) * n + src);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) t6[k] = __ldg(cur.tau + uint64_t(k) * n + src);
+        if (SCHEME != kSchemePic) Bp = load_m3(cur, kB, src);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) mv[k] = m * v3[k];
         // dt * V0 * tau from the stress cache written by the previous G2P
         // (or the initial stress pass): P2G runs no constitutive model.
-        {
-          T t6[6];
 #pragma unroll
-          for (int k = 0; k < 6; ++k) t6[k] = dt * __ldg(cur.tau + uint64_t(k) * n + src);
-          Ap.a[0][0] = t6[0];
-          Ap.a[0][1] = Ap.a[1][0] = t6[1];
-          Ap.a[0][2] = Ap.a[2][0] = t6[2];
-          Ap.a[1][1] = t6[3];
-          Ap.a[1][2] = Ap.a[2][1] = t6[4];
-          Ap.a[2][2] = t6[5];
-        }
+        for (int k = 0; k < 6; ++k) t6[k] = dt * t6[k];
+        Ap.a[0][0] = t6[0];
+        Ap.a[0][1] = Ap.a[1][0] = t6[1];
+        Ap.a[0][2] = Ap.a[2][0] = t6[2];
+        Ap.a[1][1] = t6[3];
+        Ap.a[1][2] = Ap.a[2][1] = t6[4];
+        Ap.a[2][2] = t6[5];
         ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
         if (SCHEME != kSchemePic) {
           M3<T> Di;
           if (!apic_d_inverse(apic_D(ds, dx), Di)) {
-            record_error(st, step, kPhaseP2G, i, 0, kErrNearSingularD);
+            record_error(st, step, kPhaseP2G, sorted_index(), 0, kErrNearSingularD);
             valid = false;
           }
-          Q = scale(m, mul(load_m3(cur, kB, src), Di));  // m * B D^-1
+          Q = scale(m, mul(Bp, Di));  // m * B D^-1
         }
         if (SCHEME == kSchemeMls) {
           T Mm[4][4];
           mls_moment(ds, dx, Mm);
           if (!gauss_inverse4(Mm, Minv)) {
-            record_error(st, step, kPhaseP2G, i, 0, kErrSingularMls);
+            record_error(st, step, kPhaseP2G, sorted_index(), 0, kErrSingularMls);
             valid = false;
           }
         }
@@ -310,7 +325,7 @@ __global__ void __launch_bounds__(kXferThreads, 2)
             const int gi = ax[0].base + s, gj = ax[1].base + t, gk = ax[2].base + u;
             const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
             if (slot < 0 || uint32_t(slot) >= cap) {
-              record_error(st, step, kPhaseP2G, i, 0, kErrInactive);
+              record_error(st, step, kPhaseP2G, sorted_index(), 0, kErrInactive);
             } else {
               T* nd = pool + node_off(slot, g, gi, gj, gk);
               atomicAdd(nd, o[0]);
@@ -505,16 +520,31 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
     decode_key(key, D, bx, by, bz);
     if (tid < 27) nbr[tid] = dir_lookup(dir, D, bx - 1 + tid / 9, by - 1 + (tid / 3) % 3, bz - 1 + tid % 3);
     __syncthreads();
-    // stage nodal velocities of both grids' 6^3 tiles
-    for (int e = tid; e < kVelVals; e += kG2PThreads) {
-      const int g = e / (3 * kTileNodes);
-      const int cc = (e / kTileNodes) % 3;
-      const int node = e % kTileNodes;
-      const int gi = 4 * bx - g + node / (kTileN * kTileN);
-      const int gj = 4 * by - g + (node / kTileN) % kTileN;
-      const int gk = 4 * bz - g + node % kTileN;
-      const int64_t off = nbr_offset(nbr, g, gi, gj, gk, bx, by, bz);
-      vt[e] = (off >= 0 && uint64_t(off) < uint64_t(cap) * kBlockVals) ? __ldg(pool + off + (1 + cc) * 64) : T(0);
+    // stage nodal velocities of both grids' 6^3 tiles: all of a thread's
+    // loads are issued before the first shared store
+    {
+      constexpr int kPer = (kVelVals + kG2PThreads - 1) / kG2PThreads;
+      T val[kPer];
+#pragma unroll
+      for (int r = 0; r < kPer; ++r) {
+        const int e = tid + r * kG2PThreads;
+        val[r] = T(0);
+        if (e < kVelVals) {
+          const int g = e / (3 * kTileNodes);
+          const int cc = (e / kTileNodes) % 3;
+          const int node = e % kTileNodes;
+          const int gi = 4 * bx - g + node / (kTileN * kTileN);
+          const int gj = 4 * by - g + (node / kTileN) % kTileN;
+          const int gk = 4 * bz - g + node % kTileN;
+          const int64_t off = nbr_offset(nbr, g, gi, gj, gk, bx, by, bz);
+          if (off >= 0 && uint64_t(off) < uint64_t(cap) * kBlockVals) val[r] = __ldg(pool + off + (1 + cc) * 64);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kPer; ++r) {
+        const int e = tid + r * kG2PThreads;
+        if (e < kVelVals) vt[e] = val[r];
+      }
     }
     __syncthreads();
     for (uint32_t cb = s0; cb < s1; cb += kG2PThreads) {
@@ -528,6 +558,9 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
         const uint64_t n = cur.stride;  // field stride (buffer capacity)
         T x = __ldg(cur.f + kX * n + src), y = __ldg(cur.f + (kX + 1) * n + src),
           z = __ldg(cur.f + (kX + 2) * n + src);
+        // pass-through fields, loaded with x so their latency overlaps the gather
+        mi = __ldg(cur.mat + src);
+        const T mass = __ldg(cur.f + kMass * n + src), vol0 = __ldg(cur.f + kVol * n + src);
         T v[3] = {T(0), T(0), T(0)};
         M3<T> Bn, G;
 #pragma unroll
@@ -537,11 +570,19 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
             Bn.a[a][b] = T(0);
             G.a[a][b] = T(0);
           }
+#if CKG_G2P_DUAL
+        // both grids' stencils from one sincos per axis (axis_pair_dual)
+        const Dual<T> ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
+#endif
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
+#if CKG_G2P_DUAL
+          const Axis<T>* ax = ds.ax[g];
+#else
           const T kq = g == 0 ? T(-0.25) : T(0.25);
-          Axis<T> ax[3] = {axis_pair(x, dx, c.inv_dx, c.pow2, kq), axis_pair(y, dx, c.inv_dx, c.pow2, kq),
-                           axis_pair(z, dx, c.inv_dx, c.pow2, kq)};
+          const Axis<T> ax[3] = {axis_pair(x, dx, c.inv_dx, c.pow2, kq), axis_pair(y, dx, c.inv_dx, c.pow2, kq),
+                                 axis_pair(z, dx, c.inv_dx, c.pow2, kq)};
+#endif
           const int lx = ax[0].base - (4 * bx - g), ly = ax[1].base - (4 * by - g), lz = ax[2].base - (4 * bz - g);
           const bool in_tile =
               lx >= 0 && ly >= 0 && lz >= 0 && lx <= kTileN - 2 && ly <= kTileN - 2 && lz <= kTileN - 2;
@@ -587,7 +628,6 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
         // update_particle_state (transfer.hpp:594-627).  Outputs are stored
         // as soon as they are final so the stress evaluation at the end runs
         // with only F live (register pressure).
-        mi = __ldg(cur.mat + src);
         const MatParam<T>& mp = c.mats[mi < kMaxMaterials ? mi : 0];
         M3<T> L = G;
         if (SCHEME == kSchemeMls) {
@@ -618,8 +658,7 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
         nxt.f[kV * n + i] = v[0];
         nxt.f[(kV + 1) * n + i] = v[1];
         nxt.f[(kV + 2) * n + i] = v[2];
-        const T vol0 = __ldg(cur.f + kVol * n + src);
-        nxt.f[kMass * n + i] = __ldg(cur.f + kMass * n + src);
+        nxt.f[kMass * n + i] = mass;
         nxt.f[kVol * n + i] = vol0;
         nxt.mat[i] = mi;
         {
