@@ -147,6 +147,7 @@ struct Context final : CtxBase {
   bool ko_valid = false;
   uint32_t *chg = nullptr, *cpre = nullptr, *ck = nullptr, *ci = nullptr, *iota = nullptr;
   uint32_t *perm_buf = nullptr, *skeys_tmp = nullptr, *ncount = nullptr;
+  uint32_t* wcnt = nullptr;  // changed count per warp of stored positions (chg holds the ballot words, cpre their scan)
   uint32_t* hcount = nullptr;  // pinned
   uint64_t last_changed = 0;
   int last_sort_kind = 0;    // 0 full radix, 1 identity, 2 incremental
@@ -235,7 +236,7 @@ struct Context final : CtxBase {
     dfree(rs.vals_alt);
     dfree(rs.hist);
     dfree(rs.partials);
-    for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount}) dfree(*b);
+    for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount, &wcnt}) dfree(*b);
     for (uint32_t** b : {&plane_start, &fl_stay, &fl_left, &fl_right, &pos_stay, &pos_left, &pos_right}) dfree(*b);
     if (hcount) cudaFreeHost(hcount);
     dfree(flags);
@@ -323,7 +324,7 @@ struct Context final : CtxBase {
     dfree(rs.vals_alt);
     dfree(rs.hist);
     dfree(rs.partials);
-    for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount}) dfree(*b);
+    for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount, &wcnt}) dfree(*b);
     n = count;
     cap = std::max<uint64_t>(want, 1);
     for (int b = 0; b < 2; ++b) {
@@ -340,6 +341,7 @@ struct Context final : CtxBase {
     rs.partials = dalloc<uint32_t>(scan_tiles(nh) + 1);
     for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp}) *b = dalloc<uint32_t>(cap);
     ncount = dalloc<uint32_t>(1);
+    wcnt = dalloc<uint32_t>(cap / 32 + 1);
     dfree(scan_partials_n);
     scan_partials_n = dalloc<uint32_t>(scan_tiles(cap) + 1);
     if (!hcount) CKG_CUDA(cudaMallocHost(&hcount, sizeof(uint32_t)));
@@ -437,7 +439,7 @@ struct Context final : CtxBase {
   void enqueue_sort() {
     PState<T> cs = state(cur);
     key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
-        cs, T(cfg.inv_dx), cfg.resolution, D, keys, core, ko_valid ? ko : nullptr, chg, dstat);
+        cs, T(cfg.inv_dx), cfg.resolution, D, keys, core, ko_valid ? ko : nullptr, chg, wcnt, dstat);
     launches += 1;
     if (ko_valid) {
       CKG_CUDA(cudaMemcpyAsync(hcount, &dstat->nchanged, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -445,8 +447,8 @@ struct Context final : CtxBase {
       const uint32_t nc = *hcount;
       last_changed = nc;
       if (nc != 0 && uint64_t(nc) * 8 <= n) {
-        exclusive_scan(chg, cpre, n, scan_partials_n, st);
-        compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci, ncount);
+        exclusive_scan(wcnt, cpre, (n + 31) / 32, scan_partials_n, st);
+        compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);
         launches += 4;
       }
       if (nc == 0) {
@@ -460,8 +462,12 @@ struct Context final : CtxBase {
         radix_sort_pairs(ck, ci, nc, key_bits, rs, st, &sck, &sci, ci);
         merge_unchanged_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, sck, sci, nc,
                                                                           perm_buf, skeys_tmp);
-        merge_changed_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, st>>>(ko, cpre, n, sck, sci, nc, perm_buf,
-                                                                          skeys_tmp);
+        // seg_begin/end still hold the previous substep's runs of ko unless
+        // the stored order was rebuilt since (slab migration)
+        const bool segs = !slab;
+        merge_changed_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, st>>>(
+            ko, chg, cpre, n, sck, sci, nc, segs ? seg_begin : nullptr, segs ? seg_end : nullptr, perm_buf,
+            skeys_tmp);
         launches += uint64_t((key_bits + kRadixBits - 1) / kRadixBits) * 5 + 2;
         std::swap(ko, skeys_tmp);
         perm = perm_buf;
@@ -493,7 +499,7 @@ struct Context final : CtxBase {
     compact_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(core, flags, dir, active, seg_begin, seg_end, nd,
                                                                pool_cap, dstat);
     if (slab) slab_ranges_kernel<<<1, 1, 0, st>>>(plane_start, D, bx_lo, bx_hi, dstat);
-    segments_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(skeys, n, seg_begin, seg_end);
+    segments_kernel<<<grid_for((n + 3) / 4, 256, 1 << 30), 256, 0, st>>>(skeys, n, seg_begin, seg_end);
   }
 
   template <int S>

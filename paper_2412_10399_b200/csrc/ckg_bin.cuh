@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
                                                             uint32_t* __restrict__ keys,
                                                             uint32_t* __restrict__ core,
                                                             const uint32_t* __restrict__ ko,
-                                                            uint32_t* __restrict__ chg, DevStatus* st) {
+                                                            uint32_t* __restrict__ cbits,
+                                                            uint32_t* __restrict__ wcnt, DevStatus* st) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool live = i < cur.n;
   bool ok = live, changed = false;
@@ -54,10 +55,7 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
     for (int a = 0; a < 3; ++a) kb[a] = key_axis(x[a], inv_dx, D);
     key = (uint32_t(kb[0]) * uint32_t(D) + uint32_t(kb[1])) * uint32_t(D) + uint32_t(kb[2]);
     keys[i] = key;
-    if (ko) {
-      changed = key != __ldg(ko + i);
-      chg[i] = changed ? 1u : 0u;
-    }
+    if (ko) changed = key != __ldg(ko + i);
     // footprint blocks relative to the key block: lo in {kb-1, kb}, hi in {kb, kb+1}
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -71,8 +69,14 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
     if (!ok) atomicOr(&st->inset_fail, 1u);
   }
   if (ko) {
+    // one word of changed flags and its count per warp (ckg_isort.cuh ranks
+    // from these instead of a per-particle scan)
     const uint32_t cb = __ballot_sync(0xffffffffu, changed);
-    if ((threadIdx.x & 31) == 0 && cb) atomicAdd(&st->nchanged, uint32_t(__popc(cb)));
+    if ((threadIdx.x & 31) == 0 && i < cur.n) {
+      cbits[i >> 5] = cb;
+      wcnt[i >> 5] = uint32_t(__popc(cb));
+      if (cb) atomicAdd(&st->nchanged, uint32_t(__popc(cb)));
+    }
   }
   // Lanes with the same footprint box (same key block and extent bits) mark
   // it once.  (A bounding box over different boxes would over-activate.)
@@ -162,11 +166,33 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t* __restrict__ cor
 __global__ void __launch_bounds__(256) segments_kernel(const uint32_t* __restrict__ skeys, uint64_t n,
                                                        uint32_t* __restrict__ seg_begin,
                                                        uint32_t* __restrict__ seg_end) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t k = skeys[i];
-  if (i == 0 || skeys[i - 1] != k) seg_begin[k] = uint32_t(i);
-  if (i == n - 1 || skeys[i + 1] != k) seg_end[k] = uint32_t(i + 1);
+  // four sorted keys per thread (16-byte loads); neighbours across threads
+  // by shuffles, across warps from memory
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t i0 = q * 4;
+  const int lane = threadIdx.x & 31;
+  uint32_t k[4];
+  if (i0 + 3 < n) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(skeys) + q);
+    k[0] = v.x, k[1] = v.y, k[2] = v.z, k[3] = v.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) k[e] = i0 + e < n ? skeys[i0 + e] : 0xffffffffu;
+  }
+  uint32_t prev = __shfl_up_sync(0xffffffffu, k[3], 1);
+  uint32_t next = __shfl_down_sync(0xffffffffu, k[0], 1);
+  if (lane == 0) prev = i0 > 0 && i0 - 1 < n ? skeys[i0 - 1] : 0xffffffffu;
+  if (lane == 31) next = i0 + 4 < n ? skeys[i0 + 4] : 0xffffffffu;
+  if (i0 >= n) return;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint64_t i = i0 + e;
+    if (i >= n) break;
+    const uint32_t kp = e == 0 ? prev : k[e - 1];
+    const uint32_t kn = (e == 3 || i + 1 >= n) ? (i + 1 < n ? next : 0xffffffffu) : k[e + 1];
+    if (i == 0 || kp != k[e]) seg_begin[k[e]] = uint32_t(i);
+    if (i == n - 1 || kn != k[e]) seg_end[k[e]] = uint32_t(i + 1);
+  }
 }
 
 }  // namespace ckg

@@ -18,26 +18,28 @@
 
 namespace ckg {
 
-__global__ void __launch_bounds__(256) changed_kernel(const uint32_t* __restrict__ keys,
-                                                      const uint32_t* __restrict__ ko, uint64_t n,
-                                                      uint32_t* __restrict__ chg) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) chg[i] = keys[i] != ko[i] ? 1u : 0u;
+// Changed flags are one ballot word per warp of 32 stored positions (cbits,
+// from key_footprint_kernel) with woff = exclusive scan of their popcounts, so
+// the number of changed positions before P is
+//   woff[P >> 5] + popc(cbits[P >> 5] & lanemask(P & 31)).
+__device__ __forceinline__ uint32_t changed_before(const uint32_t* __restrict__ cbits,
+                                                   const uint32_t* __restrict__ woff, uint64_t p) {
+  const uint32_t b = __ldg(cbits + (p >> 5));
+  return __ldg(woff + (p >> 5)) + uint32_t(__popc(b & ((1u << (p & 31)) - 1u)));
 }
 
-// After the exclusive scan: |C| and the compacted changed list (index order).
+// |C| entries in index order (compacted changed list).
 __global__ void __launch_bounds__(256) compact_changed_kernel(const uint32_t* __restrict__ keys,
-                                                              const uint32_t* __restrict__ chg,
-                                                              const uint32_t* __restrict__ cpre, uint64_t n,
-                                                              uint32_t* __restrict__ ck, uint32_t* __restrict__ ci,
-                                                              uint32_t* __restrict__ count) {
+                                                              const uint32_t* __restrict__ cbits,
+                                                              const uint32_t* __restrict__ woff, uint64_t n,
+                                                              uint32_t* __restrict__ ck, uint32_t* __restrict__ ci) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (chg[i]) {
-    ck[cpre[i]] = keys[i];
-    ci[cpre[i]] = uint32_t(i);
-  }
-  if (i == n - 1) *count = cpre[i] + chg[i];
+  const uint32_t b = __ldg(cbits + (i >> 5));
+  if (!((b >> (i & 31)) & 1u)) return;
+  const uint32_t pos = changed_before(cbits, woff, i);
+  ck[pos] = keys[i];
+  ci[pos] = uint32_t(i);
 }
 
 __global__ void __launch_bounds__(256) iota_kernel(uint32_t* __restrict__ p, uint64_t n) {
@@ -45,58 +47,106 @@ __global__ void __launch_bounds__(256) iota_kernel(uint32_t* __restrict__ p, uin
   if (i < n) p[i] = uint32_t(i);
 }
 
-// Unchanged particles: count changed entries ordered before (k, i).
+// Unchanged particles: count changed entries ordered before (k, i).  The
+// unchanged particles of a CTA are in increasing (k, i) order, so one thread
+// binary searches for the CTA's first one and every thread walks forward from
+// that bound (usually zero or one step: only changed entries whose (key,
+// index) falls inside the CTA's range), with a binary search when the walk is
+// long.
 __global__ void __launch_bounds__(256) merge_unchanged_kernel(const uint32_t* __restrict__ keys,
-                                                              const uint32_t* __restrict__ chg,
-                                                              const uint32_t* __restrict__ cpre, uint64_t n,
+                                                              const uint32_t* __restrict__ cbits,
+                                                              const uint32_t* __restrict__ woff, uint64_t n,
                                                               const uint32_t* __restrict__ ck,
                                                               const uint32_t* __restrict__ ci, uint32_t nc,
                                                               uint32_t* __restrict__ perm,
                                                               uint32_t* __restrict__ skeys) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n || chg[i]) return;
-  const uint32_t k = keys[i];
-  uint32_t lo = 0, hi = nc;  // first c with (ck, ci) >= (k, i)
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    const uint32_t km = __ldg(ck + mid);
-    if (km < k || (km == k && __ldg(ci + mid) < uint32_t(i)))
-      lo = mid + 1;
-    else
-      hi = mid;
+  __shared__ uint32_t s_lo;
+  const uint64_t base = uint64_t(blockIdx.x) * blockDim.x;
+  const uint64_t i = base + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  auto before = [&](uint32_t j, uint32_t k, uint64_t idx) {  // changed entry j ordered before (k, idx)?
+    const uint32_t kj = __ldg(ck + j);
+    return kj < k || (kj == k && uint64_t(__ldg(ci + j)) < idx);
+  };
+  auto lower = [&](uint32_t lo, uint32_t hi, uint32_t k, uint64_t idx) {
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (before(mid, k, idx)) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  // (key of the CTA's first unchanged entry, base) orders before or equal to
+  // every unchanged (k, i) of the CTA, so its bound is a common start
+  if (threadIdx.x == 0) {
+    uint32_t kmin = 0xffffffffu;
+    for (uint64_t t = base; t < min(base + blockDim.x, n); ++t) {
+      const uint32_t b = __ldg(cbits + (t >> 5));
+      if (!((b >> (t & 31)) & 1u)) {
+        kmin = keys[t];  // first unchanged entry: smallest (k, i) of the CTA's unchanged ones
+        break;
+      }
+    }
+    s_lo = kmin == 0xffffffffu ? 0u : lower(0, nc, kmin, base);
   }
-  const uint64_t pos = (i - cpre[i]) + lo;
+  __syncthreads();
+  if (i >= n) return;
+  const uint32_t b = __ldg(cbits + (i >> 5));
+  if ((b >> lane) & 1u) return;
+  const uint32_t k = keys[i];
+  uint32_t lo = s_lo;
+  int steps = 0;
+  while (lo < nc && steps < 8 && before(lo, k, i)) {
+    ++lo;
+    ++steps;
+  }
+  if (steps == 8) lo = lower(lo, nc, k, i);
+  const uint64_t pos = (i - (__ldg(woff + (i >> 5)) + uint32_t(__popc(b & ((1u << lane) - 1u))))) + lo;
   perm[pos] = uint32_t(i);
   skeys[pos] = k;
 }
 
 // Changed particles: count unchanged entries ordered before (k, j) using the
 // sorted old keys ko (unchanged entries carry key == ko).
+// When the previous substep's segment table is still intact (seg_begin/end
+// hold the runs of ko), a non-empty run gives lower/upper_bound(ko, k)
+// directly; otherwise binary search.
 __global__ void __launch_bounds__(256) merge_changed_kernel(const uint32_t* __restrict__ ko,
-                                                            const uint32_t* __restrict__ cpre, uint64_t n,
+                                                            const uint32_t* __restrict__ cbits,
+                                                            const uint32_t* __restrict__ woff, uint64_t n,
                                                             const uint32_t* __restrict__ ck,
                                                             const uint32_t* __restrict__ ci, uint32_t nc,
+                                                            const uint32_t* __restrict__ old_begin,
+                                                            const uint32_t* __restrict__ old_end,
                                                             uint32_t* __restrict__ perm,
                                                             uint32_t* __restrict__ skeys) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nc) return;
   const uint32_t k = ck[r], j = ci[r];
-  uint64_t lo = 0, hi = n;  // lower_bound(ko, k)
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (__ldg(ko + mid) < k) lo = mid + 1; else hi = mid;
+  uint64_t lb, ub;
+  const uint32_t ob = old_begin ? __ldg(old_begin + k) : 0u, oe = old_begin ? __ldg(old_end + k) : 0u;
+  if (oe > ob) {
+    lb = ob;
+    ub = oe;
+  } else {
+    uint64_t lo = 0, hi = n;  // lower_bound(ko, k)
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (__ldg(ko + mid) < k) lo = mid + 1; else hi = mid;
+    }
+    lb = lo;
+    if (!old_begin) {  // no segment table: upper_bound(ko, k) as well
+      hi = n;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (__ldg(ko + mid) <= k) lo = mid + 1; else hi = mid;
+      }
+    }
+    ub = lo;  // (with a segment table an empty run means lower == upper bound)
   }
-  const uint64_t lb = lo;
-  hi = n;  // upper_bound(ko, k)
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (__ldg(ko + mid) <= k) lo = mid + 1; else hi = mid;
-  }
-  const uint64_t ub = lo;
   // positions [0, P) hold exactly the entries with (ko, idx) < (k, j)
   const uint64_t P = j < lb ? lb : (j > ub ? ub : j);
-  const uint64_t changed_before = P < n ? cpre[P] : uint64_t(nc);
-  const uint64_t pos = r + (P - changed_before);
+  const uint64_t cb = P < n ? changed_before(cbits, woff, P) : uint64_t(nc);
+  const uint64_t pos = r + (P - cb);
   perm[pos] = j;
   skeys[pos] = k;
 }
