@@ -460,15 +460,17 @@ struct Context final : CtxBase {
       if (uint64_t(nc) * 8 <= n) {
         uint32_t *sck = nullptr, *sci = nullptr;
         radix_sort_pairs(ck, ci, nc, key_bits, rs, st, &sck, &sci, ci);
-        merge_unchanged_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, sck, sci, nc,
-                                                                          perm_buf, skeys_tmp);
+        const uint64_t tiles = (n + kMergeTile - 1) / kMergeTile;
+        merge_bounds_kernel<<<grid_for(tiles, 256, 1 << 30), 256, 0, st>>>(keys, chg, n, sck, sci, nc, wcnt);
+        merge_unchanged_kernel<<<unsigned(tiles), kMergeTile, 0, st>>>(keys, chg, cpre, n, sck, sci, nc, wcnt,
+                                                                       perm_buf, skeys_tmp);
         // seg_begin/end still hold the previous substep's runs of ko unless
         // the stored order was rebuilt since (slab migration)
         const bool segs = !slab;
         merge_changed_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, st>>>(
             ko, chg, cpre, n, sck, sci, nc, segs ? seg_begin : nullptr, segs ? seg_end : nullptr, perm_buf,
             skeys_tmp);
-        launches += uint64_t((key_bits + kRadixBits - 1) / kRadixBits) * 5 + 2;
+        launches += uint64_t((key_bits + kRadixBits - 1) / kRadixBits) * 5 + 3;
         std::swap(ko, skeys_tmp);
         perm = perm_buf;
         skeys = ko;

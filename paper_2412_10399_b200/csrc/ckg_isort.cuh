@@ -48,58 +48,69 @@ __global__ void __launch_bounds__(256) iota_kernel(uint32_t* __restrict__ p, uin
 }
 
 // Unchanged particles: count changed entries ordered before (k, i).  The
-// unchanged particles of a CTA are in increasing (k, i) order, so one thread
-// binary searches for the CTA's first one and every thread walks forward from
-// that bound (usually zero or one step: only changed entries whose (key,
-// index) falls inside the CTA's range), with a binary search when the walk is
-// long.
-__global__ void __launch_bounds__(256) merge_unchanged_kernel(const uint32_t* __restrict__ keys,
-                                                              const uint32_t* __restrict__ cbits,
-                                                              const uint32_t* __restrict__ woff, uint64_t n,
-                                                              const uint32_t* __restrict__ ck,
-                                                              const uint32_t* __restrict__ ci, uint32_t nc,
-                                                              uint32_t* __restrict__ perm,
-                                                              uint32_t* __restrict__ skeys) {
-  __shared__ uint32_t s_lo;
-  const uint64_t base = uint64_t(blockIdx.x) * blockDim.x;
-  const uint64_t i = base + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  auto before = [&](uint32_t j, uint32_t k, uint64_t idx) {  // changed entry j ordered before (k, idx)?
-    const uint32_t kj = __ldg(ck + j);
-    return kj < k || (kj == k && uint64_t(__ldg(ci + j)) < idx);
-  };
-  auto lower = [&](uint32_t lo, uint32_t hi, uint32_t k, uint64_t idx) {
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (before(mid, k, idx)) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-  };
-  // (key of the CTA's first unchanged entry, base) orders before or equal to
-  // every unchanged (k, i) of the CTA, so its bound is a common start
-  if (threadIdx.x == 0) {
-    uint32_t kmin = 0xffffffffu;
-    for (uint64_t t = base; t < min(base + blockDim.x, n); ++t) {
-      const uint32_t b = __ldg(cbits + (t >> 5));
-      if (!((b >> (t & 31)) & 1u)) {
-        kmin = keys[t];  // first unchanged entry: smallest (k, i) of the CTA's unchanged ones
-        break;
-      }
-    }
-    s_lo = kmin == 0xffffffffu ? 0u : lower(0, nc, kmin, base);
+// unchanged entries of a 256-position tile are in increasing (k, i) order, so
+// merge_bounds_kernel binary searches once per tile for (key of its first
+// unchanged entry, tile start) -- one thread per tile, all tiles in a single
+// wave -- and merge_unchanged_kernel walks forward from that bound (usually
+// zero or one step: only changed entries whose (key, index) falls inside the
+// tile), with a binary search when the walk is long.
+__device__ __forceinline__ bool changed_entry_before(const uint32_t* __restrict__ ck,
+                                                     const uint32_t* __restrict__ ci, uint32_t j, uint32_t k,
+                                                     uint64_t idx) {
+  const uint32_t kj = __ldg(ck + j);
+  return kj < k || (kj == k && uint64_t(__ldg(ci + j)) < idx);
+}
+__device__ __forceinline__ uint32_t changed_lower(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ ci,
+                                                  uint32_t lo, uint32_t hi, uint32_t k, uint64_t idx) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (changed_entry_before(ck, ci, mid, k, idx)) lo = mid + 1; else hi = mid;
   }
-  __syncthreads();
+  return lo;
+}
+
+constexpr int kMergeTile = 256;
+
+__global__ void __launch_bounds__(256) merge_bounds_kernel(const uint32_t* __restrict__ keys,
+                                                           const uint32_t* __restrict__ cbits, uint64_t n,
+                                                           const uint32_t* __restrict__ ck,
+                                                           const uint32_t* __restrict__ ci, uint32_t nc,
+                                                           uint32_t* __restrict__ tile_lo) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t base = t * kMergeTile;
+  if (base >= n) return;
+  uint64_t first = n;
+  for (int w = 0; w < kMergeTile / 32 && base + 32 * w < n; ++w) {
+    const uint32_t un = ~__ldg(cbits + (base >> 5) + w);
+    if (un) {
+      first = base + 32 * w + (__ffs(un) - 1);
+      break;
+    }
+  }
+  tile_lo[t] = first < n ? changed_lower(ck, ci, 0, nc, keys[first], base) : 0u;
+}
+
+__global__ void __launch_bounds__(kMergeTile) merge_unchanged_kernel(const uint32_t* __restrict__ keys,
+                                                                     const uint32_t* __restrict__ cbits,
+                                                                     const uint32_t* __restrict__ woff, uint64_t n,
+                                                                     const uint32_t* __restrict__ ck,
+                                                                     const uint32_t* __restrict__ ci, uint32_t nc,
+                                                                     const uint32_t* __restrict__ tile_lo,
+                                                                     uint32_t* __restrict__ perm,
+                                                                     uint32_t* __restrict__ skeys) {
+  const uint64_t i = uint64_t(blockIdx.x) * kMergeTile + threadIdx.x;
+  const int lane = threadIdx.x & 31;
   if (i >= n) return;
   const uint32_t b = __ldg(cbits + (i >> 5));
   if ((b >> lane) & 1u) return;
   const uint32_t k = keys[i];
-  uint32_t lo = s_lo;
+  uint32_t lo = __ldg(tile_lo + blockIdx.x);
   int steps = 0;
-  while (lo < nc && steps < 8 && before(lo, k, i)) {
+  while (lo < nc && steps < 8 && changed_entry_before(ck, ci, lo, k, i)) {
     ++lo;
     ++steps;
   }
-  if (steps == 8) lo = lower(lo, nc, k, i);
+  if (steps == 8) lo = changed_lower(ck, ci, lo, nc, k, i);
   const uint64_t pos = (i - (__ldg(woff + (i >> 5)) + uint32_t(__popc(b & ((1u << lane) - 1u))))) + lo;
   perm[pos] = uint32_t(i);
   skeys[pos] = k;
