@@ -83,14 +83,17 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
   const uint64_t gbox = ok ? ((uint64_t(key) << 8) | ext) : (~0ull - (threadIdx.x & 31));
   const uint32_t peers = __match_any_sync(0xffffffffu, gbox);
   if (!ok || (__ffs(peers) - 1) != int(threadIdx.x & 31)) return;
-  const int x0 = kb[0] - int(ext & 1u), x1 = kb[0] + int((ext >> 1) & 1u);
-  const int y0 = kb[1] - int((ext >> 2) & 1u), y1 = kb[1] + int((ext >> 3) & 1u);
-  const int z0 = kb[2] - int((ext >> 4) & 1u), z1 = kb[2] + int((ext >> 5) & 1u);
-  for (int bi = x0; bi <= x1; ++bi)
-    for (int bj = y0; bj <= y1; ++bj)
-      for (int bk = z0; bk <= z1; ++bk)
-        if (bi >= 0 && bj >= 0 && bk >= 0 && bi < D && bj < D && bk < D)
-          core[(int64_t(bi) * D + bj) * D + bk] = 1u;
+  // inset particles (s in [2, res-2]) have footprint cells in [1, res-1], so
+  // every box block lies inside the (res/4 + 2)^3 directory: no bounds checks
+  const int nx = 1 + int(ext & 1u) + int((ext >> 1) & 1u);
+  const int ny = 1 + int((ext >> 2) & 1u) + int((ext >> 3) & 1u);
+  const int nz = 1 + int((ext >> 4) & 1u) + int((ext >> 5) & 1u);
+  const int64_t DD = int64_t(D) * D;
+  uint32_t* c0 = core + (int64_t(kb[0] - int(ext & 1u)) * D + (kb[1] - int((ext >> 2) & 1u))) * D +
+                 (kb[2] - int((ext >> 4) & 1u));
+  for (int a = 0; a < nx; ++a)
+    for (int b = 0; b < ny; ++b)
+      for (int k = 0; k < nz; ++k) c0[a * DD + b * D + k] = 1u;
 }
 
 // Lowest sorted index violating the inset (only runs its loop on failure).
