@@ -117,15 +117,19 @@ def dist_env():
 
 
 def algorithmic_bytes(n, nblocks, scheme, precision):
-    """SURVEY §8(d) compulsory bytes per launch:
-    P2G reads x,v,F,(B),m,V0,mat + perm, writes every active node once
-    (2 grids x {m,p} x 64 nodes); G2P reads x,F,J,m,V0,mat (+B for PIC) + perm
-    and the nodal velocities, writes the full 27-field state + mat."""
+    """SURVEY §8(d) compulsory bytes per launch for the reference semantics
+    (stress recomputed in P2G, sort applied through the G2P writes):
+    P2G reads x, v, F, B, m, V0, mat (FP64 APIC 212 B/particle; PIC -72 B)
+    and writes every active node once (2 grids x 64 nodes x {m, p} = 32 B/node);
+    G2P reads x, F, mat (100 B) and writes x, v, F, B (192 B; PIC -72 B),
+    plus the nodal velocities (24 B/node).  The implementation's own choices
+    (stress cache, full-state rewrite) are not counted: profiles/traffic.json
+    holds what the kernels actually move."""
     s = precision
-    b_read = 9 * s if scheme != "pic" else 0
-    p2g = n * (3 * s + 3 * s + 9 * s + b_read + s + s + 4 + 4) + nblocks * 2 * 64 * 4 * s
-    g2p = n * (3 * s + 9 * s + s + s + s + 4 + 4 + (9 * s if scheme == "pic" else 0) + 27 * s + 4) \
-        + nblocks * 2 * 64 * 3 * s
+    b = 9 * s if scheme != "pic" else 0
+    nodes = nblocks * 2 * 64
+    p2g = n * (3 * s + 3 * s + 9 * s + b + s + s + 4) + nodes * 4 * s
+    g2p = n * (3 * s + 9 * s + 4) + n * (3 * s + 3 * s + 9 * s + b) + nodes * 3 * s
     return p2g, g2p
 
 
