@@ -47,6 +47,9 @@ constexpr int kXferWarps = kXferThreads / 32;
 #ifndef CKG_G2P_DUAL
 #define CKG_G2P_DUAL 0
 #endif
+#ifndef CKG_P2G_EXP
+#define CKG_P2G_EXP 0  // development experiments only (1: no node ordering, 2: no tile RMW)
+#endif
 #ifndef CKG_P2G_MINB
 #define CKG_P2G_MINB 2
 #endif
@@ -62,6 +65,46 @@ constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full 
 constexpr int kPT = 5;
 constexpr int kPTNodes = kPT * kPT * kPT;  // 125
 constexpr int kPTVals = 2 * 4 * kPTNodes;  // 1000
+// Tile layout [grid][node][m, px, py, pz]: one node's four values are
+// contiguous, so a node update is two 16-byte shared loads/stores (FP64).
+#ifndef CKG_P2G_NODEMAJOR
+#define CKG_P2G_NODEMAJOR 0
+#endif
+constexpr int kNS = CKG_P2G_NODEMAJOR ? 4 : 1;         // node stride in a tile grid
+constexpr int kVS = CKG_P2G_NODEMAJOR ? 1 : kPTNodes;  // value stride
+__device__ __forceinline__ void tile_add4(double* p, const double (&o)[4]) {
+  if (CKG_P2G_NODEMAJOR) {
+    double2* q = reinterpret_cast<double2*>(p);
+    double2 a = q[0], b = q[1];
+    a.x += o[0];
+    a.y += o[1];
+    b.x += o[2];
+    b.y += o[3];
+    q[0] = a;
+    q[1] = b;
+  } else {
+    p[0] += o[0];
+    p[kVS] += o[1];
+    p[2 * kVS] += o[2];
+    p[3 * kVS] += o[3];
+  }
+}
+__device__ __forceinline__ void tile_add4(float* p, const float (&o)[4]) {
+  if (CKG_P2G_NODEMAJOR) {
+    float4* q = reinterpret_cast<float4*>(p);
+    float4 a = *q;
+    a.x += o[0];
+    a.y += o[1];
+    a.z += o[2];
+    a.w += o[3];
+    *q = a;
+  } else {
+    p[0] += o[0];
+    p[kVS] += o[1];
+    p[2 * kVS] += o[2];
+    p[3 * kVS] += o[3];
+  }
+}
 template <typename T>
 constexpr size_t p2g_smem_bytes() {
   return size_t(kXferWarps) * kPTVals * sizeof(T);
@@ -271,7 +314,10 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
             o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
           }
         };
-        T* p0 = wt + g * 4 * kPTNodes + (lx * kPT + ly) * kPT + lz;
+        T* p0 = wt + g * 4 * kPTNodes + ((lx * kPT + ly) * kPT + lz) * kNS;
+#if CKG_P2G_EXP == 2
+        T sink = T(0);
+#endif
         if (maxrank == 0) {
           // fast path: every lane owns a distinct base cell in this warp, so
           // at a fixed node offset all lanes write distinct nodes
@@ -284,16 +330,17 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
                 for (int u = 0; u < 2; ++u) {
                   T o[4];
                   contrib(s, t, u, o);
-                  T* p = p0 + (s * kPT + t) * kPT + u;
-                  if (in_tile) {
-                  p[0] += o[0];
-                  p[kPTNodes] += o[1];
-                  p[2 * kPTNodes] += o[2];
-                  p[3 * kPTNodes] += o[3];
-                  }
+                  T* p = p0 + ((s * kPT + t) * kPT + u) * kNS;
+#if CKG_P2G_EXP == 2
+                  sink += o[0] + o[1] + o[2] + o[3];
+#else
+                  if (in_tile) tile_add4(p, o);
+#endif
+#if CKG_P2G_EXP == 0
                   // node (s,t,u) of one lane can be node (0,0,0) of its
                   // neighbour: order the read-modify-writes across lanes
                   __syncwarp();
+#endif
                 }
           }
         } else {
@@ -303,18 +350,16 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
             const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
             T o[4];
             contrib(s, t, u, o);
-            T* p = p0 + (s * kPT + t) * kPT + u;
+            T* p = p0 + ((s * kPT + t) * kPT + u) * kNS;
             for (uint32_t layer = 0; layer <= maxrank; ++layer) {
-              if (in_tile && rank == layer) {
-                p[0] += o[0];
-                p[kPTNodes] += o[1];
-                p[2 * kPTNodes] += o[2];
-                p[3 * kPTNodes] += o[3];
-              }
+              if (in_tile && rank == layer) tile_add4(p, o);
               __syncwarp();
             }
           }
         }
+#if CKG_P2G_EXP == 2
+        if (sink == T(12345)) p0[0] = sink;
+#endif
         if (valid && !in_tile) {
           // footprint outside the block tile: direct REDs through the directory
 #pragma unroll 1
@@ -348,8 +393,8 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
       int g, v, i, j, k;
       if (e < 4 * kPTNodes) {
         g = 0;
-        v = e / kPTNodes;
-        const int node = e % kPTNodes;
+        v = CKG_P2G_NODEMAJOR ? e % 4 : e / kPTNodes;
+        const int node = CKG_P2G_NODEMAJOR ? e / 4 : e % kPTNodes;
         i = node / (kPT * kPT);
         j = (node / kPT) % kPT;
         k = node % kPT;
@@ -371,7 +416,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
         for (int w = 0; w < kXferWarps; ++w) {
           const int li = i - 1 + (w & 1), lj = j - 1 + ((w >> 1) & 1), lk = k - 1 + ((w >> 2) & 1);
           if (li >= 0 && lj >= 0 && lk >= 0 && li < kPT && lj < kPT && lk < kPT) {
-            T* q = tiles + w * kPTVals + 4 * kPTNodes + v * kPTNodes + (li * kPT + lj) * kPT + lk;
+            T* q = tiles + w * kPTVals + 4 * kPTNodes + v * kVS + ((li * kPT + lj) * kPT + lk) * kNS;
             sum += *q;
             *q = T(0);
           }
