@@ -408,8 +408,10 @@ int64_t ckref_p2g(const ckg_config* cfg, const void* particles, uint64_t n, doub
 }
 
 // Stable-sort permutation and keys as the reference computes them: the
-// particle's position in the pre-sort array is smuggled through the material
-// tag (sort_particles reads only x, simulation.hpp:248-274).
+// particle's position in the pre-sort array is smuggled through volume0
+// (sort_particles reads only x, simulation.hpp:248-274; restore's
+// refresh_velocity_stats reads v, J and indexes the material table, so the
+// material tag must stay a valid index).  Exact for n < 2^24 in float.
 int32_t ckref_sort(const ckg_config* cfg, const void* particles, uint64_t n, uint32_t* keys,
                    uint32_t* order) {
   auto run = [&](auto tag) {
@@ -418,11 +420,14 @@ int32_t ckref_sort(const ckg_config* cfg, const void* particles, uint64_t n, uin
     SimConfig<T> c = with_dummy_body(to_config<T>(*cfg, &ex));
     Simulation<T> sim(c);
     std::vector<Particle<T>> ps = from_raw<T>(particles, n);
-    for (uint64_t i = 0; i < n; ++i) ps[i].material = static_cast<uint32_t>(i);
+    for (uint64_t i = 0; i < n; ++i) {
+      ps[i].material = 0;
+      ps[i].volume0 = static_cast<T>(i);
+    }
     sim.restore(std::move(ps), T(0), 0, 0, T(cfg->mass_eps));
     sim.sort_particles();
     for (uint64_t i = 0; i < n; ++i) {
-      uint32_t src = sim.particles_[i].material;
+      uint32_t src = static_cast<uint32_t>(sim.particles_[i].volume0);
       order[i] = src;
       keys[i] = static_cast<uint32_t>(sim.keys_[src]);
     }
