@@ -45,6 +45,7 @@ extern "C" {
 #define CKG_NUM_FLUID_J 9            /* transfer.hpp:616 NumericalError "fluid compression drove J <= 0" */
 #define CKG_NUM_NONFINITE 10         /* simulation.hpp:384-387 NumericalError "non-finite particle state after step N" */
 #define CKG_NUM_INACTIVE_BLOCK 11    /* grid.hpp:166-169 NumericalError "access to inactive grid block ..." (defensive) */
+#define CKG_NUM_SUBSTEP_LIMIT 12     /* simulation.hpp:205-207 NumericalError "substep limit exceeded within one frame at t = T" */
 
 #define CKG_MAX_MATERIALS 16
 #define CKG_MAX_BOUNDARIES 32
@@ -151,6 +152,41 @@ typedef struct ckg_step_out {
   int32_t _pad2;
 } ckg_step_out;
 
+/* advance_frame (simulation.hpp:193-211) on the device: the host passes the
+ * reference driver's bookkeeping (time_, frame_index_, vmax_, min_j_ and the
+ * config's cfl / max_dt / frame_dt / max_substeps_per_frame); the substeps,
+ * cfl_dt (simulation.hpp:134-145) and the frame-boundary test run on the GPU as
+ * one CUDA-graph launch (conditional WHILE node), with no host round trip per
+ * substep.  Without a per-substep callback this replaces the reference loop;
+ * with one, callers keep the host loop over ckg_step. */
+typedef struct ckg_frame_in {
+  double time;                        /* time_ at entry (T value) */
+  double frame_dt;                    /* cfg.frame_dt */
+  uint64_t frame_index;               /* frame_index_ (frame_end = frame_dt * (frame_index + 1)) */
+  double cfl, max_dt;                 /* cfg.cfl, cfg.max_dt */
+  uint64_t max_substeps;              /* cfg.max_substeps_per_frame */
+  double vmax;                        /* vmax_ */
+  double min_j[CKG_MAX_MATERIALS];    /* min_j_ */
+} ckg_frame_in;
+
+typedef struct ckg_frame_out {
+  uint64_t substeps;                  /* substeps completed in this call */
+  double time;                        /* time_ after the call (frame_end when the frame completed) */
+  double last_dt;                     /* dt of the last completed substep */
+  double vmax;                        /* vmax_ / min_j_ after the last completed substep */
+  double min_j[CKG_MAX_MATERIALS];
+  double device_ms;                   /* device time of the frame */
+  int32_t status;                     /* CKG_OK / CKG_ERR_* (as ckg_step; the failing substep is not counted) */
+  int32_t error_code;                 /* CKG_NUM_* (CKG_NUM_SUBSTEP_LIMIT after max_substeps + 1 substeps) */
+  int32_t error_axis;
+  int32_t error_phase;
+  uint64_t error_particle;
+  uint64_t active_blocks;
+  uint64_t kernel_launches;           /* kernels executed (graph nodes x substeps) */
+  int32_t graph;                      /* 1: device-driven graph; 0: host loop (slab mode, growing pool) */
+  int32_t _pad;
+} ckg_frame_out;
+
 /* DiagnosticsRow<T> (simulation.hpp:44-53), computed on the device
  * (compute_diagnostics, simulation.hpp:55-69). */
 typedef struct ckg_diagnostics {
@@ -190,6 +226,9 @@ int32_t ckg_step(ckg_ctx* ctx, double dt, ckg_step_out* out);
  * (errors are latched on the device and reported by ckg_sync).  `out` may be
  * NULL; when given it receives the state after the last substep. */
 int32_t ckg_step_many(ckg_ctx* ctx, double dt, int32_t count, ckg_step_out* out);
+/* Simulation::advance_frame() without a callback (simulation.hpp:193-211, :213-215). */
+int32_t ckg_advance_frame(ckg_ctx* ctx, const ckg_frame_in* in, ckg_frame_out* out);
+
 /* Runs step(dt) only up to and including `stop_after` (CKG_PHASE_*); particle
  * state is not advanced unless stop_after == CKG_PHASE_G2P.  Test/parity hook
  * (the reference exposes the same cut points through full_step's pieces,

@@ -180,8 +180,43 @@ class Simulation {
     }
     ++frame_index_;
   }
+  // Without a per-substep callback the whole frame runs on the device
+  // (ckg_advance_frame: one CUDA-graph launch, cfl_dt and the frame-boundary
+  // test evaluated on the GPU, no host round trip per substep).
   void advance_frame() {
-    advance_frame([](Simulation&, T) {});
+    if (host_dirty_) upload();
+    ckg_frame_in in{};
+    in.time = double(time_);
+    in.frame_dt = double(cfg_.frame_dt);
+    in.frame_index = std::uint64_t(frame_index_);
+    in.cfl = double(cfg_.cfl);
+    in.max_dt = double(cfg_.max_dt);
+    in.max_substeps = std::uint64_t(cfg_.max_substeps_per_frame);
+    in.vmax = double(vmax_);
+    for (int m = 0; m < CKG_MAX_MATERIALS; ++m)
+      in.min_j[m] = m < int(min_j_.size()) ? double(min_j_[m]) : 1.0;
+    ckg_frame_out out{};
+    const int32_t rc = ckg_advance_frame(ctx_, &in, &out);
+    // completed substeps are kept also when a later one failed (as the
+    // reference, whose state advances substep by substep)
+    time_ = T(out.time);
+    step_count_ += out.substeps;
+    vmax_ = T(out.vmax);
+    for (std::size_t m = 0; m < min_j_.size(); ++m) min_j_[m] = T(out.min_j[m]);
+    timers_.substeps += out.substeps;
+    const std::uint64_t per = cfg_.scheme == TransferScheme::mls ? 32 : 16;
+    counters_.p2g_node_visits += per * host_.size() * out.substeps;
+    counters_.g2p_node_visits += 16 * host_.size() * out.substeps;
+    counters_.p2g_transfers += host_.size() * out.substeps;
+    counters_.g2p_transfers += host_.size() * out.substeps;
+    if (out.substeps) host_valid_ = false;
+    if (rc != CKG_OK) {
+      ckg_step_out so{};
+      so.error_code = out.error_code;
+      so.error_particle = out.error_particle;
+      throw_for(rc, so);
+    }
+    ++frame_index_;
   }
 
   // B200 extension: the same row reduced on the device (no particle download;

@@ -27,6 +27,7 @@ NUM_F_INVERTED = 8
 NUM_FLUID_J = 9
 NUM_NONFINITE = 10
 NUM_INACTIVE_BLOCK = 11
+NUM_SUBSTEP_LIMIT = 12
 
 MAX_MATERIALS = 16
 MAX_BOUNDARIES = 32
@@ -91,6 +92,26 @@ class StepOut(C.Structure):
         ("kernel_launches", C.c_uint64),
         ("sort_changed", C.c_uint64),
         ("sort_kind", C.c_int32), ("_pad2", C.c_int32),
+    ]
+
+
+class FrameIn(C.Structure):
+    """ckg_frame_in: the reference driver's advance_frame bookkeeping."""
+    _fields_ = [
+        ("time", C.c_double), ("frame_dt", C.c_double), ("frame_index", C.c_uint64),
+        ("cfl", C.c_double), ("max_dt", C.c_double), ("max_substeps", C.c_uint64),
+        ("vmax", C.c_double), ("min_j", C.c_double * MAX_MATERIALS),
+    ]
+
+
+class FrameOut(C.Structure):
+    _fields_ = [
+        ("substeps", C.c_uint64), ("time", C.c_double), ("last_dt", C.c_double),
+        ("vmax", C.c_double), ("min_j", C.c_double * MAX_MATERIALS), ("device_ms", C.c_double),
+        ("status", C.c_int32), ("error_code", C.c_int32),
+        ("error_axis", C.c_int32), ("error_phase", C.c_int32),
+        ("error_particle", C.c_uint64), ("active_blocks", C.c_uint64),
+        ("kernel_launches", C.c_uint64), ("graph", C.c_int32), ("_pad", C.c_int32),
     ]
 
 

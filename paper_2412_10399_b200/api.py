@@ -309,8 +309,15 @@ class Simulation:
             dt = min(dt, T(self.cfg.max_dt))
         return float(min(dt, T(remaining)))
 
-    def advance_frame(self, cb: Optional[Callable[["Simulation", float], None]] = None):
-        """advance_frame (simulation.hpp:193-211)."""
+    def advance_frame(self, cb: Optional[Callable[["Simulation", float], None]] = None,
+                      device: bool = True) -> int:
+        """advance_frame (simulation.hpp:193-211); returns the substeps taken.
+
+        Without a per-substep callback the whole frame runs on the device
+        (ckg_advance_frame: CUDA graph, device cfl_dt, no host round trip per
+        substep); with one (or device=False) this host loop over step() runs."""
+        if cb is None and device:
+            return self._advance_frame_device()
         T = self._T
         frame_dt = T(self.cfg.frame_dt)
         frame_end = frame_dt * T(self._frame_index + 1)
@@ -328,6 +335,41 @@ class Simulation:
             if steps > self.cfg.max_substeps_per_frame:
                 raise NumericalError(f"substep limit exceeded within one frame at t = {self._time:.6f}")
         self._frame_index += 1
+        return steps
+
+    def _advance_frame_device(self) -> int:
+        fin = abi.FrameIn()
+        fin.time = self._time
+        fin.frame_dt = float(self._T(self.cfg.frame_dt))
+        fin.frame_index = self._frame_index
+        fin.cfl = float(self._T(self.cfg.cfl))
+        fin.max_dt = float(self._T(self.cfg.max_dt))
+        fin.max_substeps = int(self.cfg.max_substeps_per_frame)
+        fin.vmax = self._vmax
+        for m in range(abi.MAX_MATERIALS):
+            fin.min_j[m] = self._min_j[m] if m < len(self._min_j) else 1.0
+        out = abi.FrameOut()
+        rc = lib().ckg_advance_frame(self._ctx, C.byref(fin), C.byref(out))
+        # bookkeeping of the completed substeps, also when a later one failed
+        self._time = float(out.time)
+        self._step_count += int(out.substeps)
+        self._timers.substeps += int(out.substeps)
+        per = 32 if self.cfg.scheme == "mls" else 16
+        c = self._counters
+        c.p2g_node_visits += per * self._n * int(out.substeps)
+        c.g2p_node_visits += 16 * self._n * int(out.substeps)
+        c.p2g_transfers += self._n * int(out.substeps)
+        c.g2p_transfers += self._n * int(out.substeps)
+        self._vmax = float(out.vmax)
+        self._min_j = [float(out.min_j[m]) for m in range(len(self.cfg.materials))]
+        if rc != abi.OK:
+            so = abi.StepOut()
+            so.error_code = out.error_code
+            so.error_particle = out.error_particle
+            _raise_for(self._ctx, rc, so)
+        self._frame_index += 1
+        self.last_frame = out
+        return int(out.substeps)
 
     def diagnostics(self) -> DiagnosticsRow:
         """compute_diagnostics (simulation.hpp:55-69) as a device reduction."""

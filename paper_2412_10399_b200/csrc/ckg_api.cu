@@ -16,6 +16,7 @@
 
 #include "../../include/ckmpm_b200.h"
 #include "ckg_bin.cuh"
+#include "ckg_frame.cuh"
 #include "ckg_isort.cuh"
 #include "ckg_kernels.cuh"
 #include "ckg_scan.cuh"
@@ -89,6 +90,7 @@ struct CtxBase {
   virtual int download(void* p, uint64_t n) = 0;
   virtual uint64_t count() const = 0;
   virtual int step(double dt, int stop_after, int count, ckg_step_out* out) = 0;
+  virtual int advance_frame(const ckg_frame_in* in, ckg_frame_out* out) = 0;
   virtual int debug_sort(uint32_t* keys, uint32_t* order, uint64_t n) = 0;
   virtual int debug_bases(int32_t* bases, uint64_t n) = 0;
   virtual uint64_t active_blocks() = 0;
@@ -170,6 +172,25 @@ struct Context final : CtxBase {
   double* dacc = nullptr;  // diagnostics accumulators (11)
   uint64_t last_active = 0;
   bool grid_valid = false;
+  // device frame driver (ckg_frame.cuh): one instantiated graph per starting
+  // state buffer, rebuilt when anything baked into it changes
+  FrameState* dframe = nullptr;
+  FrameState* hframe = nullptr;  // pinned
+  T* ddt = nullptr;
+  uint32_t* dnc = nullptr;
+  cudaStream_t cst[3] = {nullptr, nullptr, nullptr};  // capture streams of the conditional bodies
+  cudaGraphExec_t fexec[2] = {nullptr, nullptr};
+  struct GraphKey {
+    uint64_t n = ~0ull, cap = 0;
+    const void *pool = nullptr, *f0 = nullptr, *f1 = nullptr, *ko = nullptr;
+    double mass_eps = 0;
+    uint32_t pool_cap = 0;
+    bool operator==(const GraphKey& o) const {
+      return n == o.n && cap == o.cap && pool == o.pool && f0 == o.f0 && f1 == o.f1 && ko == o.ko &&
+             mass_eps == o.mass_eps && pool_cap == o.pool_cap;
+    }
+  } fkey[2];
+  uint64_t graph_kernels = 0;  // kernels per graph substep (both sort branches counted once each)
 
   explicit Context(const ckg_config& c) {
     cfg = c;
@@ -229,6 +250,14 @@ struct Context final : CtxBase {
       dfree(mbuf[b]);
       dfree(tbuf[b]);
     }
+    for (auto& e : fexec)
+      if (e) cudaGraphExecDestroy(e);
+    for (auto& c : cst)
+      if (c) cudaStreamDestroy(c);
+    dfree(dframe);
+    dfree(ddt);
+    dfree(dnc);
+    if (hframe) cudaFreeHost(hframe);
     dfree(staging);
     dfree(keys);
     dfree(vals);
@@ -461,14 +490,15 @@ struct Context final : CtxBase {
         uint32_t *sck = nullptr, *sci = nullptr;
         radix_sort_pairs(ck, ci, nc, key_bits, rs, st, &sck, &sci, ci);
         const uint64_t tiles = (n + kMergeTile - 1) / kMergeTile;
-        merge_bounds_kernel<<<grid_for(tiles, 256, 1 << 30), 256, 0, st>>>(keys, chg, n, sck, sci, nc, wcnt);
-        merge_unchanged_kernel<<<unsigned(tiles), kMergeTile, 0, st>>>(keys, chg, cpre, n, sck, sci, nc, wcnt,
-                                                                       perm_buf, skeys_tmp);
+        merge_bounds_kernel<<<grid_for(tiles, 256, 1 << 30), 256, 0, st>>>(keys, chg, n, sck, sci, nc, nullptr,
+                                                                           wcnt);
+        merge_unchanged_kernel<<<unsigned(tiles), kMergeTile, 0, st>>>(keys, chg, cpre, n, sck, sci, nc, nullptr,
+                                                                       wcnt, perm_buf, skeys_tmp);
         // seg_begin/end still hold the previous substep's runs of ko unless
         // the stored order was rebuilt since (slab migration)
         const bool segs = !slab;
         merge_changed_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, st>>>(
-            ko, chg, cpre, n, sck, sci, nc, segs ? seg_begin : nullptr, segs ? seg_end : nullptr, perm_buf,
+            ko, chg, cpre, n, sck, sci, nc, nullptr, segs ? seg_begin : nullptr, segs ? seg_end : nullptr, perm_buf,
             skeys_tmp);
         launches += uint64_t((key_bits + kRadixBits - 1) / kRadixBits) * 5 + 3;
         std::swap(ko, skeys_tmp);
@@ -687,6 +717,310 @@ struct Context final : CtxBase {
     }
     out->status = rc;
     return rc;
+  }
+
+  // ---------------------------------------------------------------- frame driver
+  // cfl_dt (simulation.hpp:134-145) on the host, in T, for the substeps the
+  // graph does not run (first substep after an upload, host-loop fallback).
+  T host_cfl_dt(const FrameState& fs, T remaining) const {
+    T cmax = T(0);
+    for (int mi = 0; mi < cfg.n_materials && mi < kMaxMaterials; ++mi) {
+      const ckg_material& m = cfg.materials[mi];
+      T sp;
+      if (m.model == CKG_MODEL_J_FLUID)
+        sp = std::sqrt(T(m.bulk) * T(m.gamma) * std::pow(T(fs.min_j[mi]), T(1) - T(m.gamma)) / T(m.density));
+      else
+        sp = std::sqrt((T(m.lambda) + T(2) * T(m.mu)) / T(m.density));
+      cmax = std::max(cmax, sp);
+    }
+    const T denom = std::max(T(fs.vmax), cmax);
+    T dt = denom > T(0) ? T(fs.cfl) * T(cfg.dx) / denom : remaining;
+    if (T(fs.max_dt) > T(0)) dt = std::min(dt, T(fs.max_dt));
+    return std::min(dt, remaining);
+  }
+
+  static cudaGraph_t capture_graph_of(cudaStream_t s) {
+    cudaStreamCaptureStatus cs;
+    unsigned long long id;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CKG_CUDA(cudaStreamGetCaptureInfo(s, &cs, &id, &g, &deps, &nd));
+    return g;
+  }
+  // Appends a conditional node after the capture's current tail; the stream
+  // continues after it. Returns the (first) body graph.
+  static cudaGraph_t add_conditional(cudaStream_t s, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
+    cudaStreamCaptureStatus cs;
+    unsigned long long id;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CKG_CUDA(cudaStreamGetCaptureInfo(s, &cs, &id, &g, &deps, &nd));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = type;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    CKG_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
+    CKG_CUDA(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    return p.conditional.phGraph_out[0];
+  }
+
+  // One substep of the frame graph, captured on `s` (conditional sort bodies
+  // on `s_aux`), reading and writing state buffer `cs` -> cs ^ 1.
+  void capture_graph_substep(cudaStream_t s, cudaStream_t s_aux, int cs, cudaGraphConditionalHandle h_loop,
+                             cudaGraphConditionalHandle h_next) {
+    const cudaStream_t saved_st = st;
+    const int saved_cur = cur;
+    st = s;
+    cur = cs;
+    StepConst<T> c = make_const(0.0);
+    c.dtp = ddt;
+    uint64_t k = 0;
+    frame_ctl_kernel<T><<<1, 32, 0, st>>>(dframe, c, ddt);
+    status_reset_kernel<<<1, 32, 0, st>>>(dstat, 1);
+    // sort: crossers counted on the device; <= kSmallSort of them are merged
+    // into the stored order, more take the full radix (IF nodes)
+    key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
+        state(cur), T(cfg.inv_dx), cfg.resolution, D, keys, core, ko, chg, wcnt, dstat);
+    const uint64_t nw = (n + 31) / 32;
+    exclusive_scan(wcnt, cpre, nw, scan_partials_n, st);
+    compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);
+    k += 7;
+    cudaGraph_t g = capture_graph_of(st);
+    cudaGraphConditionalHandle hs, hf;
+    CKG_CUDA(cudaGraphConditionalHandleCreate(&hs, g, 0, cudaGraphCondAssignDefault));
+    CKG_CUDA(cudaGraphConditionalHandleCreate(&hf, g, 0, cudaGraphCondAssignDefault));
+    sort_decide_kernel<<<1, 32, 0, st>>>(cpre, wcnt, nw, dnc, hs, hf);
+    k += 1;
+    {
+      cudaGraph_t body = add_conditional(st, hs, cudaGraphCondTypeIf);
+      CKG_CUDA(cudaStreamBeginCaptureToGraph(s_aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      uint32_t *sck = rs.keys_alt, *sci = rs.vals_alt;
+      small_sort_kernel<<<1, 1024, kSmallSort * sizeof(unsigned long long), s_aux>>>(ck, ci, dnc, sck, sci);
+      const uint64_t tiles = (n + kMergeTile - 1) / kMergeTile;
+      merge_bounds_kernel<<<grid_for(tiles, 256, 1 << 30), 256, 0, s_aux>>>(keys, chg, n, sck, sci, 0u, dnc, wcnt);
+      merge_unchanged_kernel<<<unsigned(tiles), kMergeTile, 0, s_aux>>>(keys, chg, cpre, n, sck, sci, 0u, dnc, wcnt,
+                                                                         perm_buf, skeys_tmp);
+      merge_changed_kernel<<<grid_for(kSmallSort, 256), 256, 0, s_aux>>>(ko, chg, cpre, n, sck, sci, 0u, dnc,
+                                                                         seg_begin, seg_end, perm_buf, skeys_tmp);
+      CKG_CUDA(cudaMemcpyAsync(ko, skeys_tmp, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s_aux));
+      cudaGraph_t done;
+      CKG_CUDA(cudaStreamEndCapture(s_aux, &done));
+      k += 4;
+    }
+    {
+      cudaGraph_t body = add_conditional(st, hf, cudaGraphCondTypeIf);
+      CKG_CUDA(cudaStreamBeginCaptureToGraph(s_aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      uint32_t *sk = nullptr, *sp = nullptr;
+      radix_sort_pairs(keys, vals, n, key_bits, rs, s_aux, &sk, &sp);
+      CKG_CUDA(cudaMemcpyAsync(ko, sk, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s_aux));
+      CKG_CUDA(cudaMemcpyAsync(perm_buf, sp, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s_aux));
+      cudaGraph_t done;
+      CKG_CUDA(cudaStreamEndCapture(s_aux, &done));
+    }
+    perm = perm_buf;
+    skeys = ko;
+    enqueue_activate(0);
+    clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
+    if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, 0);
+    else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_p2g<kSchemeApic>(c, 0);
+    else enqueue_p2g<kSchemeMls>(c, 0);
+    grid_update_kernel<T><<<148 * 8, 256, 0, st>>>(pool, active, dstat, pool_cap, c, dbcs);
+    if (cfg.scheme == CKG_SCHEME_PIC) enqueue_g2p<kSchemePic>(c, 0);
+    else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_g2p<kSchemeApic>(c, 0);
+    else enqueue_g2p<kSchemeMls>(c, 0);
+    frame_end_kernel<T><<<1, 32, 0, st>>>(dframe, dstat, h_loop, h_next, cfg.n_materials);
+    k += 7 + 1 + 3 + 1;
+    graph_kernels = k;
+    CKG_CUDA(cudaGetLastError());
+    st = saved_st;
+    cur = saved_cur;
+  }
+
+  GraphKey graph_key() const {
+    GraphKey k;
+    k.n = n;
+    k.cap = cap;
+    k.pool = pool;
+    k.f0 = fbuf[0];
+    k.f1 = fbuf[1];
+    k.ko = ko;
+    k.mass_eps = cfg.mass_eps;
+    k.pool_cap = pool_cap;
+    return k;
+  }
+
+  // WHILE(h_loop) { substep(c0 -> c0^1); IF(h_next) { substep(c0^1 -> c0) } }
+  void build_frame_graph(int c0) {
+    if (!dframe) {
+      dframe = dalloc<FrameState>(1);
+      ddt = dalloc<T>(1);
+      dnc = dalloc<uint32_t>(1);
+      CKG_CUDA(cudaMallocHost(&hframe, sizeof(FrameState)));
+      for (auto& c : cst) CKG_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+      CKG_CUDA(cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kSmallSort * sizeof(unsigned long long))));
+    }
+    if (fexec[c0]) {
+      CKG_CUDA(cudaGraphExecDestroy(fexec[c0]));
+      fexec[c0] = nullptr;
+    }
+    cudaGraph_t g;
+    CKG_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hw;
+    CKG_CUDA(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = hw;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t wn;
+    CKG_CUDA(cudaGraphAddNode(&wn, g, nullptr, 0, &p));
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    uint32_t* const saved_perm = perm;
+    uint32_t* const saved_skeys = skeys;
+    CKG_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    cudaGraphConditionalHandle hi;
+    CKG_CUDA(cudaGraphConditionalHandleCreate(&hi, capture_graph_of(st), 0, cudaGraphCondAssignDefault));
+    capture_graph_substep(st, cst[0], c0, hw, hi);
+    cudaGraph_t second = add_conditional(st, hi, cudaGraphCondTypeIf);
+    CKG_CUDA(cudaStreamBeginCaptureToGraph(cst[1], second, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    capture_graph_substep(cst[1], cst[2], c0 ^ 1, hw, hw);
+    cudaGraph_t done;
+    CKG_CUDA(cudaStreamEndCapture(cst[1], &done));
+    CKG_CUDA(cudaStreamEndCapture(st, &done));
+    CKG_CUDA(cudaGraphInstantiate(&fexec[c0], g, 0));
+    CKG_CUDA(cudaGraphDestroy(g));
+    perm = saved_perm;
+    skeys = saved_skeys;
+    fkey[c0] = graph_key();
+  }
+
+  // The graph needs: the stored-order keys (incremental sort), a valid stress
+  // cache, a pool that cannot overflow (sized for the whole directory) and a
+  // single domain.
+  bool graph_ready() const { return !slab && n > 0 && ko_valid && stress_valid && pool_cap >= nd; }
+
+  // Host-side bookkeeping of one completed host-loop substep (gather_all + the
+  // loop body of advance_frame).  Returns true when the frame continues.
+  bool host_substep(FrameState& fs, ckg_frame_out* out, int& rc) {
+    const T rem = T(fs.frame_end) - T(fs.time);
+    const T dt = host_cfl_dt(fs, rem);
+    ckg_step_out so;
+    rc = step(double(dt), CKG_PHASE_G2P, 1, &so);
+    out->kernel_launches += so.kernel_launches;
+    out->active_blocks = so.active_blocks;
+    if (rc != CKG_OK) {
+      out->error_code = so.error_code;
+      out->error_axis = so.error_axis;
+      out->error_phase = so.error_phase;
+      out->error_particle = so.error_particle;
+      return false;
+    }
+    fs.vmax = so.vmax;
+    for (int m = 0; m < kMaxMaterials; ++m) fs.min_j[m] = so.min_j[m];
+    fs.time = double(T(fs.time) + dt);
+    fs.dt = double(dt);
+    fs.substeps += 1;
+    if (fs.substeps > fs.max_substeps) {
+      fs.status = 3;
+      return false;
+    }
+    const T r2 = T(fs.frame_end) - T(fs.time);
+    if (r2 <= T(fs.frame_dt) * T(1e-9)) {
+      fs.time = fs.frame_end;
+      fs.status = 1;
+      return false;
+    }
+    return true;
+  }
+
+  int advance_frame(const ckg_frame_in* in, ckg_frame_out* out) override {
+    CKG_CUDA(cudaSetDevice(device));
+    std::memset(out, 0, sizeof(*out));
+    FrameState fs{};
+    const T frame_dt = T(in->frame_dt);
+    fs.frame_dt = double(frame_dt);
+    fs.frame_end = double(frame_dt * T(double(in->frame_index + 1)));
+    fs.time = double(T(in->time));
+    fs.cfl = in->cfl;
+    fs.max_dt = in->max_dt;
+    fs.vmax = in->vmax;
+    for (int m = 0; m < kMaxMaterials; ++m) fs.min_j[m] = in->min_j[m];
+    fs.max_substeps = uint32_t(std::min<uint64_t>(in->max_substeps, 0xfffffff0u));
+    fs.status = 0;
+    int rc = CKG_OK;
+    const uint64_t steps0 = step_count;
+    auto finish = [&](int code) {
+      out->substeps = fs.substeps;
+      out->time = fs.time;
+      out->last_dt = fs.dt;
+      out->vmax = fs.vmax;
+      for (int m = 0; m < kMaxMaterials; ++m) out->min_j[m] = fs.min_j[m];
+      if (fs.status == 3) {
+        last_error = "substep limit exceeded within one frame at t = " + std::to_string(double(T(fs.time)));
+        out->error_code = CKG_NUM_SUBSTEP_LIMIT;
+        code = CKG_ERR_NUMERICAL;
+      }
+      out->status = code;
+      return code;
+    };
+    {
+      const T rem = T(fs.frame_end) - T(fs.time);
+      if (rem <= frame_dt * T(1e-9)) {
+        fs.time = fs.frame_end;
+        fs.status = 1;
+        return finish(CKG_OK);
+      }
+    }
+    // substeps the graph cannot run yet go through the host loop
+    while (!graph_ready()) {
+      if (!host_substep(fs, out, rc)) return finish(rc);
+    }
+    out->graph = 1;
+    const int c0 = cur;
+    if (!fexec[c0] || !(fkey[c0] == graph_key())) build_frame_graph(c0);
+    fs.parity = uint32_t(cur);
+    *hframe = fs;
+    CKG_CUDA(cudaMemcpyAsync(dframe, hframe, sizeof(FrameState), cudaMemcpyHostToDevice, st));
+    CKG_CUDA(cudaEventRecord(tev[14], st));
+    CKG_CUDA(cudaGraphLaunch(fexec[c0], st));
+    CKG_CUDA(cudaEventRecord(tev[15], st));
+    CKG_CUDA(cudaMemcpyAsync(hframe, dframe, sizeof(FrameState), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tev[14], tev[15]);
+    out->device_ms = ms;
+    const uint32_t graph_steps = hframe->substeps - fs.substeps;
+    fs = *hframe;
+    cur = int(fs.parity);
+    step_count = steps0 + fs.substeps;
+    out->kernel_launches += uint64_t(graph_steps + (fs.status == 2 ? 1 : 0)) * graph_kernels;
+    out->active_blocks = hstat->n_active;
+    grid_valid = true;
+    last_active = hstat->n_active;
+    perm = perm_buf;
+    skeys = ko;
+    if (fs.status == 2) {
+      ko_valid = false;  // the failing substep re-sorted; the stored order did not move
+      ckg_step_out so;
+      std::memset(&so, 0, sizeof so);
+      if (hstat->overflow) {
+        last_error = "grid block pool capacity exceeded";
+        return finish(CKG_ERR_DEVICE);
+      }
+      const int code = decode_status(&so, CKG_PHASE_G2P);
+      out->error_code = so.error_code;
+      out->error_axis = so.error_axis;
+      out->error_phase = so.error_phase;
+      out->error_particle = so.error_particle;
+      return finish(code);
+    }
+    return finish(CKG_OK);
   }
 
   int debug_sort(uint32_t* hkeys, uint32_t* horder, uint64_t count) override {
@@ -1079,6 +1413,11 @@ int32_t ckg_step(ckg_ctx* ctx, double dt, ckg_step_out* out) {
 int32_t ckg_step_many(ckg_ctx* ctx, double dt, int32_t count, ckg_step_out* out) {
   if (!ctx || count < 1 || count > 255) return CKG_ERR_CONFIG;
   return guard(ctx, "ckg_step_many", [&] { return ctx->impl->step(dt, CKG_PHASE_G2P, count, out); });
+}
+
+int32_t ckg_advance_frame(ckg_ctx* ctx, const ckg_frame_in* in, ckg_frame_out* out) {
+  if (!ctx || !in || !out || !(in->frame_dt > 0)) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_advance_frame", [&] { return ctx->impl->advance_frame(in, out); });
 }
 
 int32_t ckg_step_phases(ckg_ctx* ctx, double dt, int32_t stop_after, ckg_step_out* out) {

@@ -75,7 +75,9 @@ __global__ void __launch_bounds__(256) merge_bounds_kernel(const uint32_t* __res
                                                            const uint32_t* __restrict__ cbits, uint64_t n,
                                                            const uint32_t* __restrict__ ck,
                                                            const uint32_t* __restrict__ ci, uint32_t nc,
+                                                           const uint32_t* __restrict__ ncp,
                                                            uint32_t* __restrict__ tile_lo) {
+  if (ncp) nc = *ncp;  // device count (graph substeps)
   const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t base = t * kMergeTile;
   if (base >= n) return;
@@ -95,12 +97,14 @@ __global__ void __launch_bounds__(kMergeTile) merge_unchanged_kernel(const uint3
                                                                      const uint32_t* __restrict__ woff, uint64_t n,
                                                                      const uint32_t* __restrict__ ck,
                                                                      const uint32_t* __restrict__ ci, uint32_t nc,
+                                                                     const uint32_t* __restrict__ ncp,
                                                                      const uint32_t* __restrict__ tile_lo,
                                                                      uint32_t* __restrict__ perm,
                                                                      uint32_t* __restrict__ skeys) {
   const uint64_t i = uint64_t(blockIdx.x) * kMergeTile + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if (i >= n) return;
+  if (ncp) nc = *ncp;
   const uint32_t b = __ldg(cbits + (i >> 5));
   if ((b >> lane) & 1u) return;
   const uint32_t k = keys[i];
@@ -126,11 +130,13 @@ __global__ void __launch_bounds__(256) merge_changed_kernel(const uint32_t* __re
                                                             const uint32_t* __restrict__ woff, uint64_t n,
                                                             const uint32_t* __restrict__ ck,
                                                             const uint32_t* __restrict__ ci, uint32_t nc,
+                                                            const uint32_t* __restrict__ ncp,
                                                             const uint32_t* __restrict__ old_begin,
                                                             const uint32_t* __restrict__ old_end,
                                                             uint32_t* __restrict__ perm,
                                                             uint32_t* __restrict__ skeys) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ncp) nc = *ncp;
   if (r >= nc) return;
   const uint32_t k = ck[r], j = ci[r];
   uint64_t lb, ub;

@@ -47,11 +47,17 @@ constexpr int kMaxBoundaries = 32;
 template <typename T>
 struct StepConst {
   T dx, inv_dx, dt, mass_eps, clamp_floor;
+  const T* dtp;  // device-resident dt (frame driver); null: use dt
   T gravity[3];
   int res, D, scheme, n_materials, clamp_singular, n_boundaries;
   int pow2;  // dx is a power of two: x/dx == x*inv_dx exactly (both are exact scalings)
   MatParam<T> mats[kMaxMaterials];
 };
+
+template <typename T>
+__device__ __forceinline__ T step_dt(const StepConst<T>& c) {
+  return c.dtp ? *c.dtp : c.dt;
+}
 
 template <typename T>
 struct BcParam {

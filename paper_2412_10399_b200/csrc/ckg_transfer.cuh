@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const uint32_t lt = lanemask_lt();
   const int D = c.D;
-  const T dx = c.dx, dt = c.dt;
+  const T dx = c.dx, dt = step_dt(c);
   for (;;) {
     __syncthreads();
     if (tid == 0) s_item = item0 + atomicAdd(&st->work[0], 1u);
@@ -445,6 +445,7 @@ __global__ void grid_update_kernel(T* __restrict__ pool, const uint32_t* __restr
   if (g1 > cap) g1 = cap;
   const uint64_t total = g1 > g0 ? uint64_t(g1 - g0) * 128 : 0;
   const int D = c.D;
+  const T dt = step_dt(c);
   for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
        k += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t slot = g0 + uint32_t(k >> 7);
@@ -454,8 +455,8 @@ __global__ void grid_update_kernel(T* __restrict__ pool, const uint32_t* __restr
     const T mass = base[0];
     if (mass > c.mass_eps) {
       const T inv = T(1) / mass;
-      T v[3] = {base[64] * inv + c.gravity[0] * c.dt, base[128] * inv + c.gravity[1] * c.dt,
-                base[192] * inv + c.gravity[2] * c.dt};
+      T v[3] = {base[64] * inv + c.gravity[0] * dt, base[128] * inv + c.gravity[1] * dt,
+                base[192] * inv + c.gravity[2] * dt};
       if (c.n_boundaries > 0) {
         int bx, by, bz;
         decode_key(__ldg(active + slot), D, bx, by, bz);
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const int D = c.D;
-  const T dx = c.dx, dt = c.dt;
+  const T dx = c.dx, dt = step_dt(c);
   T vmax2 = T(0);
   for (;;) {
     __syncthreads();
