@@ -185,6 +185,7 @@ typedef struct ckg_frame_out {
   uint64_t kernel_launches;           /* kernels executed (graph nodes x substeps) */
   int32_t graph;                      /* 1: device-driven graph; 0: host loop (slab mode, growing pool) */
   int32_t _pad;
+  uint64_t sort_paths[3];             /* graph substeps by sort path: one-CTA crosser sort, padded radix, full radix */
 } ckg_frame_out;
 
 /* DiagnosticsRow<T> (simulation.hpp:44-53), computed on the device

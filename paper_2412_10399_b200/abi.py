@@ -112,6 +112,7 @@ class FrameOut(C.Structure):
         ("error_axis", C.c_int32), ("error_phase", C.c_int32),
         ("error_particle", C.c_uint64), ("active_blocks", C.c_uint64),
         ("kernel_launches", C.c_uint64), ("graph", C.c_int32), ("_pad", C.c_int32),
+        ("sort_paths", C.c_uint64 * 3),
     ]
 
 

@@ -790,23 +790,40 @@ struct Context final : CtxBase {
     compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);
     k += 7;
     cudaGraph_t g = capture_graph_of(st);
-    cudaGraphConditionalHandle hs, hf;
+    cudaGraphConditionalHandle hs, hm, hf;
     CKG_CUDA(cudaGraphConditionalHandleCreate(&hs, g, 0, cudaGraphCondAssignDefault));
+    CKG_CUDA(cudaGraphConditionalHandleCreate(&hm, g, 0, cudaGraphCondAssignDefault));
     CKG_CUDA(cudaGraphConditionalHandleCreate(&hf, g, 0, cudaGraphCondAssignDefault));
-    sort_decide_kernel<<<1, 32, 0, st>>>(cpre, wcnt, nw, dnc, hs, hf);
+    const uint32_t bound = uint32_t(std::max<uint64_t>(n / 8, kSmallSort));
+    sort_decide_kernel<<<1, 32, 0, st>>>(cpre, wcnt, nw, bound, dnc, dframe, hs, hm, hf);
     k += 1;
+    const uint64_t tiles = (n + kMergeTile - 1) / kMergeTile;
+    // crossers sorted into (sck, sci): merge them with the stored order
+    auto merge = [&](cudaStream_t s2, uint32_t* sck, uint32_t* sci, uint32_t max_nc) {
+      merge_bounds_kernel<<<grid_for(tiles, 256, 1 << 30), 256, 0, s2>>>(keys, chg, n, sck, sci, 0u, dnc, wcnt);
+      merge_unchanged_kernel<<<unsigned(tiles), kMergeTile, 0, s2>>>(keys, chg, cpre, n, sck, sci, 0u, dnc, wcnt,
+                                                                      perm_buf, skeys_tmp);
+      merge_changed_kernel<<<grid_for(max_nc, 256, 1 << 30), 256, 0, s2>>>(ko, chg, cpre, n, sck, sci, 0u, dnc,
+                                                                           seg_begin, seg_end, perm_buf, skeys_tmp);
+      CKG_CUDA(cudaMemcpyAsync(ko, skeys_tmp, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s2));
+    };
+    {
+      cudaGraph_t body = add_conditional(st, hm, cudaGraphCondTypeIf);
+      CKG_CUDA(cudaStreamBeginCaptureToGraph(s_aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      const uint32_t pad_key = key_bits >= 32 ? 0xffffffffu : uint32_t((1ull << key_bits) - 1);
+      pad_crossers_kernel<<<grid_for(bound, 256), 256, 0, s_aux>>>(ck, ci, dnc, bound, pad_key);
+      uint32_t *sck = nullptr, *sci = nullptr;
+      radix_sort_pairs(ck, ci, bound, key_bits, rs, s_aux, &sck, &sci, ci);
+      merge(s_aux, sck, sci, bound);
+      cudaGraph_t done;
+      CKG_CUDA(cudaStreamEndCapture(s_aux, &done));
+    }
     {
       cudaGraph_t body = add_conditional(st, hs, cudaGraphCondTypeIf);
       CKG_CUDA(cudaStreamBeginCaptureToGraph(s_aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
       uint32_t *sck = rs.keys_alt, *sci = rs.vals_alt;
       small_sort_kernel<<<1, 1024, kSmallSort * sizeof(unsigned long long), s_aux>>>(ck, ci, dnc, sck, sci);
-      const uint64_t tiles = (n + kMergeTile - 1) / kMergeTile;
-      merge_bounds_kernel<<<grid_for(tiles, 256, 1 << 30), 256, 0, s_aux>>>(keys, chg, n, sck, sci, 0u, dnc, wcnt);
-      merge_unchanged_kernel<<<unsigned(tiles), kMergeTile, 0, s_aux>>>(keys, chg, cpre, n, sck, sci, 0u, dnc, wcnt,
-                                                                         perm_buf, skeys_tmp);
-      merge_changed_kernel<<<grid_for(kSmallSort, 256), 256, 0, s_aux>>>(ko, chg, cpre, n, sck, sci, 0u, dnc,
-                                                                         seg_begin, seg_end, perm_buf, skeys_tmp);
-      CKG_CUDA(cudaMemcpyAsync(ko, skeys_tmp, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s_aux));
+      merge(s_aux, sck, sci, kSmallSort);
       cudaGraph_t done;
       CKG_CUDA(cudaStreamEndCapture(s_aux, &done));
       k += 4;
@@ -960,6 +977,7 @@ struct Context final : CtxBase {
       out->last_dt = fs.dt;
       out->vmax = fs.vmax;
       for (int m = 0; m < kMaxMaterials; ++m) out->min_j[m] = fs.min_j[m];
+      for (int k = 0; k < 3; ++k) out->sort_paths[k] = fs.sort_paths[k];
       if (fs.status == 3) {
         last_error = "substep limit exceeded within one frame at t = " + std::to_string(double(T(fs.time)));
         out->error_code = CKG_NUM_SUBSTEP_LIMIT;

@@ -27,6 +27,7 @@ struct FrameState {
   unsigned int substeps, max_substeps;
   unsigned int status;              // 0 running, 1 frame done, 2 device error latched, 3 substep limit
   unsigned int parity;              // state buffer holding the current particles
+  unsigned int sort_paths[3];       // substeps per sort path: one-CTA, padded radix, full radix
 };
 
 template <typename T>
@@ -114,18 +115,37 @@ __global__ void frame_end_kernel(FrameState* fs, const DevStatus* st, cudaGraphC
   cudaGraphSetConditional(h_next, cont);
 }
 
-// Sort path for a graph substep: crossers counted by the warp-count scan;
-// up to kSmallSort of them are ordered by one CTA, more take the full radix.
+// Sort path of a graph substep, from the crosser count of the warp-count
+// scan: up to kSmallSort crossers are ordered by one CTA; up to `bound` (the
+// host path's merge threshold n/8) they are padded to `bound` entries and
+// radix sorted at that fixed size; more take the full radix sort.
 constexpr uint32_t kSmallSort = 8192;
 
 __global__ void sort_decide_kernel(const uint32_t* __restrict__ woff, const uint32_t* __restrict__ wcnt,
-                                   uint64_t nw, uint32_t* __restrict__ nc_out,
-                                   cudaGraphConditionalHandle h_small, cudaGraphConditionalHandle h_full) {
+                                   uint64_t nw, uint32_t bound, uint32_t* __restrict__ nc_out, FrameState* fs,
+                                   cudaGraphConditionalHandle h_small, cudaGraphConditionalHandle h_mid,
+                                   cudaGraphConditionalHandle h_full) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const uint32_t nc = nw ? woff[nw - 1] + wcnt[nw - 1] : 0u;
   *nc_out = nc;
-  cudaGraphSetConditional(h_small, nc <= kSmallSort ? 1u : 0u);
-  cudaGraphSetConditional(h_full, nc <= kSmallSort ? 0u : 1u);
+  const unsigned small = nc <= kSmallSort, mid = !small && nc <= bound;
+  fs->sort_paths[small ? 0 : (mid ? 1 : 2)] += 1;
+  cudaGraphSetConditional(h_small, small);
+  cudaGraphSetConditional(h_mid, mid);
+  cudaGraphSetConditional(h_full, !small && !mid);
+}
+
+// Entries [nc, bound) of the crosser list get the largest key of the sorted
+// bit range (a real key equal to it stays ahead: the sort is stable and the
+// padding indices are larger), so a fixed-size sort leaves the nc real
+// entries first, in order.
+__global__ void pad_crossers_kernel(uint32_t* __restrict__ ck, uint32_t* __restrict__ ci,
+                                    const uint32_t* __restrict__ ncp, uint32_t bound, uint32_t pad_key) {
+  const uint32_t nc = *ncp;
+  for (uint32_t i = nc + blockIdx.x * blockDim.x + threadIdx.x; i < bound; i += gridDim.x * blockDim.x) {
+    ck[i] = pad_key;
+    ci[i] = 0xffffffffu;
+  }
 }
 
 // Stable sort of the compacted crossers (keys ck, indices ci in increasing

@@ -42,6 +42,7 @@ int main(void) {
          sizeof(ckg_step_out), sizeof(ckg_diagnostics), sizeof(ckg_particle_f64), sizeof(ckg_particle_f32));
   printf("%zu %zu %zu\n", offsetof(ckg_config, materials), offsetof(ckg_config, boundaries),
          offsetof(ckg_step_out, status));
+  printf("%zu %zu %zu\n", sizeof(ckg_frame_in), sizeof(ckg_frame_out), offsetof(ckg_frame_out, status));
   return 0;
 }
 '''
@@ -54,7 +55,8 @@ int main(void) {
     got = list(map(int, out))
     want = [C.sizeof(abi.Config), C.sizeof(abi.Material), C.sizeof(abi.Boundary), C.sizeof(abi.StepOut),
             C.sizeof(abi.Diagnostics), abi.particle_dtype(8).itemsize, abi.particle_dtype(4).itemsize,
-            abi.Config.materials.offset, abi.Config.boundaries.offset, abi.StepOut.status.offset]
+            abi.Config.materials.offset, abi.Config.boundaries.offset, abi.StepOut.status.offset,
+            C.sizeof(abi.FrameIn), C.sizeof(abi.FrameOut), abi.FrameOut.status.offset]
     assert got == want
 
 

@@ -67,13 +67,17 @@ def test_frame_device_matches_host_loop_and_reference():
     assert dev.counters().g2p_transfers == host.counters().g2p_transfers
 
 
-def test_frame_full_radix_fallback():
-    """More block crossers per substep than the one-CTA merge sort takes
-    (> 8192): the graph's IF node runs the full radix sort instead."""
-    obj = {"resolution": 128, "scheme": "apic", "gravity": [0, 0, 0], "frame_dt": 1.0 / 120,
+@pytest.mark.parametrize("velocity,path", [((7.5, 0.0, 0.0), 1), ((15.0, 15.0, 15.0), 2)],
+                         ids=["padded_radix", "full_radix"])
+def test_frame_sort_paths(velocity, path):
+    """More block crossers per substep than the one-CTA crosser sort takes
+    (> 8192): up to n/8 of them go through the fixed-size padded radix sort,
+    more through the full radix sort -- the graph's IF nodes pick the path on
+    the device; results match the host loop's incremental / full sort."""
+    obj = {"resolution": 128, "scheme": "apic", "gravity": [0, 0, 0], "frame_dt": 1.0 / 240,
            "materials": [{"model": "fixed_corotated", "density": 1000.0, "E": 1e5, "nu": 0.4}],
-           "bodies": [{"shape": {"kind": "box", "lo": [0.25, 0.375, 0.375], "hi": [0.5, 0.625, 0.5]},
-                       "material": 0, "ppc": 8, "velocity": [15.0, 0.0, 0.0]}],
+           "bodies": [{"shape": {"kind": "box", "lo": [0.25, 0.25, 0.25], "hi": [0.5, 0.5, 0.5]},
+                       "material": 0, "ppc": 8, "velocity": list(velocity)}],
            "boundaries": []}
     cfg = SceneConfig.from_json(obj)
     p = tag_volumes(seed_particles(cfg))
@@ -83,6 +87,7 @@ def test_frame_full_radix_fallback():
     n_host = host.advance_frame(device=False)
     assert n_dev == n_host > 4
     assert dev.time() == host.time()
+    assert dev.last_frame.sort_paths[path] > 0, list(dev.last_frame.sort_paths)
     _compare_states(dev.particles(), host.particles(), 1e-10)
 
 
