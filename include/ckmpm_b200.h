@@ -67,6 +67,9 @@ extern "C" {
 
 /* Phases of Simulation::step (simulation.hpp:150-187), also the stop points
  * of ckg_step_phases. */
+/* ckg_config.flags */
+#define CKG_FLAG_QUADRATIC 1  /* KernelKind::quadratic (transfer.hpp:17): the 27-node B-spline baseline on one grid */
+
 #define CKG_PHASE_SORT 1
 #define CKG_PHASE_ACTIVATE 2
 #define CKG_PHASE_CLEAR 3
@@ -114,7 +117,7 @@ typedef struct ckg_config {
   ckg_material materials[CKG_MAX_MATERIALS];
   ckg_boundary boundaries[CKG_MAX_BOUNDARIES];
   int32_t device;        /* CUDA ordinal */
-  int32_t flags;         /* reserved, 0 */
+  int32_t flags;         /* CKG_FLAG_*; 0 = compact kernel on the dual grids */
 } ckg_config;
 
 /* Particle<T> (transfer.hpp:19-28), byte-identical layout: 224 B (double),

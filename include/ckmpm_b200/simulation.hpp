@@ -82,8 +82,6 @@ class Simulation {
  public:
   explicit Simulation(SimConfig<T> cfg, int device = 0) : cfg_(std::move(cfg)) {
     validate_config(cfg_);  // scene.hpp:184-200
-    if (cfg_.kernel != KernelKind::compact)
-      throw ConfigError("kernel: the B200 backend implements the compact kernel only");
     host_ = seed_particles(cfg_);  // scene.hpp:204-230
     mass_eps_ = compute_mass_epsilon(host_);
     min_j_.assign(cfg_.materials.size(), T(1));
@@ -301,6 +299,7 @@ class Simulation {
         d.center[a] = double(b.center[a]);
       }
     }
+    c.flags = cfg_.kernel == KernelKind::quadratic ? CKG_FLAG_QUADRATIC : 0;
     c.device = device;
     return c;
   }

@@ -130,7 +130,7 @@ SimConfig<T> to_config(const ckg_config& c, const ckref_extra* ex) {
   SimConfig<T> cfg;
   cfg.resolution = c.resolution;
   cfg.extent = T(c.extent);
-  cfg.kernel = KernelKind::compact;
+  cfg.kernel = (c.flags & CKG_FLAG_QUADRATIC) ? KernelKind::quadratic : KernelKind::compact;
   cfg.scheme = static_cast<TransferScheme>(c.scheme);
   cfg.gravity = v3<T>(c.gravity);
   cfg.deterministic = c.deterministic != 0;

@@ -28,6 +28,7 @@ NUM_FLUID_J = 9
 NUM_NONFINITE = 10
 NUM_INACTIVE_BLOCK = 11
 NUM_SUBSTEP_LIMIT = 12
+FLAG_QUADRATIC = 1  # ckg_config.flags: KernelKind::quadratic
 
 MAX_MATERIALS = 16
 MAX_BOUNDARIES = 32

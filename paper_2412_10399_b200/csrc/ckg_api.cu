@@ -22,6 +22,7 @@
 #include "ckg_scan.cuh"
 #include "ckg_slab.cuh"
 #include "ckg_transfer.cuh"
+#include "ckg_quad.cuh"
 
 namespace ckg {
 
@@ -159,6 +160,7 @@ struct Context final : CtxBase {
   uint32_t* seg_begin = nullptr;
   uint32_t* seg_end = nullptr;
   int p2g_ctas = 0, g2p_ctas = 0;
+  int p2gq_ctas = 0, g2pq_ctas = 0;  // quadratic baseline kernels
   int32_t* dir = nullptr;
   uint32_t* active = nullptr;
   uint32_t* scan_partials = nullptr;
@@ -298,35 +300,49 @@ struct Context final : CtxBase {
 
   PState<T> state(int b) const { return PState<T>{fbuf[b], mbuf[b], tbuf[b], n, cap}; }
 
+  // Smallest shared-memory carveout holding two CTAs of a P2G kernel: the
+  // rest of the 256 KB stays L1 for the class-order particle gathers and spills.
+  template <typename K>
+  void set_two_cta_carveout(K* kernel, size_t smem) {
+    cudaFuncAttributes fa{};
+    CKG_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    int smem_sm = 0;
+    CKG_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+    const size_t need = 2 * (smem + fa.sharedSizeBytes + 1024);  // + 1 KB reserved per CTA
+    // supported sm_100 carveouts (KB); the driver rounds the percentage up to
+    // the next one, so ask for floor(target) of the smallest that fits
+    size_t target = size_t(smem_sm);
+    for (int kb : {64, 100, 132, 164, 196, 228})
+      if (size_t(kb) * 1024 >= need) {
+        target = std::min<size_t>(size_t(kb) * 1024, size_t(smem_sm));
+        break;
+      }
+    const int pct = int(std::min<size_t>(100, target * 100 / std::max(smem_sm, 1)));
+    CKG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  }
+
   template <int S>
   void occupancy_for() {
     int nsm = 0, per = 0;
     CKG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
     const size_t smem = p2g_smem_bytes<T>();
     CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    {
-      // smallest shared-memory carveout holding two P2G CTAs: the rest of
-      // the 256 KB stays L1 for the class-order particle gathers and spills
-      cudaFuncAttributes fa{};
-      CKG_CUDA(cudaFuncGetAttributes(&fa, p2g_tile_kernel<T, S>));
-      int smem_sm = 0;
-      CKG_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
-      const size_t need = 2 * (smem + fa.sharedSizeBytes + 1024);  // + 1 KB reserved per CTA
-      // supported sm_100 carveouts (KB); the driver rounds the percentage up
-      // to the next one, so ask for floor(target) of the smallest that fits
-      size_t target = size_t(smem_sm);
-      for (int kb : {64, 100, 132, 164, 196, 228})
-        if (size_t(kb) * 1024 >= need) {
-          target = std::min<size_t>(size_t(kb) * 1024, size_t(smem_sm));
-          break;
-        }
-      const int pct = int(std::min<size_t>(100, target * 100 / std::max(smem_sm, 1)));
-      CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    }
+    set_two_cta_carveout(p2g_tile_kernel<T, S>, smem);
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kXferThreads, smem));
     if (cfg.scheme == S) p2g_ctas = std::max(1, per) * nsm;
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S>, kG2PThreads, 0));
     if (cfg.scheme == S) g2p_ctas = std::max(1, per) * nsm;
+    if constexpr (S != kSchemeMls) {
+      if (quad() && cfg.scheme == S) {
+        const size_t qs = p2g_quad_smem_bytes<T>();
+        CKG_CUDA(cudaFuncSetAttribute(p2g_quad_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qs)));
+        set_two_cta_carveout(p2g_quad_kernel<T, S>, qs);
+        CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_quad_kernel<T, S>, kXferThreads, qs));
+        p2gq_ctas = std::max(1, per) * nsm;
+        CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S, 1>, kG2PThreads, 0));
+        g2pq_ctas = std::max(1, per) * nsm;
+      }
+    }
   }
 
   void setup_persistent() {
@@ -426,8 +442,11 @@ struct Context final : CtxBase {
 
   uint64_t count() const override { return n; }
 
+  int quad() const { return (cfg.flags & CKG_FLAG_QUADRATIC) ? 1 : 0; }
+
   StepConst<T> make_const(double dt) const {
     StepConst<T> c{};
+    c.quad = quad();
     c.dx = T(cfg.dx);
     c.inv_dx = T(cfg.inv_dx);
     c.dt = T(dt);
@@ -468,7 +487,7 @@ struct Context final : CtxBase {
   void enqueue_sort() {
     PState<T> cs = state(cur);
     key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
-        cs, T(cfg.inv_dx), cfg.resolution, D, keys, core, ko_valid ? ko : nullptr, chg, wcnt, dstat);
+        cs, T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko_valid ? ko : nullptr, chg, wcnt, dstat);
     launches += 1;
     if (ko_valid) {
       CKG_CUDA(cudaMemcpyAsync(hcount, &dstat->nchanged, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -536,11 +555,24 @@ struct Context final : CtxBase {
 
   template <int S>
   void enqueue_p2g(const StepConst<T>& c, int step_idx) {
+    if (quad()) {
+      if constexpr (S != kSchemeMls)
+        p2g_quad_kernel<T, S><<<p2gq_ctas, kXferThreads, p2g_quad_smem_bytes<T>(), st>>>(
+            state(cur), perm, c, dir, active, seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
+      return;
+    }
     p2g_tile_kernel<T, S><<<p2g_ctas, kXferThreads, p2g_smem_bytes<T>(), st>>>(
         state(cur), perm, c, dir, active, seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
   }
   template <int S>
   void enqueue_g2p(const StepConst<T>& c, int step_idx) {
+    if (quad()) {
+      if constexpr (S != kSchemeMls)
+        g2p_tile_kernel<T, S, 1><<<g2pq_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir,
+                                                                     active, seg_begin, seg_end, pool, pool_cap,
+                                                                     dstat, step_idx);
+      return;
+    }
     g2p_tile_kernel<T, S><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir, active,
                                                               seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
   }
@@ -784,7 +816,7 @@ struct Context final : CtxBase {
     // sort: crossers counted on the device; <= kSmallSort of them are merged
     // into the stored order, more take the full radix (IF nodes)
     key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
-        state(cur), T(cfg.inv_dx), cfg.resolution, D, keys, core, ko, chg, wcnt, dstat);
+        state(cur), T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko, chg, wcnt, dstat);
     const uint64_t nw = (n + 31) / 32;
     exclusive_scan(wcnt, cpre, nw, scan_partials_n, st);
     compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);
@@ -1350,6 +1382,9 @@ std::string validate(const ckg_config* c) {
     if (model != CKG_MODEL_FIXED_COROTATED && model != CKG_MODEL_J_FLUID && model != CKG_MODEL_DRUCKER_PRAGER)
       return "material: reserved tag and not implemented";
   }
+  if (c->flags & ~CKG_FLAG_QUADRATIC) return "config: unknown flags";
+  if ((c->flags & CKG_FLAG_QUADRATIC) && c->scheme == CKG_SCHEME_MLS)
+    return "scheme: mls requires the compact kernel";  // scene.hpp:193-194
   long long D = c->resolution / 4 + 2;
   if (D * D * D >= (1ll << 31)) return "resolution: too large for the block directory";
   return {};

@@ -22,9 +22,16 @@ namespace ckg {
 // upper node), with s = x*inv_dx exactly as activate computes it
 // (grid.hpp:121-137).  The key cell floor(s + 1/4) is the same rounded sum,
 // so lo, hi are within one block of the key block.
+// Quadratic baseline (grid.hpp:133-136): nodes floor(s - 1/2) .. +2.
 template <typename T>
-__device__ __forceinline__ void axis_footprint(T x, T inv_dx, int& lo, int& hi) {
+__device__ __forceinline__ void axis_footprint(T x, T inv_dx, int quad, int& lo, int& hi) {
   const T s = mul_rn(x, inv_dx);
+  if (quad) {
+    const int base = static_cast<int>(dfloor(sub_rn(s, T(0.5))));
+    lo = base >> 2;
+    hi = (base + 2) >> 2;
+    return;
+  }
   lo = static_cast<int>(dfloor(sub_rn(s, T(0.25)))) >> 2;
   hi = (static_cast<int>(dfloor(add_rn(s, T(0.25)))) + 1) >> 2;
 }
@@ -36,7 +43,7 @@ __device__ __forceinline__ bool inset_ok(T x, T inv_dx, int res) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv_dx, int res, int D,
+__global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv_dx, int res, int D, int quad,
                                                             uint32_t* __restrict__ keys,
                                                             uint32_t* __restrict__ core,
                                                             const uint32_t* __restrict__ ko,
@@ -61,7 +68,7 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
     for (int a = 0; a < 3; ++a) {
       ok = ok && inset_ok(x[a], inv_dx, res);
       int lo, hi;
-      axis_footprint(x[a], inv_dx, lo, hi);
+      axis_footprint(x[a], inv_dx, quad, lo, hi);
       ok = ok && lo >= kb[a] - 1 && hi <= kb[a] + 1;
       ext |= (lo < kb[a] ? 1u : 0u) << (2 * a);
       ext |= (hi > kb[a] ? 1u : 0u) << (2 * a + 1);

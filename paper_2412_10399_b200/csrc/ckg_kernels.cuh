@@ -51,6 +51,7 @@ struct StepConst {
   T gravity[3];
   int res, D, scheme, n_materials, clamp_singular, n_boundaries;
   int pow2;  // dx is a power of two: x/dx == x*inv_dx exactly (both are exact scalings)
+  int quad;  // quadratic B-spline baseline (single grid, slot 0)
   MatParam<T> mats[kMaxMaterials];
 };
 
@@ -417,6 +418,61 @@ __device__ __forceinline__ Dual<T> dual_stencil(T x, T y, T z, T dx, T inv_dx, i
   axis_pair_dual(y, dx, inv_dx, pow2, d.ax[0][1], d.ax[1][1]);
   axis_pair_dual(z, dx, inv_dx, pow2, d.ax[0][2], d.ax[1][2]);
   return d;
+}
+
+// Quadratic B-spline baseline (kernel.hpp:208-241): 3 nodes per axis on the
+// unstaggered grid (grid slot 0, nodes at i*dx).  s = x/dx - 1/2 in the
+// division form the reference uses (exact multiply when dx is a power of two).
+template <typename T>
+struct QAxis {
+  int base;
+  T w[3], g[3];
+  T xi0;  // base*dx - x (node offsets xi_s = xi0 + s*dx)
+};
+
+template <typename T>
+__device__ __forceinline__ QAxis<T> quad_axis(T x, T dx, T inv_dx, int pow2) {
+  QAxis<T> a;
+  const T xd = over_dx(x, dx, inv_dx, pow2);
+  const T fb = dfloor(sub_rn(xd, T(0.5)));
+  a.base = static_cast<int>(fb);
+  const T f = sub_rn(xd, T(a.base));  // [0.5, 1.5)
+  const T t0 = sub_rn(T(1.5), f), t1 = sub_rn(f, T(1)), t2 = sub_rn(f, T(0.5));
+  a.w[0] = mul_rn(mul_rn(T(0.5), t0), t0);
+  a.w[1] = sub_rn(T(0.75), mul_rn(t1, t1));
+  a.w[2] = mul_rn(mul_rn(T(0.5), t2), t2);
+  a.g[0] = div_rn(-t0, dx);
+  a.g[1] = div_rn(mul_rn(T(-2), t1), dx);
+  a.g[2] = div_rn(t2, dx);
+  a.xi0 = sub_rn(mul_rn(T(a.base), dx), x);
+  return a;
+}
+
+// compute_apic_D over the 27-node quadratic stencil (transfer.hpp:101-116),
+// separable: D_aa = M2_a S_b S_c, D_ab = M1_a M1_b S_c.
+template <typename T>
+__device__ __forceinline__ M3<T> apic_D_quad(const QAxis<T> (&q)[3], T dx) {
+  T S[3], M1[3], M2[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    S[a] = M1[a] = M2[a] = T(0);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const T xi = q[a].xi0 + T(k) * dx;
+      S[a] += q[a].w[k];
+      M1[a] += q[a].w[k] * xi;
+      M2[a] += q[a].w[k] * xi * xi;
+    }
+  }
+  M3<T> D;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const int c3 = 3 - a - b;
+      D.a[a][b] = a == b ? M2[a] * S[(a + 1) % 3] * S[(a + 2) % 3] : M1[a] * M1[b] * S[c3];
+    }
+  return D;
 }
 
 // compute_apic_D (transfer.hpp:77-100) in separable form: with per-axis

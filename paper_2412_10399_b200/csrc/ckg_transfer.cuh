@@ -33,6 +33,7 @@ constexpr int kTileN = 6;
 constexpr int kTileNodes = kTileN * kTileN * kTileN;  // 216
 constexpr int kTileVals = 2 * 4 * kTileNodes;         // 1728 (m, px, py, pz on both grids)
 constexpr int kVelVals = 2 * 3 * kTileNodes;          // 1296
+constexpr int kQG = 7, kQGNodes = kQG * kQG * kQG;   // quadratic G2P tile (3 x 343 <= kVelVals)
 constexpr int kXferThreads = 256;
 constexpr int kXferWarps = kXferThreads / 32;
 // G2P CTA shape: small CTAs keep more of them resident per SM when one
@@ -443,13 +444,15 @@ __global__ void grid_update_kernel(T* __restrict__ pool, const uint32_t* __restr
   const uint32_t g0 = st->grid_lo;
   uint32_t g1 = st->grid_hi;
   if (g1 > cap) g1 = cap;
-  const uint64_t total = g1 > g0 ? uint64_t(g1 - g0) * 128 : 0;
+  // both grids (compact kernel) or slot 0 only (quadratic baseline)
+  const int sh = c.quad ? 6 : 7;
+  const uint64_t total = g1 > g0 ? uint64_t(g1 - g0) << sh : 0;
   const int D = c.D;
   const T dt = step_dt(c);
   for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
        k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t slot = g0 + uint32_t(k >> 7);
-    const int g = int(k >> 6) & 1;
+    const uint32_t slot = g0 + uint32_t(k >> sh);
+    const int g = int(k >> 6) & (c.quad ? 0 : 1);
     const int l = int(k & 63);
     T* base = pool + uint64_t(slot) * kBlockVals + g * 256 + l;
     const T mass = base[0];
@@ -460,7 +463,7 @@ __global__ void grid_update_kernel(T* __restrict__ pool, const uint32_t* __restr
       if (c.n_boundaries > 0) {
         int bx, by, bz;
         decode_key(__ldg(active + slot), D, bx, by, bz);
-        const T off = (g == 0 ? T(-0.25) : T(0.25)) * c.dx;
+        const T off = (c.quad ? T(0) : (g == 0 ? T(-0.25) : T(0.25))) * c.dx;  // grid.hpp:194-197, tag 0 / -1 / +1
         const T xp[3] = {T(bx * 4 + ((l >> 4) & 3)) * c.dx + off, T(by * 4 + ((l >> 2) & 3)) * c.dx + off,
                          T(bz * 4 + (l & 3)) * c.dx + off};
         for (int b = 0; b < c.n_boundaries; ++b) {
@@ -538,7 +541,46 @@ __device__ __forceinline__ void gather_grid(const Axis<T>* ax, T dx, VelFn V, T 
   }
 }
 
-template <typename T, int SCHEME>
+// gather_one over the 27-node quadratic stencil (transfer.hpp:512-543),
+// sum-factorised; V(s,t,u,c) yields nodal velocity component c.
+template <typename T, typename VelFn>
+__device__ __forceinline__ void gather_quad(const QAxis<T> (&q)[3], T dx, VelFn V, T (&v)[3], M3<T>& Bm,
+                                            M3<T>& G) {
+#pragma unroll
+  for (int cc = 0; cc < 3; ++cc) {
+    T Y[3], Yg[3], Yz[3], Yx[3], Yzx[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      T Z[3], Zg[3], Zx[3];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const T a0 = V(s, t, 0, cc), a1 = V(s, t, 1, cc), a2 = V(s, t, 2, cc);
+        Z[t] = q[2].w[0] * a0 + q[2].w[1] * a1 + q[2].w[2] * a2;
+        Zg[t] = q[2].g[0] * a0 + q[2].g[1] * a1 + q[2].g[2] * a2;
+        Zx[t] = q[2].w[0] * q[2].xi0 * a0 + q[2].w[1] * (q[2].xi0 + dx) * a1 +
+                q[2].w[2] * (q[2].xi0 + T(2) * dx) * a2;
+      }
+      Y[s] = q[1].w[0] * Z[0] + q[1].w[1] * Z[1] + q[1].w[2] * Z[2];
+      Yg[s] = q[1].g[0] * Z[0] + q[1].g[1] * Z[1] + q[1].g[2] * Z[2];
+      Yz[s] = q[1].w[0] * Zg[0] + q[1].w[1] * Zg[1] + q[1].w[2] * Zg[2];
+      Yx[s] = q[1].w[0] * q[1].xi0 * Z[0] + q[1].w[1] * (q[1].xi0 + dx) * Z[1] +
+              q[1].w[2] * (q[1].xi0 + T(2) * dx) * Z[2];
+      Yzx[s] = q[1].w[0] * Zx[0] + q[1].w[1] * Zx[1] + q[1].w[2] * Zx[2];
+    }
+    v[cc] = q[0].w[0] * Y[0] + q[0].w[1] * Y[1] + q[0].w[2] * Y[2];
+    G.a[cc][0] = q[0].g[0] * Y[0] + q[0].g[1] * Y[1] + q[0].g[2] * Y[2];
+    G.a[cc][1] = q[0].w[0] * Yg[0] + q[0].w[1] * Yg[1] + q[0].w[2] * Yg[2];
+    G.a[cc][2] = q[0].w[0] * Yz[0] + q[0].w[1] * Yz[1] + q[0].w[2] * Yz[2];
+    Bm.a[cc][0] = q[0].w[0] * q[0].xi0 * Y[0] + q[0].w[1] * (q[0].xi0 + dx) * Y[1] +
+                  q[0].w[2] * (q[0].xi0 + T(2) * dx) * Y[2];
+    Bm.a[cc][1] = q[0].w[0] * Yx[0] + q[0].w[1] * Yx[1] + q[0].w[2] * Yx[2];
+    Bm.a[cc][2] = q[0].w[0] * Yzx[0] + q[0].w[1] * Yzx[1] + q[0].w[2] * Yzx[2];
+  }
+}
+
+// KQ = 0: compact kernel on the dual grids; 1: quadratic B-spline baseline
+// on grid slot 0 (the particle update below is shared).
+template <typename T, int SCHEME, int KQ = 0>
 __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
     g2p_tile_kernel(PState<T> cur, PState<T> nxt, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ active,
@@ -575,7 +617,14 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
       for (int r = 0; r < kPer; ++r) {
         const int e = tid + r * kG2PThreads;
         val[r] = T(0);
-        if (e < kVelVals) {
+        if (KQ && e < 3 * kQGNodes) {
+          // quadratic: slot-0 velocities of the 7^3 nodes from 4b - 1
+          const int cc = e / kQGNodes, node = e % kQGNodes;
+          const int gi = 4 * bx - 1 + node / (kQG * kQG), gj = 4 * by - 1 + (node / kQG) % kQG,
+                    gk = 4 * bz - 1 + node % kQG;
+          const int64_t off = nbr_offset(nbr, 0, gi, gj, gk, bx, by, bz);
+          if (off >= 0 && uint64_t(off) < uint64_t(cap) * kBlockVals) val[r] = __ldg(pool + off + (1 + cc) * 64);
+        } else if (!KQ && e < kVelVals) {
           const int g = e / (3 * kTileNodes);
           const int cc = (e / kTileNodes) % 3;
           const int node = e % kTileNodes;
@@ -616,12 +665,37 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
             Bn.a[a][b] = T(0);
             G.a[a][b] = T(0);
           }
+        if (KQ) {
+          // quadratic baseline: 27 nodes of grid slot 0 (transfer.hpp:512-543)
+          const QAxis<T> q[3] = {quad_axis(x, dx, c.inv_dx, c.pow2), quad_axis(y, dx, c.inv_dx, c.pow2),
+                                 quad_axis(z, dx, c.inv_dx, c.pow2)};
+          const int lx = q[0].base - (4 * bx - 1), ly = q[1].base - (4 * by - 1), lz = q[2].base - (4 * bz - 1);
+          if (lx >= 0 && ly >= 0 && lz >= 0 && lx <= kQG - 3 && ly <= kQG - 3 && lz <= kQG - 3) {
+            const T* vg = vt + (lx * kQG + ly) * kQG + lz;
+            gather_quad<T>(
+                q, dx, [&](int s, int t, int u, int cc) { return vg[cc * kQGNodes + (s * kQG + t) * kQG + u]; }, v,
+                Bn, G);
+          } else {
+            gather_quad<T>(
+                q, dx,
+                [&](int s, int t, int u, int cc) {
+                  const int gi = q[0].base + s, gj = q[1].base + t, gk = q[2].base + u;
+                  const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
+                  if (slot < 0 || uint32_t(slot) >= cap) {
+                    record_error(st, step, kPhaseG2P, i, 0, kErrInactive);
+                    return T(0);
+                  }
+                  return __ldg(pool + node_off(slot, 0, gi, gj, gk) + (1 + cc) * 64);
+                },
+                v, Bn, G);
+          }
+        }
 #if CKG_G2P_DUAL
         // both grids' stencils from one sincos per axis (axis_pair_dual)
         const Dual<T> ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
 #endif
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < (KQ ? 0 : 2); ++g) {
 #if CKG_G2P_DUAL
           const Axis<T>* ax = ds.ax[g];
 #else

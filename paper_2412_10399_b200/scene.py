@@ -202,10 +202,8 @@ class SceneConfig:
             raise ConfigError("materials: at least one required")
         if not self.bodies:
             raise ConfigError("bodies: at least one required")
-        if self.kernel != "compact":
-            # The quadratic B-spline baseline is a different discretisation
-            # (SURVEY §8f rank 4); this backend implements the compact kernel.
-            raise ConfigError("kernel: the B200 backend implements the compact kernel only")
+        if self.kernel == "quadratic" and self.scheme == "mls":
+            raise ConfigError("scheme: mls requires the compact kernel")  # scene.hpp:193-194
         for b in self.bodies:
             if b.material >= len(self.materials):
                 raise ConfigError("bodies: material index out of range")
@@ -228,6 +226,8 @@ class SceneConfig:
         c.resolution = int(obj["resolution"])
         c.extent = float(obj.get("extent", 1.0))
         c.kernel = obj.get("kernel", "compact")
+        if c.kernel not in ("compact", "quadratic"):
+            raise ConfigError("config.kernel: expected 'compact' or 'quadratic'")  # io.hpp:255-261
         c.scheme = obj.get("scheme", "apic")
         if c.scheme not in abi.SCHEME_NAMES:
             raise ConfigError("config.scheme: expected 'pic', 'apic' or 'mls'")
@@ -491,6 +491,7 @@ def to_abi_config(cfg: SceneConfig, precision: int = 8, mass_eps: float = 0.0,
             d.lo[a], d.hi[a] = float(T(b.lo[a])), float(T(b.hi[a]))
             d.normal[a] = float(T(b.normal[a]))
             d.velocity[a], d.omega[a], d.center[a] = float(T(b.velocity[a])), float(T(b.omega[a])), float(T(b.center[a]))
+    c.flags = abi.FLAG_QUADRATIC if cfg.kernel == "quadratic" else 0
     c.device = device
     return c
 
