@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cells", type=int, default=108, help="C5 block edge in cells (108 -> 10.08M p)")
     ap.add_argument("--res", type=int, default=512)
     ap.add_argument("--scheme", default="apic")
+    ap.add_argument("--kernel", default="compact", choices=["compact", "quadratic"],
+                    help="quadratic: the 27-node B-spline baseline (paper's comparison)")
     ap.add_argument("--precision", type=int, default=8, choices=[8, 4])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -146,7 +148,7 @@ def cpu_baseline(args, threads):
     Simulation<double>::step on a bounded sample of the same workload family
     (C5 block, same res/material/scheme/dt rule), atomic (default) mode."""
     from oracle import bind
-    cfg = block_scene(args.cpu_cells, resolution=args.res, scheme=args.scheme)
+    cfg = block_scene(args.cpu_cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
     p = seed_particles(cfg, args.precision)
     ref = bind.Ref(cfg, p, precision=args.precision, threads=threads, deterministic=False)
     dt = ref.cfl_dt(1.0)
@@ -173,7 +175,7 @@ def run_reference(args):
         return
     threads = os.cpu_count() or 1
     from oracle import bind
-    cfg = block_scene(args.cpu_cells, resolution=args.res, scheme=args.scheme)
+    cfg = block_scene(args.cpu_cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
     p = seed_particles(cfg, args.precision)
     ref = bind.Ref(cfg, p, precision=args.precision, threads=threads, deterministic=False)
     dt = ref.cfl_dt(1.0)
@@ -216,7 +218,7 @@ def run_slab(args, ws, rank, local):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = lib()
     cells = int(round(args.cells * ws ** (1.0 / 3.0)))
-    cfg = block_scene(cells, resolution=args.res, scheme=args.scheme)
+    cfg = block_scene(cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
     bounds, rk = build_rank_for_box(cfg, ws, rank, args.precision, local)
     tr = DistTransport(dist, rank, ws, torch.device("cuda", local))
     n_local = torch.tensor([rk.n], dtype=torch.int64, device=f"cuda:{local}")
@@ -296,7 +298,7 @@ def main():
 
     L = lib()
     prec = args.precision
-    cfg = block_scene(args.cells, resolution=args.res, scheme=args.scheme)
+    cfg = block_scene(args.cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
     host = seed_particles(cfg, prec)
     n = len(host)
     sim = Simulation(cfg, precision=prec, device=local, particles=host)
@@ -408,7 +410,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if prec == 8 else "f32", "data": "synthetic",
-            "config": {"workload": f"C5_block_{args.cells}", "particles_per_gpu": n, "resolution": args.res,
+            "config": {"workload": f"C5_block_{args.cells}", "particles_per_gpu": n, "resolution": args.res, "kernel": args.kernel,
                        "scheme": args.scheme, "material": "fixed_corotated", "ppc": 8,
                        "active_blocks": nblocks, "dt": dt,
                        "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas (weak)",

@@ -499,7 +499,7 @@ def to_abi_config(cfg: SceneConfig, precision: int = 8, mass_eps: float = 0.0,
 def block_scene(n_cells: int, resolution: int = 512, scheme: str = "apic",
                 model: str = "fixed_corotated", E: float = 1e5, nu: float = 0.4,
                 density: float = 1000.0, gravity=(0.0, -9.8, 0.0), y0: float = 0.0625,
-                boundary: Optional[str] = "sticky") -> SceneConfig:
+                boundary: Optional[str] = "sticky", kernel: str = "compact") -> SceneConfig:
     """SURVEY Appendix C 'C5_block_n' family: FC block of n^3 cells at res 512."""
     h = (n_cells / 2) / resolution
     lo = (0.5 - h, y0, 0.5 - h)
@@ -507,7 +507,7 @@ def block_scene(n_cells: int, resolution: int = 512, scheme: str = "apic",
     mats = [{"model": model, "density": density, "E": E, "nu": nu}]
     if model == "drucker_prager":
         mats[0]["friction_angle_deg"] = 30.0
-    obj = {"name": f"C5_block_{n_cells}", "resolution": resolution, "scheme": scheme,
+    obj = {"name": f"C5_block_{n_cells}", "resolution": resolution, "scheme": scheme, "kernel": kernel,
            "gravity": list(gravity), "materials": mats,
            "bodies": [{"shape": {"kind": "box", "lo": list(lo), "hi": list(hi)}, "material": 0, "ppc": 8}],
            "boundaries": []}
