@@ -27,11 +27,14 @@ clean:
 # C++ drop-in test binary (needs the reference headers; built where they exist,
 # the binary travels to the GPU box).
 REF ?= /root/reference
+# nlohmann/json for the reference's io.hpp (file-format comparison in the io test)
+JSON_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+JSON_INC = $(if $(wildcard $(JSON_DIR)/json.hpp),-I$(JSON_DIR),)
 DROPIN_BIN = tests/cpp/_bin/dropin_test
 dropin: $(PKG)/libckmpm_b200.so
 	@if [ -d $(REF)/proj/include/ckmpm ]; then \
 	  mkdir -p tests/cpp/_bin && g++ -std=gnu++20 -O3 -DNDEBUG -fno-math-errno -pthread \
-	    -I$(REF)/proj/include -Iinclude tests/cpp/dropin_test.cpp -L$(PKG) -lckmpm_b200 \
+	    -I$(REF)/proj/include -Iinclude $(JSON_INC) tests/cpp/dropin_test.cpp -L$(PKG) -lckmpm_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../../../$(PKG)' -o $(DROPIN_BIN) ; \
 	else echo "reference tree absent: keeping prebuilt $(DROPIN_BIN)"; fi
 

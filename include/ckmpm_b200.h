@@ -233,6 +233,24 @@ int32_t ckg_step_many(ckg_ctx* ctx, double dt, int32_t count, ckg_step_out* out)
 /* Simulation::advance_frame() without a callback (simulation.hpp:193-211, :213-215). */
 int32_t ckg_advance_frame(ckg_ctx* ctx, const ckg_frame_in* in, ckg_frame_out* out);
 
+/* Checkpoint / snapshot bodies packed on the device from the current state,
+ * in the exact byte layout of the reference's files (io.hpp:344-430), so a
+ * writer only prepends the header:
+ *   CKG_RECORDS_CHECKPOINT: CKCHKPT1 particle records (write_checkpoint,
+ *     io.hpp:392-430): 27 T fields (x, v, F, B row-major, J, mass, volume0) + u32 material;
+ *   CKG_RECORDS_SNAPSHOT: CKSNAP1 particle records (write_snapshot_binary,
+ *     io.hpp:370-390): x, v, (J if fluid else det F) as 7 doubles + u32 material.
+ * Particles are in the device's current (sorted) order, as the reference's
+ * particles() after the same substeps.  async != 0 returns once the pack is
+ * enqueued; the device-to-host copy runs on its own stream and later substeps
+ * overlap it; ckg_records_wait() blocks until `host` is filled (use pinned
+ * memory for a truly asynchronous copy). */
+#define CKG_RECORDS_CHECKPOINT 0
+#define CKG_RECORDS_SNAPSHOT 1
+uint64_t ckg_record_bytes(const ckg_ctx* ctx, int32_t kind);
+int32_t ckg_pack_records(ckg_ctx* ctx, int32_t kind, void* host, uint64_t bytes, int32_t async);
+int32_t ckg_records_wait(ckg_ctx* ctx);
+
 /* Runs step(dt) only up to and including `stop_after` (CKG_PHASE_*); particle
  * state is not advanced unless stop_after == CKG_PHASE_G2P.  Test/parity hook
  * (the reference exposes the same cut points through full_step's pieces,

@@ -217,6 +217,18 @@ class Simulation {
     ++frame_index_;
   }
 
+  // Device-packed checkpoint / snapshot bodies (ckg_pack_records): the file
+  // body of the reference's CKCHKPT1 / CKSNAP1 writers, one record per
+  // particle in the current order (include/ckmpm_b200/io.hpp writes the files).
+  std::size_t record_bytes(int kind) const { return std::size_t(ckg_record_bytes(ctx_, kind)); }
+  void pack_records(int kind, void* buf, std::size_t bytes, bool async = false) const {
+    if (host_dirty_) const_cast<Simulation*>(this)->upload();
+    const int32_t rc = ckg_pack_records(ctx_, kind, buf, bytes, async ? 1 : 0);
+    if (rc != CKG_OK) const_cast<Simulation*>(this)->throw_for(rc, ckg_step_out{});
+  }
+  void records_wait() const { ckg_records_wait(ctx_); }
+  std::size_t particle_count() const { return host_.size(); }
+
   // B200 extension: the same row reduced on the device (no particle download;
   // summation order differs from the serial host loop at round-off).
   DiagnosticsRow<T> device_diagnostics() const {

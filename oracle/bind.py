@@ -65,6 +65,10 @@ def ref_lib():
         l.ckref_sim_active_blocks.restype = C.c_uint64
         l.ckref_sim_grid.argtypes = [vp, vp, vp, C.c_uint64]
         l.ckref_sim_diagnostics.argtypes = [vp, P(abi.Diagnostics)]
+        l.ckref_sim_write_checkpoint.argtypes = [vp, C.c_char_p]
+        l.ckref_sim_write_checkpoint.restype = C.c_int32
+        l.ckref_sim_write_snapshot.argtypes = [vp, C.c_char_p, C.c_int32, C.c_int32]
+        l.ckref_sim_write_snapshot.restype = C.c_int32
         l.ckref_sim_mass_epsilon.argtypes = [vp]
         l.ckref_sim_mass_epsilon.restype = C.c_double
         l.ckref_p2g.argtypes = [P(abi.Config), vp, C.c_uint64, C.c_double, vp, vp, C.c_uint64, C.c_char_p, C.c_int32]
@@ -192,6 +196,12 @@ class Ref:
         d = abi.Diagnostics()
         ref_lib().ckref_sim_diagnostics(self.h, C.byref(d))
         return d
+
+    def write_checkpoint(self, path):
+        return ref_lib().ckref_sim_write_checkpoint(self.h, str(path).encode())
+
+    def write_snapshot(self, path, frame, binary=True):
+        return ref_lib().ckref_sim_write_snapshot(self.h, str(path).encode(), int(frame), int(binary))
 
     def close(self):
         if self.h:

@@ -61,6 +61,10 @@ void ckref_sim_timers(void* sim, double* out6);
 uint64_t ckref_sim_active_blocks(void* sim);
 /* Blocks in the reference's own (first-touch) order. nodes: nb*128*4. */
 int32_t ckref_sim_grid(void* sim, int32_t* coords, double* nodes, uint64_t nb);
+/* The reference's write_checkpoint / write_snapshot_{binary,text} (io.hpp:344-430)
+ * on the current state; 0 ok, 4 io error, 5 shim built without io.hpp. */
+int32_t ckref_sim_write_checkpoint(void* sim, const char* path);
+int32_t ckref_sim_write_snapshot(void* sim, const char* path, int32_t frame, int32_t binary);
 void ckref_sim_diagnostics(void* sim, ckg_diagnostics* out);
 double ckref_sim_mass_epsilon(void* sim);
 

@@ -47,6 +47,10 @@
 #include "ckmpm/simulation.hpp"
 #include "ckmpm/transfer.hpp"
 #undef private
+#if __has_include(<json.hpp>)
+#include "ckmpm/io.hpp"  // writers only (public API); needs nlohmann/json on the include path
+#define CKREF_HAVE_IO 1
+#endif
 
 #include "ckref.h"
 
@@ -500,3 +504,52 @@ void ckref_force_matrix(const ckg_particle_f64* p, const ckg_material* m, double
 }
 
 }  // extern "C"
+
+// The reference's own checkpoint / snapshot writers (io.hpp:344-430), for the
+// byte-exact comparison of the device-packed files.  5 = built without io.hpp.
+extern "C" int32_t ckref_sim_write_checkpoint(void* s, const char* path) {
+#ifdef CKREF_HAVE_IO
+  try {
+    if (static_cast<SimBase*>(s)->precision == 4)
+      write_checkpoint(path, *as<float>(s)->sim);
+    else
+      write_checkpoint(path, *as<double>(s)->sim);
+  } catch (const std::exception&) {
+    return 4;
+  }
+  return 0;
+#else
+  (void)s;
+  (void)path;
+  return 5;
+#endif
+}
+
+extern "C" int32_t ckref_sim_write_snapshot(void* s, const char* path, int32_t frame, int32_t binary) {
+#ifdef CKREF_HAVE_IO
+  auto run = [&](auto& sim) {
+    using T = std::decay_t<decltype(sim.time())>;
+    std::span<const Particle<T>> ps = sim.particles();
+    std::span<const Material<T>> mats(sim.config().materials);
+    if (binary)
+      write_snapshot_binary<T>(path, ps, mats, frame, sim.time(), sim.config().dx());
+    else
+      write_snapshot_text<T>(path, ps, mats, frame, sim.time(), sim.config().dx());
+  };
+  try {
+    if (static_cast<SimBase*>(s)->precision == 4)
+      run(*as<float>(s)->sim);
+    else
+      run(*as<double>(s)->sim);
+  } catch (const std::exception&) {
+    return 4;
+  }
+  return 0;
+#else
+  (void)s;
+  (void)path;
+  (void)frame;
+  (void)binary;
+  return 5;
+#endif
+}

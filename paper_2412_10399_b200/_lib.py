@@ -46,6 +46,12 @@ def _declare(lib: C.CDLL) -> None:
     lib.ckg_step.restype = i32
     lib.ckg_step_many.argtypes = [vp, C.c_double, i32, P(abi.StepOut)]
     lib.ckg_step_many.restype = i32
+    lib.ckg_record_bytes.argtypes = [vp, i32]
+    lib.ckg_record_bytes.restype = u64
+    lib.ckg_pack_records.argtypes = [vp, i32, vp, u64, i32]
+    lib.ckg_pack_records.restype = i32
+    lib.ckg_records_wait.argtypes = [vp]
+    lib.ckg_records_wait.restype = i32
     lib.ckg_advance_frame.argtypes = [vp, P(abi.FrameIn), P(abi.FrameOut)]
     lib.ckg_advance_frame.restype = i32
     lib.ckg_step_phases.argtypes = [vp, C.c_double, i32, P(abi.StepOut)]
@@ -90,7 +96,8 @@ def _declare(lib: C.CDLL) -> None:
 EXPORTED = (
     "ckg_abi_version", "ckg_build_info", "ckg_status_string", "ckg_create", "ckg_destroy",
     "ckg_upload", "ckg_download", "ckg_particle_count", "ckg_set_mass_epsilon", "ckg_step",
-    "ckg_step_many", "ckg_step_phases", "ckg_advance_frame", "ckg_debug_sort", "ckg_debug_bases",
+    "ckg_step_many", "ckg_step_phases", "ckg_advance_frame", "ckg_record_bytes", "ckg_pack_records",
+    "ckg_records_wait", "ckg_debug_sort", "ckg_debug_bases",
     "ckg_grid_active_block_count", "ckg_grid_download", "ckg_grid_totals",
     "ckg_diagnostics_compute", "ckg_timer_mark", "ckg_timer_elapsed", "ckg_last_error_message",
     "ckg_slab_set", "ckg_slab_bin", "ckg_slab_p2g", "ckg_slab_halo", "ckg_slab_grid", "ckg_slab_g2p",

@@ -29,6 +29,8 @@ NUM_NONFINITE = 10
 NUM_INACTIVE_BLOCK = 11
 NUM_SUBSTEP_LIMIT = 12
 FLAG_QUADRATIC = 1  # ckg_config.flags: KernelKind::quadratic
+RECORDS_CHECKPOINT = 0
+RECORDS_SNAPSHOT = 1
 
 MAX_MATERIALS = 16
 MAX_BOUNDARIES = 32

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import abi
 from ._lib import lib
-from .scene import (ConfigError, DeviceError, InvertedElementError, NumericalError,
+from .scene import (ConfigError, DeviceError, InvertedElementError, IoError, NumericalError,
                     OutOfDomainError, SceneConfig, mass_epsilon, seed_particles, to_abi_config)
 
 _INVERTED = {abi.NUM_FC_STRESS_INVERTED, abi.NUM_DP_STRESS_INVERTED, abi.NUM_RETURN_MAP_INVERTED,
@@ -377,6 +377,70 @@ class Simulation:
         _raise_for(self._ctx, lib().ckg_diagnostics_compute(self._ctx, C.byref(d)))
         return DiagnosticsRow(self._step_count, self._time, np.array(d.momentum[:]), np.array(d.angular[:]),
                               np.array(d.momentum_massfree[:]), float(d.kinetic_energy), float(d.vmax))
+
+    # -- checkpoint / snapshot (io.hpp:344-477) ---------------------------
+    def _records(self, kind: int) -> np.ndarray:
+        """Device-packed file body (ckg_pack_records), one record per particle."""
+        nb = int(lib().ckg_record_bytes(self._ctx, kind))
+        buf = np.empty(self._n * nb, dtype=np.uint8)
+        _raise_for(self._ctx, lib().ckg_pack_records(self._ctx, kind, abi.ptr(buf), buf.nbytes, 0))
+        return buf
+
+    def write_checkpoint(self, path: str):
+        """write_checkpoint (io.hpp:392-430), CKCHKPT1, byte-identical layout."""
+        import struct
+        T = self._T
+        head = b"CKCHKPT1" + struct.pack("<IQi", np.dtype(T).itemsize, self._step_count, self._frame_index)
+        head += np.array([self._time, self._mass_eps], dtype=T).tobytes() + struct.pack("<Q", self._n)
+        with open(path, "wb") as f:
+            f.write(head)
+            f.write(self._records(abi.RECORDS_CHECKPOINT).tobytes())
+
+    def read_checkpoint(self, path: str):
+        """read_checkpoint (io.hpp:432-477) into this simulation (restore)."""
+        import struct
+        T = self._T
+        ts = np.dtype(T).itemsize
+        data = open(path, "rb").read()
+        if data[:8] != b"CKCHKPT1":
+            raise IoError(f"not a checkpoint file: {path}")
+        (scalar,) = struct.unpack_from("<I", data, 8)
+        if scalar != ts:
+            raise IoError(f"checkpoint scalar width mismatch in {path}")
+        step, frame = struct.unpack_from("<Qi", data, 12)
+        time, eps = np.frombuffer(data, dtype=T, count=2, offset=24)
+        (count,) = struct.unpack_from("<Q", data, 24 + 2 * ts)
+        rec = np.dtype([("f", T, 27), ("mat", "<u4")])
+        off = 32 + 2 * ts
+        if len(data) < off + count * rec.itemsize:
+            raise IoError(f"truncated checkpoint particle data: {path}")
+        r = np.frombuffer(data, dtype=rec, count=count, offset=off)
+        p = np.zeros(count, dtype=abi.particle_dtype(self.precision))
+        p["x"], p["v"] = r["f"][:, 0:3], r["f"][:, 3:6]
+        p["F"], p["B"] = r["f"][:, 6:15].reshape(-1, 3, 3), r["f"][:, 15:24].reshape(-1, 3, 3)
+        p["J"], p["mass"], p["volume0"] = r["f"][:, 24], r["f"][:, 25], r["f"][:, 26]
+        p["material"] = r["mat"]
+        self.restore(p, float(time), int(step), int(frame), float(eps))
+
+    def write_snapshot(self, path: str, frame: int, binary: bool = True):
+        """write_snapshot_binary / _text (io.hpp:344-390): x, v, J (fluids) or
+        det F, material; same bytes as the reference's writers."""
+        import struct
+        body = self._records(abi.RECORDS_SNAPSHOT)
+        dx = float(self.cfg.dx(self.precision))
+        t = float(self._T(self._time))
+        if binary:
+            with open(path, "wb") as f:
+                f.write(b"CKSNAP1\0" + struct.pack("<qdqd", frame, t, self._n, dx))
+                f.write(body.tobytes())
+            return
+        r = np.frombuffer(body, dtype=np.dtype([("c", "<f8", 7), ("mat", "<u4")]))
+        lines = ["# ckmpm-snapshot-v1\n", f"frame {frame}\n", "time %.17g\n" % t, f"count {self._n}\n",
+                 "dx %.17g\n" % dx, "# x y z vx vy vz J_or_detF material_id\n"]
+        for c, m in zip(r["c"].tolist(), r["mat"].tolist()):
+            lines.append("".join("%.17g " % v for v in c) + f"{m}\n")
+        with open(path, "w") as f:
+            f.write("".join(lines))
 
     # -- binning parity hooks -------------------------------------------
     def debug_sort(self):

@@ -17,6 +17,7 @@
 #include "../../include/ckmpm_b200.h"
 #include "ckg_bin.cuh"
 #include "ckg_frame.cuh"
+#include "ckg_io.cuh"
 #include "ckg_isort.cuh"
 #include "ckg_kernels.cuh"
 #include "ckg_scan.cuh"
@@ -92,6 +93,9 @@ struct CtxBase {
   virtual uint64_t count() const = 0;
   virtual int step(double dt, int stop_after, int count, ckg_step_out* out) = 0;
   virtual int advance_frame(const ckg_frame_in* in, ckg_frame_out* out) = 0;
+  virtual uint64_t record_bytes(int kind) const = 0;
+  virtual int pack_records(int kind, void* host, uint64_t bytes, int async) = 0;
+  virtual int records_wait() = 0;
   virtual int debug_sort(uint32_t* keys, uint32_t* order, uint64_t n) = 0;
   virtual int debug_bases(int32_t* bases, uint64_t n) = 0;
   virtual uint64_t active_blocks() = 0;
@@ -193,6 +197,13 @@ struct Context final : CtxBase {
     }
   } fkey[2];
   uint64_t graph_kernels = 0;  // kernels per graph substep (both sort branches counted once each)
+  // checkpoint / snapshot records (ckg_io.cuh): packed on the context stream,
+  // copied to the host on their own stream so later substeps overlap the D2H
+  uint32_t* iobuf = nullptr;
+  uint64_t iobuf_words = 0;
+  cudaStream_t iost = nullptr;
+  cudaEvent_t io_packed = nullptr, io_done = nullptr;
+  bool io_pending = false;
 
   explicit Context(const ckg_config& c) {
     cfg = c;
@@ -252,6 +263,11 @@ struct Context final : CtxBase {
       dfree(mbuf[b]);
       dfree(tbuf[b]);
     }
+    if (iost) cudaStreamSynchronize(iost);
+    dfree(iobuf);
+    if (io_packed) cudaEventDestroy(io_packed);
+    if (io_done) cudaEventDestroy(io_done);
+    if (iost) cudaStreamDestroy(iost);
     for (auto& e : fexec)
       if (e) cudaGraphExecDestroy(e);
     for (auto& c : cst)
@@ -1073,6 +1089,58 @@ struct Context final : CtxBase {
     return finish(CKG_OK);
   }
 
+  // ---------------------------------------------------------------- checkpoint / snapshot
+  uint64_t record_bytes(int kind) const override {
+    return kind == CKG_RECORDS_CHECKPOINT ? uint64_t(checkpoint_words<T>()) * 4 : uint64_t(kSnapshotWords) * 4;
+  }
+
+  int pack_records(int kind, void* host, uint64_t bytes, int async) override {
+    if (kind != CKG_RECORDS_CHECKPOINT && kind != CKG_RECORDS_SNAPSHOT) {
+      last_error = "records: unknown kind";
+      return CKG_ERR_CONFIG;
+    }
+    const uint64_t need = n * record_bytes(kind);
+    if (bytes < need) {
+      last_error = "records: host buffer too small";
+      return CKG_ERR_CONFIG;
+    }
+    if (n == 0) return CKG_OK;
+    CKG_CUDA(cudaSetDevice(device));
+    if (!iost) {
+      CKG_CUDA(cudaStreamCreateWithFlags(&iost, cudaStreamNonBlocking));
+      CKG_CUDA(cudaEventCreateWithFlags(&io_packed, cudaEventDisableTiming));
+      CKG_CUDA(cudaEventCreateWithFlags(&io_done, cudaEventDisableTiming));
+    }
+    if (io_pending) CKG_CUDA(cudaStreamWaitEvent(st, io_done, 0));  // the previous copy still reads iobuf
+    const uint64_t words = need / 4;
+    if (words > iobuf_words) {
+      CKG_CUDA(cudaStreamSynchronize(st));
+      dfree(iobuf);
+      iobuf = dalloc<uint32_t>(words);
+      iobuf_words = words;
+    }
+    uint32_t fluid = 0;
+    for (int m = 0; m < cfg.n_materials && m < 32; ++m)
+      if (cfg.materials[m].model == CKG_MODEL_J_FLUID) fluid |= 1u << m;
+    pack_records_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), kind, fluid, iobuf);
+    CKG_CUDA(cudaGetLastError());
+    CKG_CUDA(cudaEventRecord(io_packed, st));
+    CKG_CUDA(cudaStreamWaitEvent(iost, io_packed, 0));
+    CKG_CUDA(cudaMemcpyAsync(host, iobuf, need, cudaMemcpyDeviceToHost, iost));
+    CKG_CUDA(cudaEventRecord(io_done, iost));
+    io_pending = true;
+    if (!async) return records_wait();
+    return CKG_OK;
+  }
+
+  int records_wait() override {
+    if (io_pending) {
+      CKG_CUDA(cudaEventSynchronize(io_done));
+      io_pending = false;
+    }
+    return CKG_OK;
+  }
+
   int debug_sort(uint32_t* hkeys, uint32_t* horder, uint64_t count) override {
     if (count != n) return CKG_ERR_CONFIG;
     if (n == 0) return CKG_OK;
@@ -1471,6 +1539,18 @@ int32_t ckg_step_many(ckg_ctx* ctx, double dt, int32_t count, ckg_step_out* out)
 int32_t ckg_advance_frame(ckg_ctx* ctx, const ckg_frame_in* in, ckg_frame_out* out) {
   if (!ctx || !in || !out || !(in->frame_dt > 0)) return CKG_ERR_CONFIG;
   return guard(ctx, "ckg_advance_frame", [&] { return ctx->impl->advance_frame(in, out); });
+}
+
+uint64_t ckg_record_bytes(const ckg_ctx* ctx, int32_t kind) { return ctx ? ctx->impl->record_bytes(kind) : 0; }
+
+int32_t ckg_pack_records(ckg_ctx* ctx, int32_t kind, void* host, uint64_t bytes, int32_t async) {
+  if (!ctx || !host) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_pack_records", [&] { return ctx->impl->pack_records(kind, host, bytes, async); });
+}
+
+int32_t ckg_records_wait(ckg_ctx* ctx) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_records_wait", [&] { return ctx->impl->records_wait(); });
 }
 
 int32_t ckg_step_phases(ckg_ctx* ctx, double dt, int32_t stop_after, ckg_step_out* out) {

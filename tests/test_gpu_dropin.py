@@ -44,3 +44,13 @@ def test_acceptance_3_two_spheres_momentum():
 
 def test_acceptance_10_stress_scenes_mass():
     run("stress")
+
+
+def test_dropin_checkpoint_snapshot_files():
+    """CKCHKPT1 / CKSNAP1 / text snapshot bytes equal to the reference's own
+    writers on the same state; restart via read_checkpoint continues like the
+    uninterrupted run."""
+    d = run("io")
+    assert d["checkpoint_bytes_equal"] and d["snapshot_binary_equal"] and d["snapshot_text_equal"]
+    assert d["restart_roundtrip"]
+
