@@ -152,7 +152,7 @@ typedef struct ckg_step_out {
   uint64_t kernel_launches;           /* device kernels this call enqueued */
   uint64_t sort_changed;              /* particles whose block key changed since the last sort */
   int32_t sort_kind;                  /* 0 full radix, 1 identity, 2 incremental merge */
-  int32_t _pad2;
+  int32_t slab_migration;             /* slab substeps: 1 boundary-plane compaction, 2 full relayout */
 } ckg_step_out;
 
 /* advance_frame (simulation.hpp:193-211) on the device: the host passes the

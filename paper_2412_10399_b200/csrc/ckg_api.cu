@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -132,6 +133,7 @@ struct Context final : CtxBase {
   bool stress_valid = false;
   int cur = 0;
   uint64_t cap = 0;  // particle buffer capacity (field stride)
+  uint64_t wb[2] = {0, 0};  // window base of each state buffer (slab mode: room to prepend migrants)
   // x-slab decomposition (ckg_slab.cuh)
   bool slab = false;
   int srank = 0, sworld = 1, bx_lo = 0, bx_hi = 0;
@@ -139,6 +141,12 @@ struct Context final : CtxBase {
   uint32_t *fl_stay = nullptr, *fl_left = nullptr, *fl_right = nullptr;
   uint32_t *pos_stay = nullptr, *pos_left = nullptr, *pos_right = nullptr;
   uint64_t mig_left = 0, mig_right = 0, n_stay = 0;
+  // region path of the migration (ckg_slab.cuh): sorted prefix [0, PL) and
+  // suffix [PR, n) hold every possible crosser; mig_region = false falls back
+  // to relaying out the whole slab
+  bool mig_region = false;
+  uint64_t reg_pl = 0, reg_pr = 0, stay_l = 0, stay_r = 0;
+  unsigned long long* dreg = nullptr;  // PL, PR, far count
   double slab_dt = 0;
   // staging for AoS transfers
   T* staging = nullptr;
@@ -285,6 +293,7 @@ struct Context final : CtxBase {
     dfree(rs.partials);
     for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount, &wcnt}) dfree(*b);
     for (uint32_t** b : {&plane_start, &fl_stay, &fl_left, &fl_right, &pos_stay, &pos_left, &pos_right}) dfree(*b);
+    dfree(dreg);
     if (hcount) cudaFreeHost(hcount);
     dfree(flags);
     dfree(core);
@@ -314,7 +323,10 @@ struct Context final : CtxBase {
     active = dalloc<uint32_t>(cap);
   }
 
-  PState<T> state(int b) const { return PState<T>{fbuf[b], mbuf[b], tbuf[b], n, cap}; }
+  PState<T> state(int b) const { return PState<T>{fbuf[b] + wb[b], mbuf[b] + wb[b], tbuf[b] + wb[b], n, cap}; }
+  PState<T> state_at(int b, uint64_t base, uint64_t count) const {
+    return PState<T>{fbuf[b] + base, mbuf[b] + base, tbuf[b] + base, count, cap};
+  }
 
   // Smallest shared-memory carveout holding two CTAs of a P2G kernel: the
   // rest of the 256 KB stays L1 for the class-order particle gathers and spills.
@@ -372,6 +384,7 @@ struct Context final : CtxBase {
     const uint64_t want = slab ? count + std::max<uint64_t>(count / 2, 1u << 20) : count;
     if (fbuf[0] && want <= cap && (slab || count == cap)) {
       n = count;
+      wb[0] = wb[1] = slab ? (cap - count) / 2 : 0;
       return;
     }
     for (int b = 0; b < 2; ++b) {
@@ -388,6 +401,7 @@ struct Context final : CtxBase {
     for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp, &ncount, &wcnt}) dfree(*b);
     n = count;
     cap = std::max<uint64_t>(want, 1);
+    wb[0] = wb[1] = slab ? (cap - count) / 2 : 0;
     for (int b = 0; b < 2; ++b) {
       fbuf[b] = dalloc<T>(uint64_t(kNumFields) * cap);
       mbuf[b] = dalloc<uint32_t>(cap);
@@ -1211,9 +1225,13 @@ struct Context final : CtxBase {
   // ---------------------------------------------------------------- slabs
   // Staged substep for the x-slab decomposition; the host moves the
   // exchange buffers between stages (paper_2412_10399_b200/slab.py).
+  bool force_full_relayout = false;  // CKMPM_SLAB_FULL_RELAYOUT=1: always take the full migration path (tests)
+
   int slab_set(int rank, int world, int lo, int hi) override {
     if (lo < 0 || hi > D || lo >= hi || rank < 0 || rank >= world) return CKG_ERR_CONFIG;
     slab = true;
+    const char* env = std::getenv("CKMPM_SLAB_FULL_RELAYOUT");
+    force_full_relayout = env && env[0] == '1';
     srank = rank;
     sworld = world;
     bx_lo = lo;
@@ -1292,6 +1310,7 @@ struct Context final : CtxBase {
   int slab_g2p(uint64_t* counts) override {
     CKG_CUDA(cudaSetDevice(device));
     const StepConst<T> c = make_const(slab_dt);
+    wb[cur ^ 1] = wb[cur];  // G2P writes the new state at the same window
     if (cfg.scheme == CKG_SCHEME_PIC) enqueue_g2p<kSchemePic>(c, 0);
     else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_g2p<kSchemeApic>(c, 0);
     else enqueue_g2p<kSchemeMls>(c, 0);
@@ -1299,10 +1318,66 @@ struct Context final : CtxBase {
     PState<T> nx = state(cur ^ 1);
     classify_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(nx, T(cfg.inv_dx), D, bx_lo, bx_hi, fl_stay,
                                                                    fl_left, fl_right);
+    launches += 2;
+    // crossers can only come from the first and last owned plane: find the
+    // sorted regions of those planes and check the middle holds none
+    if (!dreg) dreg = dalloc<unsigned long long>(3);
+    CKG_CUDA(cudaMemsetAsync(dreg, 0, 3 * sizeof(unsigned long long), st));
+    const uint64_t DD = uint64_t(D) * D;
+    slab_regions_kernel<<<1, 1, 0, st>>>(skeys, n, uint32_t((bx_lo + 1) * DD), uint32_t((bx_hi - 1) * DD), dreg);
+    unsigned long long hreg[3] = {0, 0, 0};
+    CKG_CUDA(cudaMemcpyAsync(hreg, dreg, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    reg_pl = hreg[0];
+    reg_pr = hreg[1];
+    mig_region = !force_full_relayout && bx_hi - bx_lo >= 2 && reg_pl <= reg_pr;
+    if (mig_region) {
+      // no crosser in the middle, none leaving the "wrong" side of a region
+      if (reg_pr > reg_pl)
+        count_far_kernel<<<grid_for(reg_pr - reg_pl, 256, 148 * 8), 256, 0, st>>>(fl_left, fl_right, reg_pl, reg_pr,
+                                                                                dreg + 2);
+      if (reg_pl)
+        count_far_kernel<<<grid_for(reg_pl, 256, 148 * 8), 256, 0, st>>>(fl_right, fl_right, 0, reg_pl, dreg + 2);
+      if (n > reg_pr)
+        count_far_kernel<<<grid_for(n - reg_pr, 256, 148 * 8), 256, 0, st>>>(fl_left, fl_left, reg_pr, n, dreg + 2);
+      // region-local scans (left: [0, PL), right: [PR, n))
+      const uint64_t nr = n - reg_pr;
+      if (reg_pl) {
+        exclusive_scan(fl_left, pos_left, reg_pl, scan_partials_n, st);
+        exclusive_scan(fl_stay, pos_stay, reg_pl, scan_partials_n, st);
+      }
+      if (nr) {
+        exclusive_scan(fl_right + reg_pr, pos_right, nr, scan_partials_n, st);
+        exclusive_scan(fl_stay + reg_pr, pos_stay + reg_pl, nr, scan_partials_n, st);
+      }
+      launches += 13;
+      uint32_t tail[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (reg_pl) {
+        CKG_CUDA(cudaMemcpyAsync(&tail[0], pos_left + reg_pl - 1, 4, cudaMemcpyDeviceToHost, st));
+        CKG_CUDA(cudaMemcpyAsync(&tail[1], fl_left + reg_pl - 1, 4, cudaMemcpyDeviceToHost, st));
+      }
+      if (nr) {
+        CKG_CUDA(cudaMemcpyAsync(&tail[2], pos_right + nr - 1, 4, cudaMemcpyDeviceToHost, st));
+        CKG_CUDA(cudaMemcpyAsync(&tail[3], fl_right + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      }
+      CKG_CUDA(cudaMemcpyAsync(&hreg[2], dreg + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      CKG_CUDA(cudaStreamSynchronize(st));
+      if (hreg[2] == 0) {
+        mig_left = uint64_t(tail[0]) + tail[1];
+        mig_right = uint64_t(tail[2]) + tail[3];
+        stay_l = reg_pl - mig_left;
+        stay_r = nr - mig_right;
+        n_stay = n - mig_left - mig_right;
+        counts[0] = mig_left;
+        counts[1] = mig_right;
+        return CKG_OK;
+      }
+      mig_region = false;  // a crosser away from the boundary planes (dt beyond CFL): full path
+    }
     exclusive_scan(fl_stay, pos_stay, n, scan_partials_n, st);
     exclusive_scan(fl_left, pos_left, n, scan_partials_n, st);
     exclusive_scan(fl_right, pos_right, n, scan_partials_n, st);
-    launches += 11;
+    launches += 9;
     uint32_t tail[6] = {0, 0, 0, 0, 0, 0};
     if (n) {
       CKG_CUDA(cudaMemcpyAsync(&tail[0], pos_stay + n - 1, 4, cudaMemcpyDeviceToHost, st));
@@ -1323,13 +1398,41 @@ struct Context final : CtxBase {
 
   int slab_pack(uint64_t nl_in, void* left, void* right) override {
     CKG_CUDA(cudaSetDevice(device));
+    PState<T> nx = state(cur ^ 1);
+    if (mig_region) {
+      // window start after the exchange: wb + out_left - in_left must stay in
+      // the buffer (else relayout through the full path below)
+      const int64_t base = int64_t(wb[cur ^ 1]) + int64_t(mig_left) - int64_t(nl_in);
+      if (base >= 0) {
+        PState<T> tmp = state_at(cur, wb[cur ^ 1], n);  // the old state buffer, same window: scratch
+        if (reg_pl)
+          region_out_kernel<T><<<grid_for(reg_pl, 256, 1 << 30), 256, 0, st>>>(
+              nx, skeys, 0, reg_pl, fl_left, pos_left, fl_right, pos_right, static_cast<T*>(left),
+              static_cast<T*>(right), tmp);
+        if (n > reg_pr)
+          region_out_kernel<T><<<grid_for(n - reg_pr, 256, 1 << 30), 256, 0, st>>>(
+              nx, skeys, reg_pr, n, fl_left, pos_left, fl_right, pos_right, static_cast<T*>(left),
+              static_cast<T*>(right), tmp);
+        launches += 2;
+        CKG_CUDA(cudaStreamSynchronize(st));
+        return CKG_OK;
+      }
+      mig_region = false;
+      // the region scans are not the full ones the relayout needs
+      exclusive_scan(fl_stay, pos_stay, n, scan_partials_n, st);
+      exclusive_scan(fl_left, pos_left, n, scan_partials_n, st);
+      exclusive_scan(fl_right, pos_right, n, scan_partials_n, st);
+      launches += 9;
+    }
+    // full relayout into the other buffer, re-centred: survivors at
+    // [nl_in, nl_in + n_stay) with their sorted keys of this substep (the
+    // next substep's ko); migrants -> records
+    const uint64_t total_max = nl_in + n_stay + std::max<uint64_t>(n, 1u << 20);
     if (nl_in + n_stay > cap) {
       last_error = "slab: particle capacity of this rank exceeded";
       return CKG_ERR_DEVICE;
     }
-    // survivors -> the cur buffer at [nl_in, nl_in + n_stay) with their
-    // sorted keys of this substep (the next substep's ko); migrants -> records
-    PState<T> nx = state(cur ^ 1);
+    wb[cur] = cap > total_max ? (cap - total_max) / 2 : 0;
     PState<T> dst = state(cur);
     migrate_out_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
         nx, skeys, fl_stay, pos_stay, fl_left, pos_left, fl_right, pos_right, dst, skeys_tmp, nl_in,
@@ -1342,19 +1445,52 @@ struct Context final : CtxBase {
   int slab_finish(const void* left, uint64_t nl, const void* right, uint64_t nr, ckg_step_out* out) override {
     CKG_CUDA(cudaSetDevice(device));
     const uint64_t total = nl + n_stay + nr;
-    if (total > cap) {
-      last_error = "slab: particle capacity of this rank exceeded";
-      return CKG_ERR_DEVICE;
+    const bool region = mig_region;
+    if (mig_region) {
+      const int nb = cur ^ 1;
+      const uint64_t base = wb[nb] + mig_left - nl;
+      if (base + total > cap) {
+        last_error = "slab: particle capacity of this rank exceeded";
+        return CKG_ERR_DEVICE;
+      }
+      // region survivors into place (old window coordinates), then the
+      // next substep's keys, then the incoming migrants (new window)
+      PState<T> tmp = state_at(cur, wb[nb], n);
+      PState<T> old_win = state_at(nb, wb[nb], n);
+      if (reg_pl)
+        region_in_kernel<T><<<grid_for(reg_pl, 256, 1 << 30), 256, 0, st>>>(tmp, 0, reg_pl, fl_stay, pos_stay, old_win,
+                                                                            int64_t(mig_left));
+      if (n > reg_pr)
+        region_in_kernel<T><<<grid_for(n - reg_pr, 256, 1 << 30), 256, 0, st>>>(
+            tmp, reg_pr, n, fl_stay, pos_stay + reg_pl, old_win, int64_t(reg_pr));
+      region_keys_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
+          skeys, n, reg_pl, reg_pr, int64_t(nl) - int64_t(mig_left), fl_stay, pos_stay, pos_stay + reg_pl, nl,
+          stay_l, skeys_tmp);
+      PState<T> dst = state_at(nb, base, total);
+      if (nl)
+        migrate_in_kernel<T><<<grid_for(nl, 256, 1 << 30), 256, 0, st>>>(static_cast<const T*>(left), nl, dst,
+                                                                         skeys_tmp, 0);
+      if (nr)
+        migrate_in_kernel<T><<<grid_for(nr, 256, 1 << 30), 256, 0, st>>>(static_cast<const T*>(right), nr, dst,
+                                                                         skeys_tmp, total - nr);
+      launches += 5;
+      wb[nb] = base;
+      cur = nb;
+    } else {
+      if (wb[cur] + total > cap) {
+        last_error = "slab: particle capacity of this rank exceeded";
+        return CKG_ERR_DEVICE;
+      }
+      PState<T> dst = state(cur);
+      dst.n = total;
+      if (nl)
+        migrate_in_kernel<T><<<grid_for(nl, 256, 1 << 30), 256, 0, st>>>(static_cast<const T*>(left), nl, dst,
+                                                                         skeys_tmp, 0);
+      if (nr)
+        migrate_in_kernel<T><<<grid_for(nr, 256, 1 << 30), 256, 0, st>>>(static_cast<const T*>(right), nr, dst,
+                                                                         skeys_tmp, nl + n_stay);
+      launches += 2;
     }
-    PState<T> dst = state(cur);
-    dst.n = total;
-    if (nl)
-      migrate_in_kernel<T><<<grid_for(nl, 256, 1 << 30), 256, 0, st>>>(static_cast<const T*>(left), nl, dst,
-                                                                       skeys_tmp, 0);
-    if (nr)
-      migrate_in_kernel<T><<<grid_for(nr, 256, 1 << 30), 256, 0, st>>>(static_cast<const T*>(right), nr, dst,
-                                                                       skeys_tmp, nl + n_stay);
-    launches += 2;
     std::swap(ko, skeys_tmp);
     ko_valid = true;  // [left keys][survivor keys][right keys] is non-decreasing
     n = total;
@@ -1366,6 +1502,7 @@ struct Context final : CtxBase {
     out->kernel_launches = launches;
     out->sort_changed = last_changed;
     out->sort_kind = last_sort_kind;
+    out->slab_migration = region ? 1 : 2;
     grid_valid = true;
     last_active = hstat->n_active;
     int rc = decode_status(out, CKG_PHASE_G2P);

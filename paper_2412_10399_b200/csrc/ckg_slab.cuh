@@ -142,4 +142,96 @@ __global__ void migrate_in_kernel(const T* __restrict__ rec, uint64_t count, PSt
   dst_oldkey[j] = word_to_u32(p[kNumFields + 7]);
 }
 
+// ---- windowed migration (region path) -----------------------------------
+// In a slab the state lives in a window [wb, wb + n) of each buffer.  Block
+// crossers can only come from the first and last owned block plane (a
+// substep moves a particle less than a cell), i.e. from the sorted prefix
+// [0, PL) and suffix [PR, n).  Only those regions are compacted; the middle
+// stays in place and the window start moves by (out_left - in_left).
+
+// PL = first sorted position with key >= key_a, PR = first with key >= key_b.
+__global__ void slab_regions_kernel(const uint32_t* __restrict__ skeys, uint64_t n, uint32_t key_a,
+                                    uint32_t key_b, unsigned long long* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const uint32_t kk[2] = {key_a, key_b};
+  for (int q = 0; q < 2; ++q) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (skeys[mid] < kk[q]) lo = mid + 1; else hi = mid;
+    }
+    out[q] = lo;
+  }
+}
+
+// Migrants found in the middle region: the region path does not apply.
+__global__ void count_far_kernel(const uint32_t* __restrict__ left, const uint32_t* __restrict__ right,
+                                 uint64_t i0, uint64_t i1, unsigned long long* __restrict__ far) {
+  unsigned int c = 0;
+  for (uint64_t i = i0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < i1;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    c += left[i] | right[i];
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(far, (unsigned long long)c);
+}
+
+template <typename T>
+__device__ __forceinline__ void copy_particle(const PState<T>& a, uint64_t i, const PState<T>& b, uint64_t j) {
+#pragma unroll 3
+  for (int k = 0; k < kNumFields; ++k) b.f[uint64_t(k) * b.stride + j] = a.f[uint64_t(k) * a.stride + i];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) b.tau[uint64_t(k) * b.stride + j] = a.tau[uint64_t(k) * a.stride + i];
+  b.mat[j] = a.mat[i];
+}
+
+// Region [i0, i1): migrants -> records (scanned positions pos_*[i - i0] local
+// to the region), survivors -> tmp at the same index.
+template <typename T>
+__global__ void region_out_kernel(PState<T> src, const uint32_t* __restrict__ oldkey, uint64_t i0, uint64_t i1,
+                                  const uint32_t* __restrict__ fl_left, const uint32_t* __restrict__ pos_left,
+                                  const uint32_t* __restrict__ fl_right, const uint32_t* __restrict__ pos_right,
+                                  T* __restrict__ rec_left, T* __restrict__ rec_right, PState<T> tmp) {
+  const uint64_t i = i0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= i1) return;
+  const uint64_t r = i - i0;
+  if (fl_left[i] | fl_right[i]) {
+    T* rec = fl_left[i] ? rec_left + uint64_t(pos_left[r]) * kMigrantWords
+                        : rec_right + uint64_t(pos_right[r]) * kMigrantWords;
+#pragma unroll 4
+    for (int k = 0; k < kNumFields; ++k) rec[k] = src.f[uint64_t(k) * src.stride + i];
+    rec[kNumFields] = word_of<T>(src.mat[i]);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) rec[kNumFields + 1 + k] = src.tau[uint64_t(k) * src.stride + i];
+    rec[kNumFields + 7] = word_of<T>(oldkey[i]);
+    return;
+  }
+  copy_particle(src, i, tmp, i);
+}
+
+// Region survivors back from tmp to dst at dst_base + (local scan of stay).
+template <typename T>
+__global__ void region_in_kernel(PState<T> tmp, uint64_t i0, uint64_t i1, const uint32_t* __restrict__ fl_stay,
+                                 const uint32_t* __restrict__ pos_stay, PState<T> dst, int64_t dst_base) {
+  const uint64_t i = i0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= i1 || !fl_stay[i]) return;
+  copy_particle(tmp, i, dst, uint64_t(dst_base + int64_t(pos_stay[i - i0])));
+}
+
+// Next substep's stored-order keys (relative to the new window): middle
+// [PL, PR) shifted by `shift` = in_left - out_left, region survivors at their
+// compacted positions; incoming migrants are filled by migrate_in_kernel.
+__global__ void region_keys_kernel(const uint32_t* __restrict__ skeys, uint64_t n, uint64_t PL, uint64_t PR,
+                                   int64_t shift, const uint32_t* __restrict__ fl_stay,
+                                   const uint32_t* __restrict__ pos_stay_l, const uint32_t* __restrict__ pos_stay_r,
+                                   uint64_t in_left, uint64_t stay_l, uint32_t* __restrict__ ko_new) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i >= PL && i < PR) {
+    ko_new[uint64_t(int64_t(i) + shift)] = skeys[i];
+  } else if (fl_stay[i]) {
+    const uint64_t j = i < PL ? in_left + pos_stay_l[i] : in_left + stay_l + (PR - PL) + pos_stay_r[i - PR];
+    ko_new[j] = skeys[i];
+  }
+}
+
 }  // namespace ckg

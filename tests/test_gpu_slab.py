@@ -32,9 +32,13 @@ def _keys(p, cfg):
     return (c[:, 0] * D + c[:, 1]) * D + c[:, 2]
 
 
+@pytest.mark.parametrize("relayout", ["region", "full"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("scheme,model", [("apic", "fixed_corotated"), ("pic", "drucker_prager")])
-def test_slab_loopback_matches_single_domain(world, scheme, model):
+def test_slab_loopback_matches_single_domain(world, scheme, model, relayout, monkeypatch):
+    # "region": crossers compacted out of the boundary planes only (windowed
+    # state); "full": the whole slab re-laid out (the fallback path)
+    monkeypatch.setenv("CKMPM_SLAB_FULL_RELAYOUT", "1" if relayout == "full" else "0")
     cfg = scene(scheme, model)
     p0 = tag_volumes(perturb(seed_particles(cfg), seed=3, fscale=0.002, vscale=0.05, bscale=0.05, xscale=0.1,
                              dx=1 / 48))
@@ -42,12 +46,14 @@ def test_slab_loopback_matches_single_domain(world, scheme, model):
     bounds, ranks = build_ranks(cfg, world, particles=p0)
     assert len(ranks) == world
     migrated = 0
+    paths = set()
     for step in range(25):
         dt = single.cfl_dt(1.0)
         assert abs(ranks[0].cfl_dt(1.0) - dt) <= 1e-9 * dt
         single.step(dt)
         n_before = [r.n for r in ranks]
         run_loopback(ranks, dt)
+        paths |= {int(r.out.slab_migration) for r in ranks}
         migrated += sum(abs(a - r.n) for a, r in zip(n_before, ranks))
         a = single.particles()
         b = np.concatenate([r.particles() for r in ranks])
@@ -68,6 +74,8 @@ def test_slab_loopback_matches_single_domain(world, scheme, model):
             y = np.asarray(b[f], dtype=np.float64)
             assert np.max(np.abs(x - y)) <= 1e-10 * max(np.max(np.abs(x)), fl), (step, f)
     assert migrated > 0, "no particle crossed a slab boundary; the test would not exercise migration"
+    # (a slab one block plane wide always takes the full relayout)
+    assert (1 in paths) if relayout == "region" else (paths == {2}), paths
     for r in ranks:
         r.close()
     single.close()
