@@ -445,7 +445,7 @@ struct Context final : CtxBase {
     const uint64_t words = count * (kNumFields + 1);
     ensure_staging(words);
     CKG_CUDA(cudaMemcpyAsync(staging, p, words * sizeof(T), cudaMemcpyHostToDevice, st));
-    aos_to_soa_kernel<T><<<grid_for(words, 256), 256, 0, st>>>(staging, state(cur));
+    aos_to_soa_kernel<T><<<grid_for(count, kXpTile, 148 * 16), 256, 0, st>>>(staging, state(cur));
     CKG_CUDA(cudaGetLastError());
     CKG_CUDA(cudaStreamSynchronize(st));
     grid_valid = false;
@@ -463,7 +463,7 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaSetDevice(device));
     const uint64_t words = count * (kNumFields + 1);
     ensure_staging(words);
-    soa_to_aos_kernel<T><<<grid_for(words, 256), 256, 0, st>>>(state(cur), staging);
+    soa_to_aos_kernel<T><<<grid_for(count, kXpTile, 148 * 16), 256, 0, st>>>(state(cur), staging);
     CKG_CUDA(cudaGetLastError());
     CKG_CUDA(cudaMemcpyAsync(p, staging, words * sizeof(T), cudaMemcpyDeviceToHost, st));
     CKG_CUDA(cudaStreamSynchronize(st));

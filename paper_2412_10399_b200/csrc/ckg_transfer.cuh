@@ -904,36 +904,61 @@ __global__ void status_reset_kernel(DevStatus* st, int reset_err) {
 }
 
 // AoS <-> SoA transposes for the C-ABI (Particle<T> layout, transfer.hpp:19-28).
+// Particle<T> AoS <-> SoA, tiled through shared memory: 64 particles per
+// tile, the AoS side read/written as one contiguous run, the SoA side as one
+// 64-particle run per field (both coalesced; odd row pitch: no bank conflicts).
+constexpr int kXpTile = 64;
+constexpr int kXpPitch = kNumFields + 2;  // 27 fields + material word, +1 pad (odd)
+
 template <typename T>
-__global__ void aos_to_soa_kernel(const T* __restrict__ aos, PState<T> p) {
-  constexpr int W = kNumFields + 1;  // 27 fields + material word(s)
-  const uint64_t total = p.n * W;
-  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
-       k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t i = k / W;
-    const int f = int(k - i * W);
-    if (f < kNumFields)
-      p.f[uint64_t(f) * p.stride + i] = aos[k];
-    else
-      p.mat[i] = *reinterpret_cast<const uint32_t*>(aos + k);
+__device__ __forceinline__ T mat_word(uint32_t m) {
+  T w = T(0);
+  memcpy(&w, &m, sizeof(uint32_t));
+  return w;
+}
+template <typename T>
+__device__ __forceinline__ uint32_t word_mat(T w) {
+  uint32_t m;
+  memcpy(&m, &w, sizeof(uint32_t));
+  return m;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) aos_to_soa_kernel(const T* __restrict__ aos, PState<T> p) {
+  constexpr int W = kNumFields + 1;
+  __shared__ T tile[kXpTile * kXpPitch];
+  for (uint64_t b = uint64_t(blockIdx.x) * kXpTile; b < p.n; b += uint64_t(gridDim.x) * kXpTile) {
+    const int cnt = int(min(uint64_t(kXpTile), p.n - b));
+    for (int e = threadIdx.x; e < cnt * W; e += blockDim.x) tile[(e / W) * kXpPitch + e % W] = aos[b * W + e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < W * kXpTile; e += blockDim.x) {
+      const int f = e / kXpTile, j = e % kXpTile;
+      if (j < cnt) {
+        const T v = tile[j * kXpPitch + f];
+        if (f < kNumFields)
+          p.f[uint64_t(f) * p.stride + b + j] = v;
+        else
+          p.mat[b + j] = word_mat(v);
+      }
+    }
+    __syncthreads();
   }
 }
 
 template <typename T>
-__global__ void soa_to_aos_kernel(PState<T> p, T* __restrict__ aos) {
+__global__ void __launch_bounds__(256) soa_to_aos_kernel(PState<T> p, T* __restrict__ aos) {
   constexpr int W = kNumFields + 1;
-  const uint64_t total = p.n * W;
-  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
-       k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t i = k / W;
-    const int f = int(k - i * W);
-    if (f < kNumFields) {
-      aos[k] = p.f[uint64_t(f) * p.stride + i];
-    } else {
-      T word = T(0);
-      *reinterpret_cast<uint32_t*>(&word) = p.mat[i];
-      aos[k] = word;
+  __shared__ T tile[kXpTile * kXpPitch];
+  for (uint64_t b = uint64_t(blockIdx.x) * kXpTile; b < p.n; b += uint64_t(gridDim.x) * kXpTile) {
+    const int cnt = int(min(uint64_t(kXpTile), p.n - b));
+    for (int e = threadIdx.x; e < W * kXpTile; e += blockDim.x) {
+      const int f = e / kXpTile, j = e % kXpTile;
+      if (j < cnt)
+        tile[j * kXpPitch + f] = f < kNumFields ? p.f[uint64_t(f) * p.stride + b + j] : mat_word<T>(p.mat[b + j]);
     }
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt * W; e += blockDim.x) aos[b * W + e] = tile[(e / W) * kXpPitch + e % W];
+    __syncthreads();
   }
 }
 
