@@ -526,7 +526,7 @@ struct Context final : CtxBase {
       last_changed = nc;
       if (nc != 0 && uint64_t(nc) * 8 <= n) {
         exclusive_scan(wcnt, cpre, (n + 31) / 32, scan_partials_n, st);
-        compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);
+        compact_changed_kernel<<<grid_for((n + 31) / 32, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);
         launches += 4;
       }
       if (nc == 0) {
@@ -849,7 +849,7 @@ struct Context final : CtxBase {
         state(cur), T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko, chg, wcnt, dstat);
     const uint64_t nw = (n + 31) / 32;
     exclusive_scan(wcnt, cpre, nw, scan_partials_n, st);
-    compact_changed_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);
+    compact_changed_kernel<<<grid_for((n + 31) / 32, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);
     k += 7;
     cudaGraph_t g = capture_graph_of(st);
     cudaGraphConditionalHandle hs, hm, hf;

@@ -28,18 +28,23 @@ __device__ __forceinline__ uint32_t changed_before(const uint32_t* __restrict__ 
   return __ldg(woff + (p >> 5)) + uint32_t(__popc(b & ((1u << (p & 31)) - 1u)));
 }
 
-// |C| entries in index order (compacted changed list).
+// |C| entries in index order (compacted changed list): one thread per warp
+// word of changed flags, work proportional to the crossers.
 __global__ void __launch_bounds__(256) compact_changed_kernel(const uint32_t* __restrict__ keys,
                                                               const uint32_t* __restrict__ cbits,
                                                               const uint32_t* __restrict__ woff, uint64_t n,
                                                               uint32_t* __restrict__ ck, uint32_t* __restrict__ ci) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t b = __ldg(cbits + (i >> 5));
-  if (!((b >> (i & 31)) & 1u)) return;
-  const uint32_t pos = changed_before(cbits, woff, i);
-  ck[pos] = keys[i];
-  ci[pos] = uint32_t(i);
+  const uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= (n + 31) / 32) return;
+  uint32_t b = __ldg(cbits + w);
+  uint32_t pos = __ldg(woff + w);
+  while (b) {
+    const uint64_t i = w * 32 + uint64_t(__ffs(b) - 1);
+    ck[pos] = keys[i];
+    ci[pos] = uint32_t(i);
+    ++pos;
+    b &= b - 1u;
+  }
 }
 
 __global__ void __launch_bounds__(256) iota_kernel(uint32_t* __restrict__ p, uint64_t n) {
