@@ -175,6 +175,9 @@ struct Context final : CtxBase {
   int p2gq_ctas = 0, g2pq_ctas = 0;  // quadratic baseline kernels
   int32_t* dir = nullptr;
   uint32_t* active = nullptr;
+  uint32_t* rec = nullptr;   // per-item transfer records (kRecWords per active slot)
+  uint32_t* cord = nullptr;  // P2G class order of every chunk (sorted positions)
+  uint4* ccnt = nullptr;     // class counts of chunks past a segment's first
   uint32_t* scan_partials = nullptr;
   uint32_t* scan_partials_n = nullptr;  // scan scratch sized for n
   T* pool = nullptr;
@@ -301,6 +304,9 @@ struct Context final : CtxBase {
     dfree(seg_end);
     dfree(dir);
     dfree(active);
+    dfree(rec);
+    dfree(cord);
+    dfree(ccnt);
     dfree(scan_partials);
     dfree(scan_partials_n);
     dfree(pool);
@@ -318,9 +324,11 @@ struct Context final : CtxBase {
   void set_pool_cap(uint32_t cap) {
     dfree(pool);
     dfree(active);
+    dfree(rec);
     pool_cap = cap;
     pool = dalloc<T>(uint64_t(cap) * kBlockVals);
     active = dalloc<uint32_t>(cap);
+    rec = dalloc<uint32_t>(uint64_t(cap) * kRecWords);
   }
 
   PState<T> state(int b) const { return PState<T>{fbuf[b] + wb[b], mbuf[b] + wb[b], tbuf[b] + wb[b], n, cap}; }
@@ -409,6 +417,10 @@ struct Context final : CtxBase {
     }
     keys = dalloc<uint32_t>(cap);
     vals = dalloc<uint32_t>(cap);
+    dfree(cord);
+    dfree(ccnt);
+    cord = dalloc<uint32_t>(cap);
+    ccnt = dalloc<uint4>(cap / kP2GChunk + 2);
     rs.keys_alt = dalloc<uint32_t>(cap);
     rs.vals_alt = dalloc<uint32_t>(cap);
     uint64_t nh = uint64_t(kRadix) * sort_tiles(cap);
@@ -581,6 +593,8 @@ struct Context final : CtxBase {
                                                                pool_cap, dstat);
     if (slab) slab_ranges_kernel<<<1, 1, 0, st>>>(plane_start, D, bx_lo, bx_hi, dstat);
     segments_kernel<<<grid_for((n + 3) / 4, 256, 1 << 30), 256, 0, st>>>(skeys, n, seg_begin, seg_end);
+    xfer_prep_kernel<T><<<148 * 8, kPrepWarps * 32, 0, st>>>(cs, perm, make_const(0.0), dir, active, seg_begin, seg_end,
+                                                 pool_cap, dstat, rec, cord, ccnt, quad() ? 0 : 1);
   }
 
   template <int S>
@@ -592,19 +606,18 @@ struct Context final : CtxBase {
       return;
     }
     p2g_tile_kernel<T, S><<<p2g_ctas, kXferThreads, p2g_smem_bytes<T>(), st>>>(
-        state(cur), perm, c, dir, active, seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
+        state(cur), perm, c, dir, rec, cord, ccnt, pool, pool_cap, dstat, step_idx);
   }
   template <int S>
   void enqueue_g2p(const StepConst<T>& c, int step_idx) {
     if (quad()) {
       if constexpr (S != kSchemeMls)
         g2p_tile_kernel<T, S, 1><<<g2pq_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir,
-                                                                     active, seg_begin, seg_end, pool, pool_cap,
-                                                                     dstat, step_idx);
+                                                                     rec, pool, pool_cap, dstat, step_idx);
       return;
     }
-    g2p_tile_kernel<T, S><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir, active,
-                                                              seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
+    g2p_tile_kernel<T, S><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir, rec, pool,
+                                                              pool_cap, dstat, step_idx);
   }
 
   // Kernels enqueue_step launches (status reset, key/footprint, 5 per radix
@@ -612,7 +625,7 @@ struct Context final : CtxBase {
   // P2G, grid, G2P).
   uint64_t launches_per_step(int stop_after) const {
     uint64_t k = 1;  // status reset; sort kernels are counted by enqueue_sort
-    if (stop_after >= CKG_PHASE_ACTIVATE) k += 7;
+    if (stop_after >= CKG_PHASE_ACTIVATE) k += 8;
     if (stop_after >= CKG_PHASE_CLEAR) k += 1;
     if (stop_after >= CKG_PHASE_P2G) k += 1;
     if (stop_after >= CKG_PHASE_GRID) k += 1;
@@ -912,7 +925,7 @@ struct Context final : CtxBase {
     else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_g2p<kSchemeApic>(c, 0);
     else enqueue_g2p<kSchemeMls>(c, 0);
     frame_end_kernel<T><<<1, 32, 0, st>>>(dframe, dstat, h_loop, h_next, cfg.n_materials);
-    k += 7 + 1 + 3 + 1;
+    k += 8 + 1 + 3 + 1;
     graph_kernels = k;
     CKG_CUDA(cudaGetLastError());
     st = saved_st;

@@ -51,6 +51,9 @@ constexpr int kXferWarps = kXferThreads / 32;
 #ifndef CKG_P2G_EXP
 #define CKG_P2G_EXP 0  // development experiments only (1: no node ordering, 2: no tile RMW)
 #endif
+#ifndef CKG_P2G_ILV
+#define CKG_P2G_ILV 0  // 1: P2G fast path with both grids' updates of a node offset in flight together
+#endif
 #ifndef CKG_P2G_MINB
 #define CKG_P2G_MINB 2
 #endif
@@ -128,18 +131,162 @@ __device__ __forceinline__ int64_t nbr_offset(const int32_t* nbr, int g, int gi,
   return int64_t(slot) * kBlockVals + g * 256 + (((gi & 3) << 4) | ((gj & 3) << 2) | (gk & 3));
 }
 
+// ---- per-item records (one per active block, built once per substep by
+// xfer_prep_kernel and read by both transfer kernels with a single 160-byte
+// load instead of the active -> segment -> directory lookup chain)
+constexpr int kRecWords = 40;
+constexpr int kRecKey = 0, kRecS0 = 1, kRecS1 = 2, kRecNbr = 4, kRecCls = 32;
+
+// Sub-octant class of a particle (frac(x/dx - 1/4) >= 1/2 per axis): particles
+// of one class have distinct -1 and +1 grid bases as soon as their +1 cells
+// differ, so a warp scattering one class sees (for lattice-like layouts) a
+// single rank layer per grid.
+template <typename T>
+__device__ __forceinline__ uint32_t subocta_class(const PState<T>& p, uint32_t src, const StepConst<T>& c) {
+  uint32_t q = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const T sa = sub_rn(over_dx(__ldg(p.f + uint64_t(kX + a) * p.stride + src), c.dx, c.inv_dx, c.pow2), T(0.25));
+    q |= ((sa - dfloor(sa)) >= T(0.5) ? 1u : 0u) << a;
+  }
+  return q;
+}
+
+// Transfer preparation (after activation + segments), one warp per active
+// item: its record {key, s0, s1, 27 neighbour slots, class counts of chunk 0},
+// and for the compact kernel's P2G the class order of every 512-particle
+// chunk of its segment: cord[cb + j] = state index of the j-th particle of
+// the chunk in (class, sorted position) order — stable and deterministic
+// (ballot ranks, no atomics).  Class counts of chunks past the first go to
+// ccnt[cb >> 9] (chunk starts past a segment's first are >= 513 apart, so the
+// index is unique).  Warps are independent (no CTA barriers) and each issues
+// its chunk's loads four 32-particle groups at a time, so the item's short
+// dependency chain (active -> segment -> perm -> x) is hidden by the other
+// warps in flight.
+constexpr int kPrepWarps = 8;
+template <typename T>
+__global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
+    PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c, const int32_t* __restrict__ dir,
+    const uint32_t* __restrict__ active, const uint32_t* __restrict__ seg_begin,
+    const uint32_t* __restrict__ seg_end, uint32_t cap, const DevStatus* st, uint32_t* __restrict__ rec,
+    uint32_t* __restrict__ cord, uint4* __restrict__ ccnt, int classes) {
+  constexpr int kG = kP2GChunk / 32;  // 32-particle groups per chunk
+  const int lane = threadIdx.x & 31;
+  const uint32_t na = min(st->item_hi, cap), lo = st->item_lo;
+  const uint32_t lt = lanemask_lt();
+  const int D = c.D;
+  const uint32_t nwarps = gridDim.x * kPrepWarps;
+  __shared__ uint32_t wcnt[kPrepWarps][8];
+  const int wib = threadIdx.x >> 5;
+  for (uint32_t item = lo + blockIdx.x * kPrepWarps + (threadIdx.x >> 5); item < na; item += nwarps) {
+    const uint32_t key = __ldg(active + item);
+    const uint32_t s0 = __ldg(seg_begin + key), s1 = __ldg(seg_end + key);
+    uint32_t* r = rec + uint64_t(item) * kRecWords;
+    {
+      int bx, by, bz;
+      decode_key(key, D, bx, by, bz);
+      uint32_t w = 0;
+      if (lane == kRecKey) w = key;
+      else if (lane == kRecS0) w = s0;
+      else if (lane == kRecS1) w = s1;
+      else if (lane >= kRecNbr && lane < kRecNbr + 27) {
+        const int t = lane - kRecNbr;
+        w = uint32_t(dir_lookup(dir, D, bx - 1 + t / 9, by - 1 + (t / 3) % 3, bz - 1 + t % 3));
+      }
+      r[lane] = w;
+    }
+    if (!classes || s1 <= s0) {
+      if (lane < kRecWords - kRecCls) r[kRecCls + lane] = 0u;
+      continue;
+    }
+    for (uint32_t cb = s0; cb < s1; cb += kP2GChunk) {
+      const uint32_t len = min(uint32_t(kP2GChunk), s1 - cb);
+      uint32_t src[kG];
+      uint32_t qp[2] = {0u, 0u};  // 4-bit class per group (8 = none)
+      if (lane < 8) wcnt[wib][lane] = 0u;
+      __syncwarp();
+      // pass 1: classes, four groups' loads in flight at a time; per-class
+      // totals accumulated by each class's leader lane
+#pragma unroll
+      for (int g0 = 0; g0 < kG; g0 += 4) {
+        T xs[4][3];
+#pragma unroll
+        for (int g = g0; g < g0 + 4; ++g) {
+          const uint32_t j = uint32_t(g) * 32 + lane;
+          src[g] = j < len ? __ldg(perm + cb + j) : 0u;
+        }
+#pragma unroll
+        for (int g = g0; g < g0 + 4; ++g) {
+          const uint32_t j = uint32_t(g) * 32 + lane;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            xs[g - g0][a] = j < len ? __ldg(cur.f + uint64_t(kX + a) * cur.stride + src[g]) : T(0);
+        }
+#pragma unroll
+        for (int g = g0; g < g0 + 4; ++g) {
+          const uint32_t j = uint32_t(g) * 32 + lane;
+          uint32_t q = 8u;
+          if (j < len) {
+            q = 0u;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              const T sa = sub_rn(over_dx(xs[g - g0][a], c.dx, c.inv_dx, c.pow2), T(0.25));
+              q |= ((sa - dfloor(sa)) >= T(0.5) ? 1u : 0u) << a;
+            }
+          }
+          qp[g >> 3] |= q << (4 * (g & 7));
+          const uint32_t peers = __match_any_sync(0xffffffffu, q);
+          if (q < 8u && (peers & lt) == 0u) wcnt[wib][q] += __popc(peers);
+          __syncwarp();
+        }
+      }
+      const uint32_t tot = lane < 8 ? wcnt[wib][lane] : 0u;
+      // class bases: exclusive scan of the 8 totals (lanes 0..7)
+      uint32_t base = tot;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, base, o);
+        if (lane >= o) base += u;
+      }
+      base -= tot;
+      __syncwarp();
+      if (lane < 8) wcnt[wib][lane] = base;  // next position of class lane
+      __syncwarp();
+      // pass 2: positions (class base + earlier groups of the class + rank)
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        const uint32_t q = (qp[g >> 3] >> (4 * (g & 7))) & 0xfu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, q);
+        if (q < 8u) {
+          cord[cb + wcnt[wib][q] + __popc(peers & lt)] = src[g];
+        }
+        __syncwarp();
+        if (q < 8u && (peers & lt) == 0u) wcnt[wib][q] += __popc(peers);
+        __syncwarp();
+      }
+      // chunk class counts (u16 pairs)
+      uint32_t pair = tot | (__shfl_down_sync(0xffffffffu, tot, 1) << 16);
+      if (lane < 8 && !(lane & 1)) {
+        if (cb == s0) r[kRecCls + (lane >> 1)] = pair;
+        else reinterpret_cast<uint32_t*>(ccnt + (cb >> 9))[lane >> 1] = pair;
+      }
+      if (cb == s0 && lane >= 4 && lane < kRecWords - kRecCls) r[kRecCls + lane] = 0u;
+    }
+  }
+}
+
 template <typename T, int SCHEME>
 __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
     p2g_tile_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
-                    const int32_t* __restrict__ dir, const uint32_t* __restrict__ active,
-                    const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_end,
+                    const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
+                    const uint32_t* __restrict__ cord, const uint4* __restrict__ ccnt,
                     T* __restrict__ pool, uint32_t cap, DevStatus* st, int step) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tiles = reinterpret_cast<T*>(smem_raw);
-  __shared__ int32_t nbr[27];
-  __shared__ uint32_t s_item;
-  __shared__ uint32_t cls_cnt[8], cls_off[8];
-  __shared__ uint32_t cls_list[kP2GChunk];  // class order -> state index (perm applied)
+  // item records double-buffered: warp 0 claims the next item and loads its
+  // record while the other warps flush the current one
+  __shared__ uint32_t s_recb[2][kRecWords];
+  __shared__ uint32_t s_itemb[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   T* wt = tiles + warp * kPTVals;
   for (int e = tid; e < kXferWarps * kPTVals; e += kXferThreads) tiles[e] = T(0);
@@ -148,64 +295,50 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
   const uint32_t lt = lanemask_lt();
   const int D = c.D;
   const T dx = c.dx, dt = step_dt(c);
-  for (;;) {
+  auto claim = [&](int b) {  // warp 0 only
+    uint32_t it = 0;
+    if (lane == 0) it = item0 + atomicAdd(&st->work[0], 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (lane == 0) s_itemb[b] = it;
+    if (it < na) {
+      const uint32_t* r = rec + uint64_t(it) * kRecWords;
+      s_recb[b][lane] = __ldg(r + lane);
+      if (lane < kRecWords - 32) s_recb[b][32 + lane] = __ldg(r + 32 + lane);
+    }
+  };
+  if (warp == 0) claim(0);
+  for (int buf = 0;; buf ^= 1) {
     __syncthreads();
-    if (tid == 0) s_item = item0 + atomicAdd(&st->work[0], 1u);
-    __syncthreads();
-    const uint32_t item = s_item;
+    const uint32_t item = s_itemb[buf];
     if (item >= na) break;
-    const uint32_t key = active[item];
-    const uint32_t s0 = seg_begin[key], s1 = seg_end[key];
-    if (s1 <= s0) continue;
+    const uint32_t* s_rec = s_recb[buf];
+    const int32_t* nbr = reinterpret_cast<const int32_t*>(s_rec + kRecNbr);
+    const uint32_t key = s_rec[kRecKey];
+    const uint32_t s0 = s_rec[kRecS0], s1 = s_rec[kRecS1];
+    if (s1 <= s0) {
+      if (warp == 0) claim(buf ^ 1);
+      continue;
+    }
     int bx, by, bz;
     decode_key(key, D, bx, by, bz);
-    if (tid < 27) nbr[tid] = dir_lookup(dir, D, bx - 1 + tid / 9, by - 1 + (tid / 3) % 3, bz - 1 + tid % 3);
-    __syncthreads();
     for (uint32_t cb = s0; cb < s1; cb += kP2GChunk) {
-      // ---- bin the chunk by sub-octant class (frac(x/dx - 1/4) >= 1/2 per
-      // axis): particles of one class have distinct -1 and +1 grid bases as
-      // soon as their +1 cells differ, so warp w scatters class w with (for
-      // lattice-like layouts) a single rank layer per grid.
-      const uint32_t len = min(uint32_t(kP2GChunk), s1 - cb);
-      if (tid < 8) cls_cnt[tid] = 0;
-      __syncthreads();
-      uint32_t myq[kP2GChunk / kXferThreads], myslot[kP2GChunk / kXferThreads], mysrc[kP2GChunk / kXferThreads];
-#pragma unroll
-      for (int r = 0; r < kP2GChunk / kXferThreads; ++r) {
-        const uint32_t j = tid + r * kXferThreads;
-        if (j < len) {
-          const uint32_t src = __ldg(perm + cb + j);
-          mysrc[r] = src;
-          uint32_t q = 0;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const T sa = sub_rn(over_dx(__ldg(cur.f + uint64_t(kX + a) * cur.stride + src), dx, c.inv_dx, c.pow2), T(0.25));
-            q |= ((sa - dfloor(sa)) >= T(0.5) ? 1u : 0u) << a;
-          }
-          myq[r] = q;
-          myslot[r] = atomicAdd(&cls_cnt[q], 1u);
-        }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        uint32_t run = 0;
+      // this warp's class list of the chunk (xfer_prep_kernel)
+      uint32_t my_cnt = 0, my_off = 0;
+      {
+        uint4 v;
+        if (cb == s0) v = make_uint4(s_rec[kRecCls], s_rec[kRecCls + 1], s_rec[kRecCls + 2], s_rec[kRecCls + 3]);
+        else v = __ldg(ccnt + (cb >> 9));
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          cls_off[q] = run;
-          run += cls_cnt[q];
+          const uint32_t cq = (w4[q >> 1] >> (16 * (q & 1))) & 0xffffu;
+          if (q < warp) my_off += cq;
+          if (q == warp) my_cnt = cq;
         }
       }
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < kP2GChunk / kXferThreads; ++r) {
-        const uint32_t j = tid + r * kXferThreads;
-        if (j < len) cls_list[cls_off[myq[r]] + myslot[r]] = mysrc[r];
-      }
-      __syncthreads();
-      const uint32_t my_cnt = cls_cnt[warp], my_off = cls_off[warp];
       for (uint32_t rb = 0; rb < my_cnt; rb += 32) {
       const bool in_round = rb + lane < my_cnt;
-      const uint32_t src = in_round ? cls_list[my_off + rb + lane] : 0u;
+      const uint32_t src = in_round ? __ldg(cord + cb + my_off + rb + lane) : 0u;
       // sorted index of this particle, for error reports only (rare path)
       auto sorted_index = [&]() -> uint32_t {
         for (uint32_t k = cb; k < min(cb + uint32_t(kP2GChunk), s1); ++k)
@@ -262,112 +395,125 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
           }
         }
       }
-      // ---- scatter, grid by grid
+      // ---- scatter: per-grid tile placement and intra-warp node conflicts
+      bool in_tile[2];
+      uint32_t rank[2], maxrank[2];
+      T* p0[2];
+      T u0[2][3];
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
         const Axis<T>* ax = ds.ax[g];
         const int lx = ax[0].base - (4 * bx - (g ? cx : 0)), ly = ax[1].base - (4 * by - (g ? cy : 0)),
                   lz = ax[2].base - (4 * bz - (g ? cz : 0));
-        const bool in_tile =
-            valid && lx >= 0 && ly >= 0 && lz >= 0 && lx <= kPT - 2 && ly <= kPT - 2 && lz <= kPT - 2;
-        const uint32_t cell = in_tile ? uint32_t((lx * kPT + ly) * kPT + lz) : (1024u + lane);
+        in_tile[g] = valid && lx >= 0 && ly >= 0 && lz >= 0 && lx <= kPT - 2 && ly <= kPT - 2 && lz <= kPT - 2;
+        const uint32_t cell = in_tile[g] ? uint32_t((lx * kPT + ly) * kPT + lz) : (1024u + lane);
         const uint32_t peers = __match_any_sync(0xffffffffu, cell);
-        const uint32_t rank = __popc(peers & lt);
-        const uint32_t maxrank = __reduce_max_sync(0xffffffffu, rank);
+        rank[g] = __popc(peers & lt);
+        maxrank[g] = __reduce_max_sync(0xffffffffu, rank[g]);
+        p0[g] = wt + g * 4 * kPTNodes + (in_tile[g] ? ((lx * kPT + ly) * kPT + lz) * kNS : 0);
         // node momentum base b_stu = m v + Q xi_stu = u0 + dx (s Qx + t Qy + u Qz)
-        T u0[3] = {mv[0], mv[1], mv[2]};
-        if (SCHEME != kSchemePic) {
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
-            u0[a] += Q.a[a][0] * ax[0].xi0 + Q.a[a][1] * ax[1].xi0 + Q.a[a][2] * ax[2].xi0;
+        for (int a = 0; a < 3; ++a) {
+          u0[g][a] = mv[a];
+          if (SCHEME != kSchemePic)
+            u0[g][a] += Q.a[a][0] * ax[0].xi0 + Q.a[a][1] * ax[1].xi0 + Q.a[a][2] * ax[2].xi0;
         }
-        // Node contribution (m w, w b - A' grad w) or, for MLS, the force
-        // through grad Phi = w M^-1 P(xi) (transfer.hpp:335-369).
-        // (selects, not arrays indexed by s/t/u: the rolled paths below
-        // would otherwise put the axis weights in local memory)
-        auto contrib = [&](int s, int t, int u, T (&o)[4]) {
-          const T wxs = s ? ax[0].w1 : ax[0].w0, wyt = t ? ax[1].w1 : ax[1].w0, wzu = u ? ax[2].w1 : ax[2].w0;
-          const T wyz = wyt * wzu;
-          const T w = wxs * wyz;
-          T gw0, gw1, gw2;
-          if (SCHEME != kSchemeMls) {
-            const T gxs = s ? -ax[0].g0 : ax[0].g0, gyt = t ? -ax[1].g0 : ax[1].g0, gzu = u ? -ax[2].g0 : ax[2].g0;
-            gw0 = gxs * wyz;
-            gw1 = wxs * (gyt * wzu);
-            gw2 = wxs * (wyt * gzu);
-          } else {
-            const T P1 = ax[0].xi0 + (s ? dx : T(0)), P2 = ax[1].xi0 + (t ? dx : T(0)),
-                    P3 = ax[2].xi0 + (u ? dx : T(0));
-            gw0 = w * (Minv[1][0] + Minv[1][1] * P1 + Minv[1][2] * P2 + Minv[1][3] * P3);
-            gw1 = w * (Minv[2][0] + Minv[2][1] * P1 + Minv[2][2] * P2 + Minv[2][3] * P3);
-            gw2 = w * (Minv[3][0] + Minv[3][1] * P1 + Minv[3][2] * P2 + Minv[3][3] * P3);
-          }
-          o[0] = w * m;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            T b = u0[a];
-            if (SCHEME != kSchemePic) {
-              // + Q (s, t, u) dx, fused (no dx-scaled copy of Q kept live)
-              if (s) b = fma(Q.a[a][0], dx, b);
-              if (t) b = fma(Q.a[a][1], dx, b);
-              if (u) b = fma(Q.a[a][2], dx, b);
-            }
-            o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
-          }
-        };
-        T* p0 = wt + g * 4 * kPTNodes + ((lx * kPT + ly) * kPT + lz) * kNS;
-#if CKG_P2G_EXP == 2
-        T sink = T(0);
-#endif
-        if (maxrank == 0) {
-          // fast path: every lane owns a distinct base cell in this warp, so
-          // at a fixed node offset all lanes write distinct nodes
-          {
-#pragma unroll
-            for (int s = 0; s < 2; ++s)
-#pragma unroll
-              for (int t = 0; t < 2; ++t)
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                  T o[4];
-                  contrib(s, t, u, o);
-                  T* p = p0 + ((s * kPT + t) * kPT + u) * kNS;
-#if CKG_P2G_EXP == 2
-                  sink += o[0] + o[1] + o[2] + o[3];
-#else
-                  if (in_tile) tile_add4(p, o);
-#endif
-#if CKG_P2G_EXP == 0
-                  // node (s,t,u) of one lane can be node (0,0,0) of its
-                  // neighbour: order the read-modify-writes across lanes
-                  __syncwarp();
-#endif
-                }
-          }
+      }
+      // Node contribution (m w, w b - A' grad w) or, for MLS, the force
+      // through grad Phi = w M^-1 P(xi) (transfer.hpp:335-369).
+      // (selects, not arrays indexed by s/t/u: the rolled paths below
+      // would otherwise put the axis weights in local memory)
+      auto contrib = [&](int g, int s, int t, int u, T (&o)[4]) {
+        const Axis<T>* ax = ds.ax[g];
+        const T wxs = s ? ax[0].w1 : ax[0].w0, wyt = t ? ax[1].w1 : ax[1].w0, wzu = u ? ax[2].w1 : ax[2].w0;
+        const T wyz = wyt * wzu;
+        const T w = wxs * wyz;
+        T gw0, gw1, gw2;
+        if (SCHEME != kSchemeMls) {
+          const T gxs = s ? -ax[0].g0 : ax[0].g0, gyt = t ? -ax[1].g0 : ax[1].g0, gzu = u ? -ax[2].g0 : ax[2].g0;
+          gw0 = gxs * wyz;
+          gw1 = wxs * (gyt * wzu);
+          gw2 = wxs * (wyt * gzu);
         } else {
-          // shared base cells: serialise by rank layers (rolled loop)
+          const T P1 = ax[0].xi0 + (s ? dx : T(0)), P2 = ax[1].xi0 + (t ? dx : T(0)),
+                  P3 = ax[2].xi0 + (u ? dx : T(0));
+          gw0 = w * (Minv[1][0] + Minv[1][1] * P1 + Minv[1][2] * P2 + Minv[1][3] * P3);
+          gw1 = w * (Minv[2][0] + Minv[2][1] * P1 + Minv[2][2] * P2 + Minv[2][3] * P3);
+          gw2 = w * (Minv[3][0] + Minv[3][1] * P1 + Minv[3][2] * P2 + Minv[3][3] * P3);
+        }
+        o[0] = w * m;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          T b = u0[g][a];
+          if (SCHEME != kSchemePic) {
+            // + Q (s, t, u) dx, fused (no dx-scaled copy of Q kept live)
+            if (s) b = fma(Q.a[a][0], dx, b);
+            if (t) b = fma(Q.a[a][1], dx, b);
+            if (u) b = fma(Q.a[a][2], dx, b);
+          }
+          o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
+        }
+      };
+      if ((SCHEME == kSchemeMls || !CKG_P2G_ILV) && (maxrank[0] | maxrank[1]) == 0) {
+        // MLS (register-heavy): one grid at a time
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int nid = 0; nid < 8; ++nid) {
+            const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
+            T o[4];
+            contrib(g, s, t, u, o);
+            if (in_tile[g]) tile_add4(p0[g] + ((s * kPT + t) * kPT + u) * kNS, o);
+            __syncwarp();
+          }
+      } else if ((maxrank[0] | maxrank[1]) == 0) {
+        // fast path: every lane owns a distinct base cell on both grids, so
+        // at a fixed node offset all lanes write distinct nodes; the two
+        // grids' tiles are disjoint, so both grids' updates of one offset
+        // are in flight together
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              T o0[4], o1[4];
+              contrib(0, s, t, u, o0);
+              contrib(1, s, t, u, o1);
+              const int off = ((s * kPT + t) * kPT + u) * kNS;
+              if (in_tile[0]) tile_add4(p0[0] + off, o0);
+              if (in_tile[1]) tile_add4(p0[1] + off, o1);
+              // node (s,t,u) of one lane can be node (0,0,0) of its
+              // neighbour: order the read-modify-writes across lanes
+              __syncwarp();
+            }
+      } else {
+        // shared base cells: serialise by rank layers (rolled loop)
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
 #pragma unroll 1
           for (int nid = 0; nid < 8; ++nid) {
             const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
             T o[4];
-            contrib(s, t, u, o);
-            T* p = p0 + ((s * kPT + t) * kPT + u) * kNS;
-            for (uint32_t layer = 0; layer <= maxrank; ++layer) {
-              if (in_tile && rank == layer) tile_add4(p, o);
+            contrib(g, s, t, u, o);
+            T* p = p0[g] + ((s * kPT + t) * kPT + u) * kNS;
+            for (uint32_t layer = 0; layer <= maxrank[g]; ++layer) {
+              if (in_tile[g] && rank[g] == layer) tile_add4(p, o);
               __syncwarp();
             }
           }
         }
-#if CKG_P2G_EXP == 2
-        if (sink == T(12345)) p0[0] = sink;
-#endif
-        if (valid && !in_tile) {
+      }
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        if (valid && !in_tile[g]) {
           // footprint outside the block tile: direct REDs through the directory
+          const Axis<T>* ax = ds.ax[g];
 #pragma unroll 1
           for (int nid = 0; nid < 8; ++nid) {
             const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
             T o[4];
-            contrib(s, t, u, o);
+            contrib(g, s, t, u, o);
             const int gi = ax[0].base + s, gj = ax[1].base + t, gk = ax[2].base + u;
             const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
             if (slot < 0 || uint32_t(slot) >= cap) {
@@ -383,9 +529,9 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
         }
       }
       }  // rounds of this warp's class list
-      __syncthreads();
     }
     __syncthreads();
+    if (warp == 0) claim(buf ^ 1);
     // ---- flush: sum the warp tiles, one REDG per non-zero node value.
     // Slot 0: all class tiles share origin 4b (5^3).  Slot 1: the 6^3 halo
     // from 4b - 1; warp w's tile covers offsets [1 - c, 5 - c] per axis.
@@ -583,13 +729,13 @@ __device__ __forceinline__ void gather_quad(const QAxis<T> (&q)[3], T dx, VelFn 
 template <typename T, int SCHEME, int KQ = 0>
 __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
     g2p_tile_kernel(PState<T> cur, PState<T> nxt, const uint32_t* __restrict__ perm, StepConst<T> c,
-                    const int32_t* __restrict__ dir, const uint32_t* __restrict__ active,
-                    const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_end,
+                    const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
                     const T* __restrict__ pool, uint32_t cap, DevStatus* st, int step) {
   __shared__ T vt[kVelVals];
-  __shared__ int32_t nbr[27];
+  __shared__ uint32_t s_rec[kRecNbr + 27];
   __shared__ uint32_t s_item;
   __shared__ T wmax[kG2PWarps];
+  const int32_t* nbr = reinterpret_cast<const int32_t*>(s_rec + kRecNbr);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const int D = c.D;
@@ -597,17 +743,24 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
   T vmax2 = T(0);
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_item = item0 + atomicAdd(&st->work[1], 1u);
+    if (warp == 0) {
+      uint32_t it = 0;
+      if (lane == 0) it = item0 + atomicAdd(&st->work[1], 1u);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (lane == 0) s_item = it;
+      if (it < na) {
+        const uint32_t* r = rec + uint64_t(it) * kRecWords;
+        if (lane < kRecNbr + 27) s_rec[lane] = __ldg(r + lane);
+      }
+    }
     __syncthreads();
     const uint32_t item = s_item;
     if (item >= na) break;
-    const uint32_t key = active[item];
-    const uint32_t s0 = seg_begin[key], s1 = seg_end[key];
+    const uint32_t key = s_rec[kRecKey];
+    const uint32_t s0 = s_rec[kRecS0], s1 = s_rec[kRecS1];
     if (s1 <= s0) continue;
     int bx, by, bz;
     decode_key(key, D, bx, by, bz);
-    if (tid < 27) nbr[tid] = dir_lookup(dir, D, bx - 1 + tid / 9, by - 1 + (tid / 3) % 3, bz - 1 + tid % 3);
-    __syncthreads();
     // stage nodal velocities of both grids' 6^3 tiles: all of a thread's
     // loads are issued before the first shared store
     {
