@@ -87,10 +87,12 @@ __device__ __forceinline__ void tile_add4(double* p, const double (&o)[4]) {
     q[0] = a;
     q[1] = b;
   } else {
-    p[0] += o[0];
-    p[kVS] += o[1];
-    p[2 * kVS] += o[2];
-    p[3 * kVS] += o[3];
+    // all four loads issued before the first add
+    const double a0 = p[0], a1 = p[kVS], a2 = p[2 * kVS], a3 = p[3 * kVS];
+    p[0] = a0 + o[0];
+    p[kVS] = a1 + o[1];
+    p[2 * kVS] = a2 + o[2];
+    p[3 * kVS] = a3 + o[3];
   }
 }
 __device__ __forceinline__ void tile_add4(float* p, const float (&o)[4]) {
@@ -395,125 +397,113 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
           }
         }
       }
-      // ---- scatter: per-grid tile placement and intra-warp node conflicts
-      bool in_tile[2];
-      uint32_t rank[2], maxrank[2];
-      T* p0[2];
-      T u0[2][3];
+      // ---- scatter, grid by grid.  Only one grid's stencil is live during
+      // its scatter: the +1 grid's axes are re-evaluated (axis_pair with
+      // k = +1/4 is bit-identical to the dual evaluation) instead of being
+      // carried through the -1 grid's scatter, which frees the registers
+      // that let each node's four read-modify-writes overlap.
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
-        const Axis<T>* ax = ds.ax[g];
+        Axis<T> ax[3];
+        if (g == 0) {
+          ax[0] = ds.ax[0][0];
+          ax[1] = ds.ax[0][1];
+          ax[2] = ds.ax[0][2];
+        } else {
+          ax[0] = axis_pair(x, dx, c.inv_dx, c.pow2, T(0.25));
+          ax[1] = axis_pair(y, dx, c.inv_dx, c.pow2, T(0.25));
+          ax[2] = axis_pair(z, dx, c.inv_dx, c.pow2, T(0.25));
+        }
         const int lx = ax[0].base - (4 * bx - (g ? cx : 0)), ly = ax[1].base - (4 * by - (g ? cy : 0)),
                   lz = ax[2].base - (4 * bz - (g ? cz : 0));
-        in_tile[g] = valid && lx >= 0 && ly >= 0 && lz >= 0 && lx <= kPT - 2 && ly <= kPT - 2 && lz <= kPT - 2;
-        const uint32_t cell = in_tile[g] ? uint32_t((lx * kPT + ly) * kPT + lz) : (1024u + lane);
+        const bool in_tile =
+            valid && lx >= 0 && ly >= 0 && lz >= 0 && lx <= kPT - 2 && ly <= kPT - 2 && lz <= kPT - 2;
+        const uint32_t cell = in_tile ? uint32_t((lx * kPT + ly) * kPT + lz) : (1024u + lane);
         const uint32_t peers = __match_any_sync(0xffffffffu, cell);
-        rank[g] = __popc(peers & lt);
-        maxrank[g] = __reduce_max_sync(0xffffffffu, rank[g]);
-        p0[g] = wt + g * 4 * kPTNodes + (in_tile[g] ? ((lx * kPT + ly) * kPT + lz) * kNS : 0);
+        const uint32_t rank = __popc(peers & lt);
+        const uint32_t maxrank = __reduce_max_sync(0xffffffffu, rank);
+        const uint32_t tmask = __ballot_sync(0xffffffffu, in_tile);
         // node momentum base b_stu = m v + Q xi_stu = u0 + dx (s Qx + t Qy + u Qz)
+        T u0[3] = {mv[0], mv[1], mv[2]};
+        if (SCHEME != kSchemePic) {
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          u0[g][a] = mv[a];
-          if (SCHEME != kSchemePic)
-            u0[g][a] += Q.a[a][0] * ax[0].xi0 + Q.a[a][1] * ax[1].xi0 + Q.a[a][2] * ax[2].xi0;
+          for (int a = 0; a < 3; ++a)
+            u0[a] += Q.a[a][0] * ax[0].xi0 + Q.a[a][1] * ax[1].xi0 + Q.a[a][2] * ax[2].xi0;
         }
-      }
-      // Node contribution (m w, w b - A' grad w) or, for MLS, the force
-      // through grad Phi = w M^-1 P(xi) (transfer.hpp:335-369).
-      // (selects, not arrays indexed by s/t/u: the rolled paths below
-      // would otherwise put the axis weights in local memory)
-      auto contrib = [&](int g, int s, int t, int u, T (&o)[4]) {
-        const Axis<T>* ax = ds.ax[g];
-        const T wxs = s ? ax[0].w1 : ax[0].w0, wyt = t ? ax[1].w1 : ax[1].w0, wzu = u ? ax[2].w1 : ax[2].w0;
-        const T wyz = wyt * wzu;
-        const T w = wxs * wyz;
-        T gw0, gw1, gw2;
-        if (SCHEME != kSchemeMls) {
-          const T gxs = s ? -ax[0].g0 : ax[0].g0, gyt = t ? -ax[1].g0 : ax[1].g0, gzu = u ? -ax[2].g0 : ax[2].g0;
-          gw0 = gxs * wyz;
-          gw1 = wxs * (gyt * wzu);
-          gw2 = wxs * (wyt * gzu);
+        // Node contribution (m w, w b - A' grad w) or, for MLS, the force
+        // through grad Phi = w M^-1 P(xi) (transfer.hpp:335-369).
+        // (selects, not arrays indexed by s/t/u: the rolled paths below
+        // would otherwise put the axis weights in local memory)
+        auto contrib = [&](int s, int t, int u, T (&o)[4]) {
+          const T wxs = s ? ax[0].w1 : ax[0].w0, wyt = t ? ax[1].w1 : ax[1].w0, wzu = u ? ax[2].w1 : ax[2].w0;
+          const T wyz = wyt * wzu;
+          const T w = wxs * wyz;
+          T gw0, gw1, gw2;
+          if (SCHEME != kSchemeMls) {
+            const T gxs = s ? -ax[0].g0 : ax[0].g0, gyt = t ? -ax[1].g0 : ax[1].g0, gzu = u ? -ax[2].g0 : ax[2].g0;
+            gw0 = gxs * wyz;
+            gw1 = wxs * (gyt * wzu);
+            gw2 = wxs * (wyt * gzu);
+          } else {
+            const T P1 = ax[0].xi0 + (s ? dx : T(0)), P2 = ax[1].xi0 + (t ? dx : T(0)),
+                    P3 = ax[2].xi0 + (u ? dx : T(0));
+            gw0 = w * (Minv[1][0] + Minv[1][1] * P1 + Minv[1][2] * P2 + Minv[1][3] * P3);
+            gw1 = w * (Minv[2][0] + Minv[2][1] * P1 + Minv[2][2] * P2 + Minv[2][3] * P3);
+            gw2 = w * (Minv[3][0] + Minv[3][1] * P1 + Minv[3][2] * P2 + Minv[3][3] * P3);
+          }
+          o[0] = w * m;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            T b = u0[a];
+            if (SCHEME != kSchemePic) {
+              // + Q (s, t, u) dx, fused (no dx-scaled copy of Q kept live)
+              if (s) b = fma(Q.a[a][0], dx, b);
+              if (t) b = fma(Q.a[a][1], dx, b);
+              if (u) b = fma(Q.a[a][2], dx, b);
+            }
+            o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
+          }
+        };
+        T* p0 = wt + g * 4 * kPTNodes + ((lx * kPT + ly) * kPT + lz) * kNS;
+        if (maxrank == 0) {
+          // fast path: every lane owns a distinct base cell in this warp, so
+          // at a fixed node offset all lanes write distinct nodes
+          if (in_tile) {
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+#pragma unroll
+              for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  T o[4];
+                  contrib(s, t, u, o);
+                  tile_add4(p0 + ((s * kPT + t) * kPT + u) * kNS, o);
+                  // node (s,t,u) of one lane can be node (0,0,0) of its
+                  // neighbour: order the read-modify-writes across lanes
+                  __syncwarp(tmask);
+                }
+          }
         } else {
-          const T P1 = ax[0].xi0 + (s ? dx : T(0)), P2 = ax[1].xi0 + (t ? dx : T(0)),
-                  P3 = ax[2].xi0 + (u ? dx : T(0));
-          gw0 = w * (Minv[1][0] + Minv[1][1] * P1 + Minv[1][2] * P2 + Minv[1][3] * P3);
-          gw1 = w * (Minv[2][0] + Minv[2][1] * P1 + Minv[2][2] * P2 + Minv[2][3] * P3);
-          gw2 = w * (Minv[3][0] + Minv[3][1] * P1 + Minv[3][2] * P2 + Minv[3][3] * P3);
-        }
-        o[0] = w * m;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          T b = u0[g][a];
-          if (SCHEME != kSchemePic) {
-            // + Q (s, t, u) dx, fused (no dx-scaled copy of Q kept live)
-            if (s) b = fma(Q.a[a][0], dx, b);
-            if (t) b = fma(Q.a[a][1], dx, b);
-            if (u) b = fma(Q.a[a][2], dx, b);
-          }
-          o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
-        }
-      };
-      if ((SCHEME == kSchemeMls || !CKG_P2G_ILV) && (maxrank[0] | maxrank[1]) == 0) {
-        // MLS (register-heavy): one grid at a time
-#pragma unroll
-        for (int g = 0; g < 2; ++g)
-#pragma unroll
-          for (int nid = 0; nid < 8; ++nid) {
-            const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
-            T o[4];
-            contrib(g, s, t, u, o);
-            if (in_tile[g]) tile_add4(p0[g] + ((s * kPT + t) * kPT + u) * kNS, o);
-            __syncwarp();
-          }
-      } else if ((maxrank[0] | maxrank[1]) == 0) {
-        // fast path: every lane owns a distinct base cell on both grids, so
-        // at a fixed node offset all lanes write distinct nodes; the two
-        // grids' tiles are disjoint, so both grids' updates of one offset
-        // are in flight together
-#pragma unroll
-        for (int s = 0; s < 2; ++s)
-#pragma unroll
-          for (int t = 0; t < 2; ++t)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              T o0[4], o1[4];
-              contrib(0, s, t, u, o0);
-              contrib(1, s, t, u, o1);
-              const int off = ((s * kPT + t) * kPT + u) * kNS;
-              if (in_tile[0]) tile_add4(p0[0] + off, o0);
-              if (in_tile[1]) tile_add4(p0[1] + off, o1);
-              // node (s,t,u) of one lane can be node (0,0,0) of its
-              // neighbour: order the read-modify-writes across lanes
-              __syncwarp();
-            }
-      } else {
-        // shared base cells: serialise by rank layers (rolled loop)
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
+          // shared base cells: serialise by rank layers (rolled loop)
 #pragma unroll 1
           for (int nid = 0; nid < 8; ++nid) {
             const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
             T o[4];
-            contrib(g, s, t, u, o);
-            T* p = p0[g] + ((s * kPT + t) * kPT + u) * kNS;
-            for (uint32_t layer = 0; layer <= maxrank[g]; ++layer) {
-              if (in_tile[g] && rank[g] == layer) tile_add4(p, o);
+            contrib(s, t, u, o);
+            T* p = p0 + ((s * kPT + t) * kPT + u) * kNS;
+            for (uint32_t layer = 0; layer <= maxrank; ++layer) {
+              if (in_tile && rank == layer) tile_add4(p, o);
               __syncwarp();
             }
           }
         }
-      }
-#pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        if (valid && !in_tile[g]) {
+        if (valid && !in_tile) {
           // footprint outside the block tile: direct REDs through the directory
-          const Axis<T>* ax = ds.ax[g];
 #pragma unroll 1
           for (int nid = 0; nid < 8; ++nid) {
             const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
             T o[4];
-            contrib(g, s, t, u, o);
+            contrib(s, t, u, o);
             const int gi = ax[0].base + s, gj = ax[1].base + t, gk = ax[2].base + u;
             const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
             if (slot < 0 || uint32_t(slot) >= cap) {

@@ -46,3 +46,19 @@ toti = sum(x[1] for x in recs) or 1
 print(f"# {kern}: {tot:.0f} stall samples, {toti:.3e} warp instructions")
 for s, i, loc, src in sorted(recs, reverse=True)[:top]:
     print(f"{100 * s / tot:5.1f}% smp {100 * i / toti:5.1f}% ins  {loc:22s} {src}")
+
+if "--ops" in sys.argv:
+    agg = {}
+    for s_, i_, loc, src in instrs:
+        op = src.split()[0] if src else "?"
+        if op.startswith("@"):
+            op = src.split()[1]
+        op = op.split(".")[0]
+        a = agg.setdefault(op, [0.0, 0.0])
+        a[0] += s_
+        a[1] += i_
+    ts = sum(v[0] for v in agg.values()) or 1
+    ti = sum(v[1] for v in agg.values()) or 1
+    print(f"# by opcode: {ti:.3e} warp instructions")
+    for op, (s_, i_) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:30]:
+        print(f"{op:14s} {100 * i_ / ti:5.1f}% ins {100 * s_ / ts:5.1f}% smp")
