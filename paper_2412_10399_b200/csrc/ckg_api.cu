@@ -178,6 +178,7 @@ struct Context final : CtxBase {
   uint32_t* rec = nullptr;   // per-item transfer records (kRecWords per active slot)
   uint32_t* cord = nullptr;  // P2G class order of every chunk (sorted positions)
   uint4* ccnt = nullptr;     // class counts of chunks past a segment's first
+  uint8_t* cls8 = nullptr;   // P2G class per particle (state order), from the key pass
   uint32_t* scan_partials = nullptr;
   uint32_t* scan_partials_n = nullptr;  // scan scratch sized for n
   T* pool = nullptr;
@@ -307,6 +308,7 @@ struct Context final : CtxBase {
     dfree(rec);
     dfree(cord);
     dfree(ccnt);
+    dfree(cls8);
     dfree(scan_partials);
     dfree(scan_partials_n);
     dfree(pool);
@@ -419,6 +421,8 @@ struct Context final : CtxBase {
     vals = dalloc<uint32_t>(cap);
     dfree(cord);
     dfree(ccnt);
+    dfree(cls8);
+    cls8 = dalloc<uint8_t>(cap);
     cord = dalloc<uint32_t>(cap);
     ccnt = dalloc<uint4>(cap / kP2GChunk + 2);
     rs.keys_alt = dalloc<uint32_t>(cap);
@@ -529,7 +533,7 @@ struct Context final : CtxBase {
   void enqueue_sort() {
     PState<T> cs = state(cur);
     key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
-        cs, T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko_valid ? ko : nullptr, chg, wcnt, dstat);
+        cs, T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko_valid ? ko : nullptr, chg, wcnt, quad() ? nullptr : cls8, dstat);
     launches += 1;
     if (ko_valid) {
       CKG_CUDA(cudaMemcpyAsync(hcount, &dstat->nchanged, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -594,7 +598,7 @@ struct Context final : CtxBase {
     if (slab) slab_ranges_kernel<<<1, 1, 0, st>>>(plane_start, D, bx_lo, bx_hi, dstat);
     segments_kernel<<<grid_for((n + 3) / 4, 256, 1 << 30), 256, 0, st>>>(skeys, n, seg_begin, seg_end);
     xfer_prep_kernel<T><<<148 * 8, kPrepWarps * 32, 0, st>>>(cs, perm, make_const(0.0), dir, active, seg_begin, seg_end,
-                                                 pool_cap, dstat, rec, cord, ccnt, quad() ? 0 : 1);
+                                                 pool_cap, dstat, rec, cord, ccnt, quad() ? nullptr : cls8);
   }
 
   template <int S>
@@ -859,7 +863,7 @@ struct Context final : CtxBase {
     // sort: crossers counted on the device; <= kSmallSort of them are merged
     // into the stored order, more take the full radix (IF nodes)
     key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
-        state(cur), T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko, chg, wcnt, dstat);
+        state(cur), T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko, chg, wcnt, quad() ? nullptr : cls8, dstat);
     const uint64_t nw = (n + 31) / 32;
     exclusive_scan(wcnt, cpre, nw, scan_partials_n, st);
     compact_changed_kernel<<<grid_for((n + 31) / 32, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);

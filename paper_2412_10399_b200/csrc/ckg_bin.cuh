@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
                                                             uint32_t* __restrict__ core,
                                                             const uint32_t* __restrict__ ko,
                                                             uint32_t* __restrict__ cbits,
-                                                            uint32_t* __restrict__ wcnt, DevStatus* st) {
+                                                            uint32_t* __restrict__ wcnt,
+                                                            uint8_t* __restrict__ cls, DevStatus* st) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool live = i < cur.n;
   bool ok = live, changed = false;
@@ -62,6 +63,17 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
     for (int a = 0; a < 3; ++a) kb[a] = key_axis(x[a], inv_dx, D);
     key = (uint32_t(kb[0]) * uint32_t(D) + uint32_t(kb[1])) * uint32_t(D) + uint32_t(kb[2]);
     keys[i] = key;
+    if (cls) {
+      // P2G sub-octant class (frac(x/dx - 1/4) >= 1/2 per axis), read by
+      // xfer_prep_kernel through the sort permutation
+      uint32_t q = 0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const T sa = sub_rn(mul_rn(x[a], inv_dx), T(0.25));
+        q |= ((sa - dfloor(sa)) >= T(0.5) ? 1u : 0u) << a;
+      }
+      cls[i] = uint8_t(q);
+    }
     if (ko) changed = key != __ldg(ko + i);
     // footprint blocks relative to the key block: lo in {kb-1, kb}, hi in {kb, kb+1}
 #pragma unroll
@@ -92,15 +104,20 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
   if (!ok || (__ffs(peers) - 1) != int(threadIdx.x & 31)) return;
   // inset particles (s in [2, res-2]) have footprint cells in [1, res-1], so
   // every box block lies inside the (res/4 + 2)^3 directory: no bounds checks
-  const int nx = 1 + int(ext & 1u) + int((ext >> 1) & 1u);
-  const int ny = 1 + int((ext >> 2) & 1u) + int((ext >> 3) & 1u);
-  const int nz = 1 + int((ext >> 4) & 1u) + int((ext >> 5) & 1u);
+  // Per axis the box is 1 or 2 blocks: the low extension needs s < 4 kb + 1/4
+  // and the high one s >= 4 kb + 11/4, never both.  So 2 x 2 x 2 predicated
+  // stores cover every box (no data-dependent loop).
+  const bool ex = (ext & 3u) != 0u, ey = ((ext >> 2) & 3u) != 0u, ez = ((ext >> 4) & 3u) != 0u;
   const int64_t DD = int64_t(D) * D;
   uint32_t* c0 = core + (int64_t(kb[0] - int(ext & 1u)) * D + (kb[1] - int((ext >> 2) & 1u))) * D +
                  (kb[2] - int((ext >> 4) & 1u));
-  for (int a = 0; a < nx; ++a)
-    for (int b = 0; b < ny; ++b)
-      for (int k = 0; k < nz; ++k) c0[a * DD + b * D + k] = 1u;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if ((a == 0 || ex) && (b == 0 || ey) && (k == 0 || ez)) c0[a * DD + b * D + k] = 1u;
 }
 
 // Lowest sorted index violating the inset (only runs its loop on failure).

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
     PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c, const int32_t* __restrict__ dir,
     const uint32_t* __restrict__ active, const uint32_t* __restrict__ seg_begin,
     const uint32_t* __restrict__ seg_end, uint32_t cap, const DevStatus* st, uint32_t* __restrict__ rec,
-    uint32_t* __restrict__ cord, uint4* __restrict__ ccnt, int classes) {
+    uint32_t* __restrict__ cord, uint4* __restrict__ ccnt, const uint8_t* __restrict__ cls) {
   constexpr int kG = kP2GChunk / 32;  // 32-particle groups per chunk
   const int lane = threadIdx.x & 31;
   const uint32_t na = min(st->item_hi, cap), lo = st->item_lo;
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
       }
       r[lane] = w;
     }
-    if (!classes || s1 <= s0) {
+    if (!cls || s1 <= s0) {
       if (lane < kRecWords - kRecCls) r[kRecCls + lane] = 0u;
       continue;
     }
@@ -207,11 +207,11 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
       uint32_t qp[2] = {0u, 0u};  // 4-bit class per group (8 = none)
       if (lane < 8) wcnt[wib][lane] = 0u;
       __syncwarp();
-      // pass 1: classes, four groups' loads in flight at a time; per-class
-      // totals accumulated by each class's leader lane
+      // pass 1: classes (from the key pass), four groups' loads in flight at
+      // a time; per-class totals accumulated by each class's leader lane
 #pragma unroll
       for (int g0 = 0; g0 < kG; g0 += 4) {
-        T xs[4][3];
+        uint32_t qs[4];
 #pragma unroll
         for (int g = g0; g < g0 + 4; ++g) {
           const uint32_t j = uint32_t(g) * 32 + lane;
@@ -220,22 +220,11 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
 #pragma unroll
         for (int g = g0; g < g0 + 4; ++g) {
           const uint32_t j = uint32_t(g) * 32 + lane;
-#pragma unroll
-          for (int a = 0; a < 3; ++a)
-            xs[g - g0][a] = j < len ? __ldg(cur.f + uint64_t(kX + a) * cur.stride + src[g]) : T(0);
+          qs[g - g0] = j < len ? uint32_t(__ldg(cls + src[g])) : 8u;
         }
 #pragma unroll
         for (int g = g0; g < g0 + 4; ++g) {
-          const uint32_t j = uint32_t(g) * 32 + lane;
-          uint32_t q = 8u;
-          if (j < len) {
-            q = 0u;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              const T sa = sub_rn(over_dx(xs[g - g0][a], c.dx, c.inv_dx, c.pow2), T(0.25));
-              q |= ((sa - dfloor(sa)) >= T(0.5) ? 1u : 0u) << a;
-            }
-          }
+          const uint32_t q = qs[g - g0];
           qp[g >> 3] |= q << (4 * (g & 7));
           const uint32_t peers = __match_any_sync(0xffffffffu, q);
           if (q < 8u && (peers & lt) == 0u) wcnt[wib][q] += __popc(peers);
