@@ -620,8 +620,19 @@ struct Context final : CtxBase {
                                                                      rec, pool, pool_cap, dstat, step_idx);
       return;
     }
-    g2p_tile_kernel<T, S><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir, rec, pool,
-                                                              pool_cap, dstat, step_idx);
+    // narrowest material-model instance covering the scene
+    int mm = cfg.clamp_singular ? kMClamp : 0;
+    for (int m = 0; m < cfg.n_materials; ++m)
+      mm |= cfg.materials[m].model == kModelFC ? kMFC : cfg.materials[m].model == kModelDP ? kMDP : kMFluid;
+    if (mm == kMFC || mm == 0)
+      g2p_tile_kernel<T, S, 0, kMFC><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir,
+                                                                       rec, pool, pool_cap, dstat, step_idx);
+    else if (mm == kMDP)
+      g2p_tile_kernel<T, S, 0, kMDP><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir,
+                                                                       rec, pool, pool_cap, dstat, step_idx);
+    else
+      g2p_tile_kernel<T, S><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir, rec, pool,
+                                                                pool_cap, dstat, step_idx);
   }
 
   // Kernels enqueue_step launches (status reset, key/footprint, 5 per radix

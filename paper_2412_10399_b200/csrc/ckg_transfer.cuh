@@ -666,6 +666,42 @@ __device__ __forceinline__ void gather_grid(const Axis<T>* ax, T dx, VelFn V, T 
   }
 }
 
+// One velocity component cc of one grid's gather_one contribution
+// (transfer.hpp:465-510), separable: o = {v, grad v row (3), B row (3)}, each
+// already scaled by the dual-grid average's 1/2 (same operations and order as
+// gather_grid).
+template <typename T, typename VelFn>
+__device__ __forceinline__ void gather_grid_cc(const Axis<T>* ax, T dx, VelFn V, int cc, T (&o)[7]) {
+  const T wx0 = ax[0].w0, wx1 = ax[0].w1, wy0 = ax[1].w0, wy1 = ax[1].w1, wz0 = ax[2].w0, wz1 = ax[2].w1;
+  const T gx0 = ax[0].g0, gy0 = ax[1].g0, gz0 = ax[2].g0;
+  const T xx0 = ax[0].xi0, xx1 = ax[0].xi0 + dx, xy0 = ax[1].xi0, xy1 = ax[1].xi0 + dx;
+  const T xz0 = ax[2].xi0, xz1 = ax[2].xi0 + dx;
+  T Y[2], Yg[2], Yz[2], Yx[2], Yzx[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    T Z[2], Zg[2], Zx[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const T a0 = V(s, t, 0, cc), a1 = V(s, t, 1, cc);
+      Z[t] = wz0 * a0 + wz1 * a1;
+      Zg[t] = gz0 * (a0 - a1);
+      Zx[t] = wz0 * xz0 * a0 + wz1 * xz1 * a1;
+    }
+    Y[s] = wy0 * Z[0] + wy1 * Z[1];
+    Yg[s] = gy0 * (Z[0] - Z[1]);
+    Yz[s] = wy0 * Zg[0] + wy1 * Zg[1];
+    Yx[s] = wy0 * xy0 * Z[0] + wy1 * xy1 * Z[1];
+    Yzx[s] = wy0 * Zx[0] + wy1 * Zx[1];
+  }
+  o[0] = T(0.5) * (wx0 * Y[0] + wx1 * Y[1]);
+  o[1] = T(0.5) * (gx0 * (Y[0] - Y[1]));
+  o[2] = T(0.5) * (wx0 * Yg[0] + wx1 * Yg[1]);
+  o[3] = T(0.5) * (wx0 * Yz[0] + wx1 * Yz[1]);
+  o[4] = T(0.5) * (wx0 * xx0 * Y[0] + wx1 * xx1 * Y[1]);
+  o[5] = T(0.5) * (wx0 * Yx[0] + wx1 * Yx[1]);
+  o[6] = T(0.5) * (wx0 * Yzx[0] + wx1 * Yzx[1]);
+}
+
 // gather_one over the 27-node quadratic stencil (transfer.hpp:512-543),
 // sum-factorised; V(s,t,u,c) yields nodal velocity component c.
 template <typename T, typename VelFn>
@@ -705,17 +741,32 @@ __device__ __forceinline__ void gather_quad(const QAxis<T> (&q)[3], T dx, VelFn 
 
 // KQ = 0: compact kernel on the dual grids; 1: quadratic B-spline baseline
 // on grid slot 0 (the particle update below is shared).
-template <typename T, int SCHEME, int KQ = 0>
+// MM: the material models (and SV clamp) the kernel instance handles
+// (kMFC | kMFluid | kMDP | kMClamp); the host picks the narrowest instance
+// covering the scene, so an elastic-only scene carries no return-map or SVD
+// code (and none of its register pressure).
+constexpr int kMFC = 1, kMFluid = 2, kMDP = 4, kMClamp = 8, kMAll = 15;
+template <typename T, int SCHEME, int KQ = 0, int MM = kMAll>
 __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
     g2p_tile_kernel(PState<T> cur, PState<T> nxt, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
                     const T* __restrict__ pool, uint32_t cap, DevStatus* st, int step) {
   __shared__ T vt[kVelVals];
+  // per-thread gather results {v, grad v row, B row} x 3 components: the
+  // -1 grid's partials, then (after the +1 grid) the final values, so no
+  // accumulator is held in registers across the two grids' gathers
+  __shared__ T gst[21][kG2PThreads];
   __shared__ uint32_t s_rec[kRecNbr + 27];
   __shared__ uint32_t s_item;
   __shared__ T wmax[kG2PWarps];
+  // material table in shared memory: indexing the by-value kernel parameter
+  // with the particle's material would copy the whole table to local memory
+  __shared__ MatParam<T> s_mats[kMaxMaterials];
   const int32_t* nbr = reinterpret_cast<const int32_t*>(s_rec + kRecNbr);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int m = 0; m < kMaxMaterials; ++m)
+    if (tid == m) s_mats[m] = c.mats[m];
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const int D = c.D;
   const T dx = c.dx, dt = step_dt(c);
@@ -785,20 +836,12 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
         const uint64_t n = cur.stride;  // field stride (buffer capacity)
         T x = __ldg(cur.f + kX * n + src), y = __ldg(cur.f + (kX + 1) * n + src),
           z = __ldg(cur.f + (kX + 2) * n + src);
-        // pass-through fields, loaded with x so their latency overlaps the gather
         mi = __ldg(cur.mat + src);
-        const T mass = __ldg(cur.f + kMass * n + src), vol0 = __ldg(cur.f + kVol * n + src);
-        T v[3] = {T(0), T(0), T(0)};
-        M3<T> Bn, G;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            Bn.a[a][b] = T(0);
-            G.a[a][b] = T(0);
-          }
+        T* gs = &gst[0][tid];  // gs[k * kG2PThreads]
         if (KQ) {
           // quadratic baseline: 27 nodes of grid slot 0 (transfer.hpp:512-543)
+          T v[3];
+          M3<T> Bn, G;
           const QAxis<T> q[3] = {quad_axis(x, dx, c.inv_dx, c.pow2), quad_axis(y, dx, c.inv_dx, c.pow2),
                                  quad_axis(z, dx, c.inv_dx, c.pow2)};
           const int lx = q[0].base - (4 * bx - 1), ly = q[1].base - (4 * by - 1), lz = q[2].base - (4 * bz - 1);
@@ -821,29 +864,43 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
                 },
                 v, Bn, G);
           }
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) {
+            gs[(cc * 7) * kG2PThreads] = v[cc];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              gs[(cc * 7 + 1 + k) * kG2PThreads] = G.a[cc][k];
+              gs[(cc * 7 + 4 + k) * kG2PThreads] = Bn.a[cc][k];
+            }
+          }
         }
-#if CKG_G2P_DUAL
-        // both grids' stencils from one sincos per axis (axis_pair_dual)
-        const Dual<T> ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
-#endif
 #pragma unroll
         for (int g = 0; g < (KQ ? 0 : 2); ++g) {
-#if CKG_G2P_DUAL
-          const Axis<T>* ax = ds.ax[g];
-#else
           const T kq = g == 0 ? T(-0.25) : T(0.25);
           const Axis<T> ax[3] = {axis_pair(x, dx, c.inv_dx, c.pow2, kq), axis_pair(y, dx, c.inv_dx, c.pow2, kq),
                                  axis_pair(z, dx, c.inv_dx, c.pow2, kq)};
-#endif
           const int lx = ax[0].base - (4 * bx - g), ly = ax[1].base - (4 * by - g), lz = ax[2].base - (4 * bz - g);
           const bool in_tile =
               lx >= 0 && ly >= 0 && lz >= 0 && lx <= kTileN - 2 && ly <= kTileN - 2 && lz <= kTileN - 2;
+          // component by component: -1 grid to the stash, +1 grid added
+          auto emit = [&](int cc, const T (&o)[7]) {
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+              T* p = gs + (cc * 7 + k) * kG2PThreads;
+              *p = g == 0 ? o[k] : *p + o[k];
+            }
+          };
           if (in_tile) {
             const T* vg = vt + g * 3 * kTileNodes + (lx * kTileN + ly) * kTileN + lz;
-            gather_grid<T>(
-                ax, dx,
-                [&](int s, int t, int u, int cc) { return vg[cc * kTileNodes + (s * kTileN + t) * kTileN + u]; },
-                v, Bn, G);
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+              T o[7];
+              gather_grid_cc<T>(
+                  ax, dx,
+                  [&](int s, int t, int u, int c2) { return vg[c2 * kTileNodes + (s * kTileN + t) * kTileN + u]; },
+                  cc, o);
+              emit(cc, o);
+            }
           } else {
             // rare: footprint outside the block tile -> stage the 8 nodes via
             // the directory into the same registers layout
@@ -874,13 +931,30 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
                       V[ss][tt][uu][2] = a2;
                     }
             }
-            gather_grid<T>(ax, dx, [&](int s, int t, int u, int cc) { return V[s][t][u][cc]; }, v, Bn, G);
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+              T o[7];
+              gather_grid_cc<T>(ax, dx, [&](int s, int t, int u, int c2) { return V[s][t][u][c2]; }, cc, o);
+              emit(cc, o);
+            }
+          }
+        }
+        const T mass = __ldg(cur.f + kMass * n + src), vol0 = __ldg(cur.f + kVol * n + src);
+        T v[3];
+        M3<T> Bn, G;
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          v[cc] = gs[(cc * 7) * kG2PThreads];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            G.a[cc][k] = gs[(cc * 7 + 1 + k) * kG2PThreads];
+            Bn.a[cc][k] = gs[(cc * 7 + 4 + k) * kG2PThreads];
           }
         }
         // update_particle_state (transfer.hpp:594-627).  Outputs are stored
         // as soon as they are final so the stress evaluation at the end runs
         // with only F live (register pressure).
-        const MatParam<T>& mp = c.mats[mi < kMaxMaterials ? mi : 0];
+        const MatParam<T>& mp = s_mats[mi < kMaxMaterials ? mi : 0];
         M3<T> L = G;
         if (SCHEME == kSchemeMls) {
           const Dual<T> ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
@@ -890,7 +964,7 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
         }
         {
           M3<T> Bout = SCHEME == kSchemePic ? load_m3(cur, kB, src) : Bn;
-          if (mp.model == kModelFluid && mp.viscosity > T(0) && SCHEME != kSchemePic) {
+          if ((MM & kMFluid) && mp.model == kModelFluid && mp.viscosity > T(0) && SCHEME != kSchemePic) {
             const T f = dexp(-mp.viscosity * dt / (mp.density * dx * dx));
             const T tb = trace(Bout) / T(3);
 #pragma unroll
@@ -921,7 +995,7 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
         T J = __ldg(cur.f + kJ * n + src);
         M3<T> Fout = load_m3(cur, kF, src);
         T t6[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};  // V0 tau of the new state
-        if (mp.model == kModelFluid) {
+        if ((MM & kMFluid) && mp.model == kModelFluid) {
           fluid = true;
           store_m3(nxt, kF, i, Fout);  // fluids carry F unchanged (transfer.hpp:609-617)
           J *= T(1) + dt * trace(L);
@@ -937,8 +1011,8 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
 #pragma unroll
             for (int b = 0; b < 3; ++b) Ld.a[a][b] = (a == b ? T(1) : T(0)) + L.a[a][b] * dt;
           M3<T> Fn = mul(Ld, Fout);
-          if (c.clamp_singular) clamp_singular_values(Fn, c.clamp_floor);
-          if (mp.model == kModelDP) {
+          if ((MM & kMClamp) && c.clamp_singular) clamp_singular_values(Fn, c.clamp_floor);
+          if ((MM & kMDP) && mp.model == kModelDP) {
             const int e = return_map_dp(Fn, mp.dp_alpha, mp.mu, mp.lambda, t6);
             if (e) record_error(st, step, kPhaseG2P, i, 0, e);
 #pragma unroll
@@ -947,7 +1021,7 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
             record_error(st, step, kPhaseG2P, i, 0, kErrFInverted);
           }
           store_m3(nxt, kF, i, Fn);
-          if (mp.model == kModelFC && det(Fn) > T(0)) stress_tau6(Fn, J, vol0, mp, t6);
+          if ((MM & kMFC) && mp.model == kModelFC && det(Fn) > T(0)) stress_tau6(Fn, J, vol0, mp, t6);
         }
         nxt.f[kJ * n + i] = J;
 #pragma unroll
