@@ -133,6 +133,21 @@ __device__ __forceinline__ int64_t nbr_offset(const int32_t* nbr, int g, int gi,
   return int64_t(slot) * kBlockVals + g * 256 + (((gi & 3) << 4) | ((gj & 3) << 2) | (gk & 3));
 }
 
+// ---- cp.async (global -> shared, L1-allocating); a false predicate
+// zero-fills the destination
+__device__ __forceinline__ void cp_async4(void* sm, const void* gm, bool pred) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gm), "r"(pred ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* sm, const void* gm, bool pred) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gm), "r"(pred ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_t(double* sm, const double* gm, bool pred) { cp_async8(sm, gm, pred); }
+__device__ __forceinline__ void cp_async_t(float* sm, const float* gm, bool pred) { cp_async4(sm, gm, pred); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 // ---- per-item records (one per active block, built once per substep by
 // xfer_prep_kernel and read by both transfer kernels with a single 160-byte
 // load instead of the active -> segment -> directory lookup chain)
@@ -756,6 +771,9 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
   // -1 grid's partials, then (after the +1 grid) the final values, so no
   // accumulator is held in registers across the two grids' gathers
   __shared__ T gst[21][kG2PThreads];
+  // per-thread prefetch (cp.async, issued before the gather) of the state the
+  // particle update reads after it: F (9), J, mass, V0
+  __shared__ T pst[12][kG2PThreads];
   __shared__ uint32_t s_rec[kRecNbr + 27];
   __shared__ uint32_t s_item;
   __shared__ T wmax[kG2PWarps];
@@ -834,6 +852,13 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
       if (live) {
         const uint32_t src = __ldg(perm + i);
         const uint64_t n = cur.stride;  // field stride (buffer capacity)
+        T* ps = &pst[0][tid];  // ps[k * kG2PThreads]
+#pragma unroll
+        for (int k = 0; k < 9; ++k) cp_async_t(ps + k * kG2PThreads, cur.f + (kF + k) * n + src, true);
+        cp_async_t(ps + 9 * kG2PThreads, cur.f + kJ * n + src, true);
+        cp_async_t(ps + 10 * kG2PThreads, cur.f + kMass * n + src, true);
+        cp_async_t(ps + 11 * kG2PThreads, cur.f + kVol * n + src, true);
+        cp_async_commit();
         T x = __ldg(cur.f + kX * n + src), y = __ldg(cur.f + (kX + 1) * n + src),
           z = __ldg(cur.f + (kX + 2) * n + src);
         mi = __ldg(cur.mat + src);
@@ -939,7 +964,8 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
             }
           }
         }
-        const T mass = __ldg(cur.f + kMass * n + src), vol0 = __ldg(cur.f + kVol * n + src);
+        cp_async_wait_all();
+        const T mass = ps[10 * kG2PThreads], vol0 = ps[11 * kG2PThreads];
         T v[3];
         M3<T> Bn, G;
 #pragma unroll
@@ -992,8 +1018,12 @@ __global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
           if (!dfinite(s2) || !dfinite(x * x + y * y + z * z)) atomicOr(&st->nonfinite, 1u);
           if (s2 > vmax2) vmax2 = s2;  // NaN never wins (std::max(vm, s2) semantics)
         }
-        T J = __ldg(cur.f + kJ * n + src);
-        M3<T> Fout = load_m3(cur, kF, src);
+        T J = ps[9 * kG2PThreads];
+        M3<T> Fout;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c2 = 0; c2 < 3; ++c2) Fout.a[r][c2] = ps[(3 * r + c2) * kG2PThreads];
         T t6[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};  // V0 tau of the new state
         if ((MM & kMFluid) && mp.model == kModelFluid) {
           fluid = true;
