@@ -289,10 +289,12 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
                     T* __restrict__ pool, uint32_t cap, DevStatus* st, int step) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tiles = reinterpret_cast<T*>(smem_raw);
-  // item records double-buffered: warp 0 claims the next item and loads its
-  // record while the other warps flush the current one
-  __shared__ uint32_t s_recb[2][kRecWords];
-  __shared__ uint32_t s_itemb[2];
+  // Items are claimed two ahead: while item k is processed, warp 0's claim of
+  // item k+2 is in flight (its atomic issued at the start of item k, its
+  // record fetched with cp.async during item k's flush), and item k+1's
+  // record is already in shared memory -- no claim latency between items.
+  __shared__ uint32_t s_recb[3][kRecWords];
+  __shared__ uint32_t s_itemb[3];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   T* wt = tiles + warp * kPTVals;
   for (int e = tid; e < kXferWarps * kPTVals; e += kXferThreads) tiles[e] = T(0);
@@ -301,28 +303,39 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
   const uint32_t lt = lanemask_lt();
   const int D = c.D;
   const T dx = c.dx, dt = step_dt(c);
-  auto claim = [&](int b) {  // warp 0 only
-    uint32_t it = 0;
-    if (lane == 0) it = item0 + atomicAdd(&st->work[0], 1u);
-    it = __shfl_sync(0xffffffffu, it, 0);
+  // warp 0: publish a claimed item and fetch its record (async)
+  auto stage = [&](int b, uint32_t it) {
     if (lane == 0) s_itemb[b] = it;
     if (it < na) {
       const uint32_t* r = rec + uint64_t(it) * kRecWords;
-      s_recb[b][lane] = __ldg(r + lane);
-      if (lane < kRecWords - 32) s_recb[b][32 + lane] = __ldg(r + 32 + lane);
+      cp_async4(&s_recb[b][lane], r + lane, true);
+      if (lane < kRecWords - 32) cp_async4(&s_recb[b][32 + lane], r + 32 + lane, true);
     }
+    cp_async_commit();
   };
-  if (warp == 0) claim(0);
-  for (int buf = 0;; buf ^= 1) {
+  if (warp == 0) {
+    uint32_t a = 0, b = 0;
+    if (lane == 0) {
+      a = item0 + atomicAdd(&st->work[0], 1u);
+      b = item0 + atomicAdd(&st->work[0], 1u);
+    }
+    stage(0, __shfl_sync(0xffffffffu, a, 0));
+    stage(1, __shfl_sync(0xffffffffu, b, 0));
+  }
+  for (int k = 0;; ++k) {
+    const int buf = k % 3;
+    if (warp == 0) asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // record k (and k+1 unless newest)
     __syncthreads();
     const uint32_t item = s_itemb[buf];
     if (item >= na) break;
+    uint32_t pend = 0;  // claim of item k+2
+    if (tid == 0) pend = item0 + atomicAdd(&st->work[0], 1u);
     const uint32_t* s_rec = s_recb[buf];
     const int32_t* nbr = reinterpret_cast<const int32_t*>(s_rec + kRecNbr);
     const uint32_t key = s_rec[kRecKey];
     const uint32_t s0 = s_rec[kRecS0], s1 = s_rec[kRecS1];
     if (s1 <= s0) {
-      if (warp == 0) claim(buf ^ 1);
+      if (warp == 0) stage((k + 2) % 3, __shfl_sync(0xffffffffu, pend, 0));
       continue;
     }
     int bx, by, bz;
@@ -525,7 +538,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
       }  // rounds of this warp's class list
     }
     __syncthreads();
-    if (warp == 0) claim(buf ^ 1);
+    if (warp == 0) stage((k + 2) % 3, __shfl_sync(0xffffffffu, pend, 0));
     // ---- flush: sum the warp tiles, one REDG per non-zero node value.
     // Slot 0: all class tiles share origin 4b (5^3).  Slot 1: the 6^3 halo
     // from 4b - 1; warp w's tile covers offsets [1 - c, 5 - c] per axis.
