@@ -68,52 +68,28 @@ constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full 
 // CTA, which leaves L1 room for the particle gathers and register spills.
 constexpr int kPT = 5;
 constexpr int kPTNodes = kPT * kPT * kPT;  // 125
-constexpr int kPTVals = 2 * 4 * kPTNodes;  // 1000
-// Tile layout [grid][node][m, px, py, pz]: one node's four values are
-// contiguous, so a node update is two 16-byte shared loads/stores (FP64).
-#ifndef CKG_P2G_NODEMAJOR
-#define CKG_P2G_NODEMAJOR 0
+// Tile layout [grid][value][node] (value stride = the grid tile's node
+// count).  The +1 grid tile is either the 6^3 block halo from 4b - 1, common
+// to all warps (CKG_P2G_T1FULL = 1: uniform flush), or warp w's 5^3 class
+// window from 4b - c_w (0: 20 KB less shared memory per CTA).
+#ifndef CKG_P2G_T1FULL
+#define CKG_P2G_T1FULL 1
 #endif
-constexpr int kNS = CKG_P2G_NODEMAJOR ? 4 : 1;         // node stride in a tile grid
-constexpr int kVS = CKG_P2G_NODEMAJOR ? 1 : kPTNodes;  // value stride
-__device__ __forceinline__ void tile_add4(double* p, const double (&o)[4]) {
-  if (CKG_P2G_NODEMAJOR) {
-    double2* q = reinterpret_cast<double2*>(p);
-    double2 a = q[0], b = q[1];
-    a.x += o[0];
-    a.y += o[1];
-    b.x += o[2];
-    b.y += o[3];
-    q[0] = a;
-    q[1] = b;
-  } else {
-    // all four loads issued before the first add
-    const double a0 = p[0], a1 = p[kVS], a2 = p[2 * kVS], a3 = p[3 * kVS];
-    p[0] = a0 + o[0];
-    p[kVS] = a1 + o[1];
-    p[2 * kVS] = a2 + o[2];
-    p[3 * kVS] = a3 + o[3];
-  }
-}
-__device__ __forceinline__ void tile_add4(float* p, const float (&o)[4]) {
-  if (CKG_P2G_NODEMAJOR) {
-    float4* q = reinterpret_cast<float4*>(p);
-    float4 a = *q;
-    a.x += o[0];
-    a.y += o[1];
-    a.z += o[2];
-    a.w += o[3];
-    *q = a;
-  } else {
-    p[0] += o[0];
-    p[kVS] += o[1];
-    p[2 * kVS] += o[2];
-    p[3 * kVS] += o[3];
-  }
+constexpr int kT1 = CKG_P2G_T1FULL ? kTileN : kPT;
+constexpr int kT1Nodes = kT1 * kT1 * kT1;
+constexpr int kWarpVals = 4 * kPTNodes + 4 * kT1Nodes;
+template <typename T>
+__device__ __forceinline__ void tile_add4(T* p, const T (&o)[4], int vs) {
+  // all four loads issued before the first add
+  const T a0 = p[0], a1 = p[vs], a2 = p[2 * vs], a3 = p[3 * vs];
+  p[0] = a0 + o[0];
+  p[vs] = a1 + o[1];
+  p[2 * vs] = a2 + o[2];
+  p[3 * vs] = a3 + o[3];
 }
 template <typename T>
 constexpr size_t p2g_smem_bytes() {
-  return size_t(kXferWarps) * kPTVals * sizeof(T);
+  return size_t(kXferWarps) * kWarpVals * sizeof(T);
 }
 
 __device__ __forceinline__ void decode_key(uint32_t key, int D, int& bx, int& by, int& bz) {
@@ -296,8 +272,8 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
   __shared__ uint32_t s_recb[3][kRecWords];
   __shared__ uint32_t s_itemb[3];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  T* wt = tiles + warp * kPTVals;
-  for (int e = tid; e < kXferWarps * kPTVals; e += kXferThreads) tiles[e] = T(0);
+  T* wt = tiles + warp * kWarpVals;
+  for (int e = tid; e < kXferWarps * kWarpVals; e += kXferThreads) tiles[e] = T(0);
   const int cx = warp & 1, cy = (warp >> 1) & 1, cz = (warp >> 2) & 1;  // class bits
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const uint32_t lt = lanemask_lt();
@@ -431,11 +407,14 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
           ax[1] = axis_pair(y, dx, c.inv_dx, c.pow2, T(0.25));
           ax[2] = axis_pair(z, dx, c.inv_dx, c.pow2, T(0.25));
         }
-        const int lx = ax[0].base - (4 * bx - (g ? cx : 0)), ly = ax[1].base - (4 * by - (g ? cy : 0)),
-                  lz = ax[2].base - (4 * bz - (g ? cz : 0));
+        // tile edge and origin shift of this grid (see kT1)
+        const int E = g ? kT1 : kPT, VS = g ? kT1Nodes : kPTNodes;
+        const int shx = g ? (CKG_P2G_T1FULL ? 1 : cx) : 0, shy = g ? (CKG_P2G_T1FULL ? 1 : cy) : 0,
+                  shz = g ? (CKG_P2G_T1FULL ? 1 : cz) : 0;
+        const int lx = ax[0].base - (4 * bx - shx), ly = ax[1].base - (4 * by - shy), lz = ax[2].base - (4 * bz - shz);
         const bool in_tile =
-            valid && lx >= 0 && ly >= 0 && lz >= 0 && lx <= kPT - 2 && ly <= kPT - 2 && lz <= kPT - 2;
-        const uint32_t cell = in_tile ? uint32_t((lx * kPT + ly) * kPT + lz) : (1024u + lane);
+            valid && lx >= 0 && ly >= 0 && lz >= 0 && lx <= E - 2 && ly <= E - 2 && lz <= E - 2;
+        const uint32_t cell = in_tile ? uint32_t((lx * E + ly) * E + lz) : (1024u + lane);
         const uint32_t peers = __match_any_sync(0xffffffffu, cell);
         const uint32_t rank = __popc(peers & lt);
         const uint32_t maxrank = __reduce_max_sync(0xffffffffu, rank);
@@ -481,7 +460,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
             o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
           }
         };
-        T* p0 = wt + g * 4 * kPTNodes + ((lx * kPT + ly) * kPT + lz) * kNS;
+        T* p0 = wt + g * 4 * kPTNodes + (lx * E + ly) * E + lz;
         if (maxrank == 0) {
           // fast path: every lane owns a distinct base cell in this warp, so
           // at a fixed node offset all lanes write distinct nodes
@@ -494,7 +473,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
                 for (int u = 0; u < 2; ++u) {
                   T o[4];
                   contrib(s, t, u, o);
-                  tile_add4(p0 + ((s * kPT + t) * kPT + u) * kNS, o);
+                  tile_add4(p0 + (s * E + t) * E + u, o, VS);
                   // node (s,t,u) of one lane can be node (0,0,0) of its
                   // neighbour: order the read-modify-writes across lanes
                   __syncwarp(tmask);
@@ -507,9 +486,9 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
             const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
             T o[4];
             contrib(s, t, u, o);
-            T* p = p0 + ((s * kPT + t) * kPT + u) * kNS;
+            T* p = p0 + (s * E + t) * E + u;
             for (uint32_t layer = 0; layer <= maxrank; ++layer) {
-              if (in_tile && rank == layer) tile_add4(p, o);
+              if (in_tile && rank == layer) tile_add4(p, o, VS);
               __syncwarp();
             }
           }
@@ -541,20 +520,21 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
     if (warp == 0) stage((k + 2) % 3, __shfl_sync(0xffffffffu, pend, 0));
     // ---- flush: sum the warp tiles, one REDG per non-zero node value.
     // Slot 0: all class tiles share origin 4b (5^3).  Slot 1: the 6^3 halo
-    // from 4b - 1; warp w's tile covers offsets [1 - c, 5 - c] per axis.
+    // from 4b - 1 (T1FULL: every warp's tile is that halo; else warp w's
+    // 5^3 window covers offsets [1 - c, 5 - c] per axis).
     for (int e = tid; e < 4 * kPTNodes + 4 * kTileNodes; e += kXferThreads) {
       T sum = T(0);
       int g, v, i, j, k;
       if (e < 4 * kPTNodes) {
         g = 0;
-        v = CKG_P2G_NODEMAJOR ? e % 4 : e / kPTNodes;
-        const int node = CKG_P2G_NODEMAJOR ? e / 4 : e % kPTNodes;
+        v = e / kPTNodes;
+        const int node = e % kPTNodes;
         i = node / (kPT * kPT);
         j = (node / kPT) % kPT;
         k = node % kPT;
 #pragma unroll
         for (int w = 0; w < kXferWarps; ++w) {
-          T* q = tiles + w * kPTVals + e;
+          T* q = tiles + w * kWarpVals + e;
           sum += *q;
           *q = T(0);
         }
@@ -568,11 +548,17 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
         k = node % kTileN;
 #pragma unroll
         for (int w = 0; w < kXferWarps; ++w) {
-          const int li = i - 1 + (w & 1), lj = j - 1 + ((w >> 1) & 1), lk = k - 1 + ((w >> 2) & 1);
-          if (li >= 0 && lj >= 0 && lk >= 0 && li < kPT && lj < kPT && lk < kPT) {
-            T* q = tiles + w * kPTVals + 4 * kPTNodes + v * kVS + ((li * kPT + lj) * kPT + lk) * kNS;
+          if (CKG_P2G_T1FULL) {
+            T* q = tiles + w * kWarpVals + e;
             sum += *q;
             *q = T(0);
+          } else {
+            const int li = i - 1 + (w & 1), lj = j - 1 + ((w >> 1) & 1), lk = k - 1 + ((w >> 2) & 1);
+            if (li >= 0 && lj >= 0 && lk >= 0 && li < kPT && lj < kPT && lk < kPT) {
+              T* q = tiles + w * kWarpVals + 4 * kPTNodes + v * kT1Nodes + (li * kPT + lj) * kPT + lk;
+              sum += *q;
+              *q = T(0);
+            }
           }
         }
       }
