@@ -27,6 +27,7 @@
 #include "ckg_quad.cuh"
 
 namespace ckg {
+constexpr uint32_t kHostSmallSort = 2048;  // host-path crosser count sorted by one CTA
 
 struct CudaError {
   cudaError_t e;
@@ -553,11 +554,29 @@ struct Context final : CtxBase {
       }
       if (uint64_t(nc) * 8 <= n) {
         uint32_t *sck = nullptr, *sci = nullptr;
-        radix_sort_pairs(ck, ci, nc, key_bits, rs, st, &sck, &sci, ci);
+        if (nc <= kHostSmallSort) {
+          // a few crossers: one-CTA bitonic sort (one launch instead of the
+          // radix passes)
+          static bool attr = false;
+          if (!attr) {
+            CKG_CUDA(cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kSmallSort * sizeof(unsigned long long))));
+            attr = true;
+          }
+          uint32_t m = 1;
+          while (m < nc) m <<= 1;
+          sck = rs.keys_alt;
+          sci = rs.vals_alt;
+          small_sort_kernel<<<1, 1024, m * sizeof(unsigned long long), st>>>(ck, ci, &dstat->nchanged, sck, sci);
+          launches += 1;
+        } else {
+          radix_sort_pairs(ck, ci, nc, key_bits, rs, st, &sck, &sci, ci);
+          launches += uint64_t((key_bits + kRadixBits - 1) / kRadixBits) * 5;
+        }
         const uint64_t tiles = (n + kMergeTile - 1) / kMergeTile;
         merge_bounds_kernel<<<grid_for(tiles, 256, 1 << 30), 256, 0, st>>>(keys, chg, n, sck, sci, nc, nullptr,
                                                                            wcnt);
-        merge_unchanged_kernel<<<unsigned(tiles), kMergeTile, 0, st>>>(keys, chg, cpre, n, sck, sci, nc, nullptr,
+        merge_unchanged_kernel<<<unsigned((n + 256 * kMergePer - 1) / (256 * kMergePer)), 256, 0, st>>>(keys, chg, cpre, n, sck, sci, nc, nullptr,
                                                                        wcnt, perm_buf, skeys_tmp);
         // seg_begin/end still hold the previous substep's runs of ko unless
         // the stored order was rebuilt since (slab migration)
@@ -565,7 +584,7 @@ struct Context final : CtxBase {
         merge_changed_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, st>>>(
             ko, chg, cpre, n, sck, sci, nc, nullptr, segs ? seg_begin : nullptr, segs ? seg_end : nullptr, perm_buf,
             skeys_tmp);
-        launches += uint64_t((key_bits + kRadixBits - 1) / kRadixBits) * 5 + 3;
+        launches += 3;
         std::swap(ko, skeys_tmp);
         perm = perm_buf;
         skeys = ko;
@@ -891,7 +910,7 @@ struct Context final : CtxBase {
     // crossers sorted into (sck, sci): merge them with the stored order
     auto merge = [&](cudaStream_t s2, uint32_t* sck, uint32_t* sci, uint32_t max_nc) {
       merge_bounds_kernel<<<grid_for(tiles, 256, 1 << 30), 256, 0, s2>>>(keys, chg, n, sck, sci, 0u, dnc, wcnt);
-      merge_unchanged_kernel<<<unsigned(tiles), kMergeTile, 0, s2>>>(keys, chg, cpre, n, sck, sci, 0u, dnc, wcnt,
+      merge_unchanged_kernel<<<unsigned((n + 256 * kMergePer - 1) / (256 * kMergePer)), 256, 0, s2>>>(keys, chg, cpre, n, sck, sci, 0u, dnc, wcnt,
                                                                       perm_buf, skeys_tmp);
       merge_changed_kernel<<<grid_for(max_nc, 256, 1 << 30), 256, 0, s2>>>(ko, chg, cpre, n, sck, sci, 0u, dnc,
                                                                            seg_begin, seg_end, perm_buf, skeys_tmp);

@@ -97,32 +97,48 @@ __global__ void __launch_bounds__(256) merge_bounds_kernel(const uint32_t* __res
   tile_lo[t] = first < n ? changed_lower(ck, ci, 0, nc, keys[first], base) : 0u;
 }
 
-__global__ void __launch_bounds__(kMergeTile) merge_unchanged_kernel(const uint32_t* __restrict__ keys,
-                                                                     const uint32_t* __restrict__ cbits,
-                                                                     const uint32_t* __restrict__ woff, uint64_t n,
-                                                                     const uint32_t* __restrict__ ck,
-                                                                     const uint32_t* __restrict__ ci, uint32_t nc,
-                                                                     const uint32_t* __restrict__ ncp,
-                                                                     const uint32_t* __restrict__ tile_lo,
-                                                                     uint32_t* __restrict__ perm,
-                                                                     uint32_t* __restrict__ skeys) {
-  const uint64_t i = uint64_t(blockIdx.x) * kMergeTile + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  if (i >= n) return;
+// Four consecutive stored positions per thread (one 16-byte key load; the
+// walk over the changed list continues from the previous position's bound,
+// since a thread's unchanged entries are in increasing (key, index) order).
+constexpr int kMergePer = 4;
+__global__ void __launch_bounds__(256) merge_unchanged_kernel(const uint32_t* __restrict__ keys,
+                                                              const uint32_t* __restrict__ cbits,
+                                                              const uint32_t* __restrict__ woff, uint64_t n,
+                                                              const uint32_t* __restrict__ ck,
+                                                              const uint32_t* __restrict__ ci, uint32_t nc,
+                                                              const uint32_t* __restrict__ ncp,
+                                                              const uint32_t* __restrict__ tile_lo,
+                                                              uint32_t* __restrict__ perm,
+                                                              uint32_t* __restrict__ skeys) {
+  const uint64_t i0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kMergePer;
+  if (i0 >= n) return;
   if (ncp) nc = *ncp;
-  const uint32_t b = __ldg(cbits + (i >> 5));
-  if ((b >> lane) & 1u) return;
-  const uint32_t k = keys[i];
-  uint32_t lo = __ldg(tile_lo + blockIdx.x);
-  int steps = 0;
-  while (lo < nc && steps < 8 && changed_entry_before(ck, ci, lo, k, i)) {
-    ++lo;
-    ++steps;
+  const uint32_t b = __ldg(cbits + (i0 >> 5));
+  const uint32_t wo = __ldg(woff + (i0 >> 5));
+  uint32_t k[kMergePer];
+  if (i0 + kMergePer <= n) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(keys) + (i0 / kMergePer));
+    k[0] = v.x, k[1] = v.y, k[2] = v.z, k[3] = v.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < kMergePer; ++e) k[e] = i0 + e < n ? keys[i0 + e] : 0u;
   }
-  if (steps == 8) lo = changed_lower(ck, ci, lo, nc, k, i);
-  const uint64_t pos = (i - (__ldg(woff + (i >> 5)) + uint32_t(__popc(b & ((1u << lane) - 1u))))) + lo;
-  perm[pos] = uint32_t(i);
-  skeys[pos] = k;
+  uint32_t lo = __ldg(tile_lo + (i0 / kMergeTile));
+  const int sh = int(i0 & 31);
+#pragma unroll
+  for (int e = 0; e < kMergePer; ++e) {
+    const uint64_t i = i0 + e;
+    if (i >= n || ((b >> (sh + e)) & 1u)) continue;
+    int steps = 0;
+    while (lo < nc && steps < 8 && changed_entry_before(ck, ci, lo, k[e], i)) {
+      ++lo;
+      ++steps;
+    }
+    if (steps == 8) lo = changed_lower(ck, ci, lo, nc, k[e], i);
+    const uint64_t pos = (i - (wo + uint32_t(__popc(b & ((1u << (sh + e)) - 1u))))) + lo;
+    perm[pos] = uint32_t(i);
+    skeys[pos] = k[e];
+  }
 }
 
 // Changed particles: count unchanged entries ordered before (k, j) using the
