@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--e2e-chains", type=int, default=2,
                     help="independent host-resident simulations stepped concurrently (one host thread each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-single", action="store_true",
+                    help="skip the secondary FP32 (Simulation<float>) device-rate figure")
     ap.add_argument("--cpu-cells", type=int, default=64, help="CPU baseline sample block edge (64 -> 2.1M p)")
     ap.add_argument("--cpu-steps", type=int, default=3)
     return ap.parse_args()
@@ -143,6 +145,38 @@ def measured_peak_hbm():
             return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def single_precision_rate(args, cfg, local):
+    """The same scene and substep in the reference's single-precision mode
+    (`ckmpm run --precision single`, tools/ckmpm_main.cpp:122): device time of
+    K substeps after W warm-up ones, CUDA events on the library stream."""
+    from paper_2412_10399_b200._lib import lib
+    from paper_2412_10399_b200.api import Simulation
+
+    L = lib()
+    host = seed_particles(cfg, 4)
+    sim = Simulation(cfg, precision=4, device=local, particles=host)
+    ctx = sim._ctx
+    dt = sim.cfl_dt(1.0)
+    o = abi.StepOut()
+    for _ in range(args.warmup):
+        assert L.ckg_step(ctx, dt, C.byref(o)) == 0
+    acc = [0.0] * 6
+    L.ckg_timer_mark(ctx, 0)
+    for _ in range(args.steps):
+        assert L.ckg_step(ctx, dt, C.byref(o)) == 0
+        for k in range(6):
+            acc[k] += o.phase_ms[k] / args.steps
+    L.ckg_timer_mark(ctx, 1)
+    el = C.c_double()
+    L.ckg_timer_elapsed(ctx, 0, 1, C.byref(el))
+    sim.close()
+    n = len(host)
+    return {"value": n * args.steps / (el.value * 1e-3), "unit": UNIT, "dtype": "f32",
+            "ms_per_step": el.value / args.steps, "phase_ms": dict(zip(abi.PHASE_NAMES, acc)),
+            "parity": "keys/order bit-exact and state <= 1e-5 vs the reference's Simulation<float> "
+                      "(tests/test_gpu_parity.py::test_float_mode_vs_reference_float)"}
 
 
 def cpu_baseline(args, threads):
@@ -429,6 +463,13 @@ def main():
         except Exception:
             traffic = None
 
+    single = None
+    if ws == 1 and prec == 8 and not args.no_single:
+        sim.close()
+        try:
+            single = single_precision_rate(args, cfg, local)
+        except Exception as e:  # reported, never silently substituted
+            single = {"value": None, "error": str(e)}
     if rank == 0:
         cb = None
         if not args.no_cpu_baseline and ws == 1:
@@ -466,9 +507,11 @@ def main():
             "gpu_launches": total_launch,
             "launches_per_step": launches_per_step,
             "clocks": clocks,
+            "single_precision": single,
         }
         print(json.dumps(line), flush=True)
-    sim.close()
+    if single is None:
+        sim.close()
     if dist is not None:
         dist.destroy_process_group()
 
