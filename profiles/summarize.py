@@ -47,9 +47,20 @@ def launches(path, out):
         except ValueError:
             continue
         seq.append((r[ki].split("(")[0].replace("void ", ""), v))
-    starts = [i for i, (n, _) in enumerate(seq) if "status_reset" in n]
-    # the last complete substep before the e2e loop: second-to-last reset pair
-    s, e = starts[-3], starts[-2]
+    starts = [i for i, (n, _) in enumerate(seq) if "status_reset" in n] + [len(seq)]
+    # steady-state substeps of the device-timed loop: windows between status
+    # resets holding a P2G launch and no upload / initial-stress / full-sort
+    # kernels; the median-length one is reported
+    wins = []
+    for a, b in zip(starts[:-1], starts[1:]):
+        names = [n for n, _ in seq[a:b]]
+        if not any("p2g" in n for n in names):
+            continue
+        if any(("aos" in n) or ("stress_kernel" in n) or ("iota" in n) for n in names):
+            continue
+        wins.append((sum(v for _, v in seq[a:b]), a, b))
+    wins.sort()
+    _, s, e = wins[len(wins) // 2]
     step = seq[s:e]
     tot = sum(v for _, v in step)
     with open(out, "w") as f:
