@@ -43,7 +43,7 @@ constexpr int kXferWarps = kXferThreads / 32;
 #define CKG_G2P_THREADS 128
 #endif
 #ifndef CKG_G2P_MINB
-#define CKG_G2P_MINB 4
+#define CKG_G2P_MINB 3
 #endif
 #ifndef CKG_G2P_DUAL
 #define CKG_G2P_DUAL 0
