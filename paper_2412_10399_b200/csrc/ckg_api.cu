@@ -342,12 +342,12 @@ struct Context final : CtxBase {
   // Smallest shared-memory carveout holding two CTAs of a P2G kernel: the
   // rest of the 256 KB stays L1 for the class-order particle gathers and spills.
   template <typename K>
-  void set_two_cta_carveout(K* kernel, size_t smem) {
+  void set_two_cta_carveout(K* kernel, size_t smem, int ctas = 2) {
     cudaFuncAttributes fa{};
     CKG_CUDA(cudaFuncGetAttributes(&fa, kernel));
     int smem_sm = 0;
     CKG_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
-    const size_t need = 2 * (smem + fa.sharedSizeBytes + 1024);  // + 1 KB reserved per CTA
+    const size_t need = size_t(ctas) * (smem + fa.sharedSizeBytes + 1024);  // + 1 KB reserved per CTA
     // supported sm_100 carveouts (KB); the driver rounds the percentage up to
     // the next one, so ask for floor(target) of the smallest that fits
     size_t target = size_t(smem_sm);
@@ -366,7 +366,7 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
     const size_t smem = p2g_smem_bytes<T>();
     CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    set_two_cta_carveout(p2g_tile_kernel<T, S>, smem);
+    set_two_cta_carveout(p2g_tile_kernel<T, S>, smem, sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB);
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kXferThreads, smem));
     if (cfg.scheme == S) p2g_ctas = std::max(1, per) * nsm;
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S>, kG2PThreads, 0));

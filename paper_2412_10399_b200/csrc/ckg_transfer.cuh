@@ -57,6 +57,12 @@ constexpr int kXferWarps = kXferThreads / 32;
 #ifndef CKG_P2G_MINB
 #define CKG_P2G_MINB 2
 #endif
+#ifndef CKG_P2G_MINB_F32
+#define CKG_P2G_MINB_F32 3
+#endif
+#ifndef CKG_G2P_MINB_F32
+#define CKG_G2P_MINB_F32 4
+#endif
 constexpr int kG2PThreads = CKG_G2P_THREADS;
 constexpr int kG2PWarps = kG2PThreads / 32;
 constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full lattice block)
@@ -258,7 +264,7 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
 }
 
 template <typename T, int SCHEME>
-__global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
+__global__ void __launch_bounds__(kXferThreads, sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB)
     p2g_tile_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
                     const uint32_t* __restrict__ cord, const uint4* __restrict__ ccnt,
@@ -761,7 +767,7 @@ __device__ __forceinline__ void gather_quad(const QAxis<T> (&q)[3], T dx, VelFn 
 // code (and none of its register pressure).
 constexpr int kMFC = 1, kMFluid = 2, kMDP = 4, kMClamp = 8, kMAll = 15;
 template <typename T, int SCHEME, int KQ = 0, int MM = kMAll>
-__global__ void __launch_bounds__(kG2PThreads, CKG_G2P_MINB)
+__global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32 : CKG_G2P_MINB)
     g2p_tile_kernel(PState<T> cur, PState<T> nxt, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
                     const T* __restrict__ pool, uint32_t cap, DevStatus* st, int step) {
