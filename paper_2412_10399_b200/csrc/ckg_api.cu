@@ -533,7 +533,7 @@ struct Context final : CtxBase {
   // read-back of the changed count picks identity / merge / full radix.
   void enqueue_sort() {
     PState<T> cs = state(cur);
-    key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
+    key_footprint_kernel<T><<<grid_for((n + kKeyPer - 1) / kKeyPer, 256, 1 << 30), 256, 0, st>>>(
         cs, T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko_valid ? ko : nullptr, chg, wcnt, quad() ? nullptr : cls8, dstat);
     launches += 1;
     if (ko_valid) {
@@ -892,7 +892,7 @@ struct Context final : CtxBase {
     status_reset_kernel<<<1, 32, 0, st>>>(dstat, 1);
     // sort: crossers counted on the device; <= kSmallSort of them are merged
     // into the stored order, more take the full radix (IF nodes)
-    key_footprint_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(
+    key_footprint_kernel<T><<<grid_for((n + kKeyPer - 1) / kKeyPer, 256, 1 << 30), 256, 0, st>>>(
         state(cur), T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko, chg, wcnt, quad() ? nullptr : cls8, dstat);
     const uint64_t nw = (n + 31) / 32;
     exclusive_scan(wcnt, cpre, nw, scan_partials_n, st);

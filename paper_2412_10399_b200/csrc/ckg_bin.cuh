@@ -42,23 +42,18 @@ __device__ __forceinline__ bool inset_ok(T x, T inv_dx, int res) {
   return s >= T(2) && s <= T(res - 2);
 }
 
+// One particle of the key pass (all 32 lanes of the warp call it for 32
+// consecutive particles; x and the stored key are loaded by the caller).
 template <typename T>
-__global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv_dx, int res, int D, int quad,
-                                                            uint32_t* __restrict__ keys,
-                                                            uint32_t* __restrict__ core,
-                                                            const uint32_t* __restrict__ ko,
-                                                            uint32_t* __restrict__ cbits,
-                                                            uint32_t* __restrict__ wcnt,
-                                                            uint8_t* __restrict__ cls, DevStatus* st) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool live = i < cur.n;
+__device__ __forceinline__ void key_footprint_one(uint64_t i, bool live, const T (&x)[3], uint32_t kov, uint64_t n,
+                                                  T inv_dx, int res, int D, int quad, uint32_t* __restrict__ keys,
+                                                  uint32_t* __restrict__ core, const uint32_t* __restrict__ ko,
+                                                  uint32_t* __restrict__ cbits, uint32_t* __restrict__ wcnt,
+                                                  uint8_t* __restrict__ cls, DevStatus* st) {
   bool ok = live, changed = false;
   uint32_t key = 0xffffffffu, ext = 0;
   int kb[3] = {0, 0, 0};
   if (live) {
-    T x[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) x[a] = __ldg(cur.f + uint64_t(kX + a) * cur.stride + i);
 #pragma unroll
     for (int a = 0; a < 3; ++a) kb[a] = key_axis(x[a], inv_dx, D);
     key = (uint32_t(kb[0]) * uint32_t(D) + uint32_t(kb[1])) * uint32_t(D) + uint32_t(kb[2]);
@@ -74,7 +69,7 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
       }
       cls[i] = uint8_t(q);
     }
-    if (ko) changed = key != __ldg(ko + i);
+    if (ko) changed = key != kov;
     // footprint blocks relative to the key block: lo in {kb-1, kb}, hi in {kb, kb+1}
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -91,7 +86,7 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
     // one word of changed flags and its count per warp (ckg_isort.cuh ranks
     // from these instead of a per-particle scan)
     const uint32_t cb = __ballot_sync(0xffffffffu, changed);
-    if ((threadIdx.x & 31) == 0 && i < cur.n) {
+    if ((threadIdx.x & 31) == 0 && i < n) {
       cbits[i >> 5] = cb;
       wcnt[i >> 5] = uint32_t(__popc(cb));
       if (cb) atomicAdd(&st->nchanged, uint32_t(__popc(cb)));
@@ -118,6 +113,40 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
 #pragma unroll
       for (int k = 0; k < 2; ++k)
         if ((a == 0 || ex) && (b == 0 || ey) && (k == 0 || ez)) c0[a * DD + b * D + k] = 1u;
+}
+
+// K1 key pass: block key (simulation.hpp:255-266), footprint boxes + inset
+// (grid.hpp:121-137), changed words, P2G class byte.  Each warp covers
+// kKeyPer x 32 consecutive particles with all their position / stored-key
+// loads issued up front (memory-level parallelism: the pass is latency-bound
+// at one particle per thread).
+constexpr int kKeyPer = 2;
+template <typename T>
+__global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv_dx, int res, int D, int quad,
+                                                            uint32_t* __restrict__ keys,
+                                                            uint32_t* __restrict__ core,
+                                                            const uint32_t* __restrict__ ko,
+                                                            uint32_t* __restrict__ cbits,
+                                                            uint32_t* __restrict__ wcnt,
+                                                            uint8_t* __restrict__ cls, DevStatus* st) {
+  const uint64_t gt = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t base = (gt >> 5) * (32 * kKeyPer) + (gt & 31);
+  T x[kKeyPer][3];
+  uint32_t kov[kKeyPer];
+#pragma unroll
+  for (int r = 0; r < kKeyPer; ++r) {
+    const uint64_t i = base + 32 * r;
+    const bool live = i < cur.n;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) x[r][a] = live ? __ldg(cur.f + uint64_t(kX + a) * cur.stride + i) : T(0);
+    kov[r] = (live && ko) ? __ldg(ko + i) : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < kKeyPer; ++r) {
+    const uint64_t i = base + 32 * r;
+    key_footprint_one<T>(i, i < cur.n, x[r], kov[r], cur.n, inv_dx, res, D, quad, keys, core, ko, cbits, wcnt, cls,
+                         st);
+  }
 }
 
 // Lowest sorted index violating the inset (only runs its loop on failure).
