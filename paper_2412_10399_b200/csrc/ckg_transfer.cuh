@@ -848,6 +848,12 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
       }
     }
     __syncthreads();
+    // software pipeline over this thread's particles of the block: the next
+    // particle's index is loaded when one starts, its position during the
+    // gather (the perm -> position chain is off the critical path)
+    uint32_t src_nx = s0 + tid < s1 ? __ldg(perm + s0 + tid) : 0u;
+    T xn = T(0), yn = T(0), zn = T(0);
+    bool have_x = false;
     for (uint32_t cb = s0; cb < s1; cb += kG2PThreads) {
       const uint32_t i = cb + tid;
       const bool live = i < s1;
@@ -855,7 +861,9 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
       T Jout = T(1);
       uint32_t mi = 0;
       if (live) {
-        const uint32_t src = __ldg(perm + i);
+        const uint32_t src = src_nx;
+        const bool has_next = i + kG2PThreads < s1;
+        if (has_next) src_nx = __ldg(perm + i + kG2PThreads);
         const uint64_t n = cur.stride;  // field stride (buffer capacity)
         T* ps = &pst[0][tid];  // ps[k * kG2PThreads]
 #pragma unroll
@@ -864,8 +872,16 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
         cp_async_t(ps + 10 * kG2PThreads, cur.f + kMass * n + src, true);
         cp_async_t(ps + 11 * kG2PThreads, cur.f + kVol * n + src, true);
         cp_async_commit();
-        T x = __ldg(cur.f + kX * n + src), y = __ldg(cur.f + (kX + 1) * n + src),
+        T x, y, z;
+        if (have_x) {
+          x = xn;
+          y = yn;
+          z = zn;
+        } else {
+          x = __ldg(cur.f + kX * n + src);
+          y = __ldg(cur.f + (kX + 1) * n + src);
           z = __ldg(cur.f + (kX + 2) * n + src);
+        }
         mi = __ldg(cur.mat + src);
         T* gs = &gst[0][tid];  // gs[k * kG2PThreads]
         if (KQ) {
@@ -968,6 +984,12 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
               emit(cc, o);
             }
           }
+        }
+        have_x = has_next;
+        if (has_next) {
+          xn = __ldg(cur.f + kX * n + src_nx);
+          yn = __ldg(cur.f + (kX + 1) * n + src_nx);
+          zn = __ldg(cur.f + (kX + 2) * n + src_nx);
         }
         cp_async_wait_all();
         const T mass = ps[10 * kG2PThreads], vol0 = ps[11 * kG2PThreads];
