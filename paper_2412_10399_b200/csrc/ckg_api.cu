@@ -366,8 +366,9 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
     const size_t smem = p2g_smem_bytes<T>();
     CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    set_two_cta_carveout(p2g_tile_kernel<T, S>, smem, sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB);
-    CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kXferThreads, smem));
+    set_two_cta_carveout(p2g_tile_kernel<T, S>, smem,
+                         CKG_P2G_CPW * (sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB));
+    CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kP2GThreads, smem));
     if (cfg.scheme == S) p2g_ctas = std::max(1, per) * nsm;
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S>, kG2PThreads, 0));
     if (cfg.scheme == S) g2p_ctas = std::max(1, per) * nsm;
@@ -628,7 +629,7 @@ struct Context final : CtxBase {
             state(cur), perm, c, dir, active, seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
       return;
     }
-    p2g_tile_kernel<T, S><<<p2g_ctas, kXferThreads, p2g_smem_bytes<T>(), st>>>(
+    p2g_tile_kernel<T, S><<<p2g_ctas, kP2GThreads, p2g_smem_bytes<T>(), st>>>(
         state(cur), perm, c, dir, rec, cord, ccnt, pool, pool_cap, dstat, step_idx);
   }
   template <int S>

@@ -93,9 +93,18 @@ __device__ __forceinline__ void tile_add4(T* p, const T (&o)[4], int vs) {
   p[2 * vs] = a2 + o[2];
   p[3 * vs] = a3 + o[3];
 }
+// Compact-kernel P2G CTA: kP2GWarps warps, each scattering CKG_P2G_CPW of
+// the 8 sub-octant classes in turn into its own tile (any class fits the
+// common tile layout when the +1 grid tile is the full halo).
+#ifndef CKG_P2G_CPW
+#define CKG_P2G_CPW 2
+#endif
+static_assert(CKG_P2G_CPW == 1 || CKG_P2G_T1FULL, "several classes per warp need the full +1 grid tile");
+constexpr int kP2GWarps = 8 / CKG_P2G_CPW;
+constexpr int kP2GThreads = 32 * kP2GWarps;
 template <typename T>
 constexpr size_t p2g_smem_bytes() {
-  return size_t(kXferWarps) * kWarpVals * sizeof(T);
+  return size_t(kP2GWarps) * kWarpVals * sizeof(T);
 }
 
 __device__ __forceinline__ void decode_key(uint32_t key, int D, int& bx, int& by, int& bz) {
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
 }
 
 template <typename T, int SCHEME>
-__global__ void __launch_bounds__(kXferThreads, sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB)
+__global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB))
     p2g_tile_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
                     const uint32_t* __restrict__ cord, const uint4* __restrict__ ccnt,
@@ -279,8 +288,7 @@ __global__ void __launch_bounds__(kXferThreads, sizeof(T) == 4 ? CKG_P2G_MINB_F3
   __shared__ uint32_t s_itemb[3];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   T* wt = tiles + warp * kWarpVals;
-  for (int e = tid; e < kXferWarps * kWarpVals; e += kXferThreads) tiles[e] = T(0);
-  const int cx = warp & 1, cy = (warp >> 1) & 1, cz = (warp >> 2) & 1;  // class bits
+  for (int e = tid; e < kP2GWarps * kWarpVals; e += kP2GThreads) tiles[e] = T(0);
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const uint32_t lt = lanemask_lt();
   const int D = c.D;
@@ -323,6 +331,10 @@ __global__ void __launch_bounds__(kXferThreads, sizeof(T) == 4 ? CKG_P2G_MINB_F3
     int bx, by, bz;
     decode_key(key, D, bx, by, bz);
     for (uint32_t cb = s0; cb < s1; cb += kP2GChunk) {
+#pragma unroll 1
+    for (int ci = 0; ci < CKG_P2G_CPW; ++ci) {
+      const int cl = warp + ci * kP2GWarps;  // this pass's sub-octant class
+      const int cx = cl & 1, cy = (cl >> 1) & 1, cz = (cl >> 2) & 1;  // class bits
       // this warp's class list of the chunk (xfer_prep_kernel)
       uint32_t my_cnt = 0, my_off = 0;
       {
@@ -333,8 +345,8 @@ __global__ void __launch_bounds__(kXferThreads, sizeof(T) == 4 ? CKG_P2G_MINB_F3
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint32_t cq = (w4[q >> 1] >> (16 * (q & 1))) & 0xffffu;
-          if (q < warp) my_off += cq;
-          if (q == warp) my_cnt = cq;
+          if (q < cl) my_off += cq;
+          if (q == cl) my_cnt = cq;
         }
       }
       for (uint32_t rb = 0; rb < my_cnt; rb += 32) {
@@ -521,6 +533,7 @@ __global__ void __launch_bounds__(kXferThreads, sizeof(T) == 4 ? CKG_P2G_MINB_F3
         }
       }
       }  // rounds of this warp's class list
+    }  // classes of this warp
     }
     __syncthreads();
     if (warp == 0) stage((k + 2) % 3, __shfl_sync(0xffffffffu, pend, 0));
@@ -528,7 +541,7 @@ __global__ void __launch_bounds__(kXferThreads, sizeof(T) == 4 ? CKG_P2G_MINB_F3
     // Slot 0: all class tiles share origin 4b (5^3).  Slot 1: the 6^3 halo
     // from 4b - 1 (T1FULL: every warp's tile is that halo; else warp w's
     // 5^3 window covers offsets [1 - c, 5 - c] per axis).
-    for (int e = tid; e < 4 * kPTNodes + 4 * kTileNodes; e += kXferThreads) {
+    for (int e = tid; e < 4 * kPTNodes + 4 * kTileNodes; e += kP2GThreads) {
       T sum = T(0);
       int g, v, i, j, k;
       if (e < 4 * kPTNodes) {
@@ -539,7 +552,7 @@ __global__ void __launch_bounds__(kXferThreads, sizeof(T) == 4 ? CKG_P2G_MINB_F3
         j = (node / kPT) % kPT;
         k = node % kPT;
 #pragma unroll
-        for (int w = 0; w < kXferWarps; ++w) {
+        for (int w = 0; w < kP2GWarps; ++w) {
           T* q = tiles + w * kWarpVals + e;
           sum += *q;
           *q = T(0);
@@ -553,7 +566,7 @@ __global__ void __launch_bounds__(kXferThreads, sizeof(T) == 4 ? CKG_P2G_MINB_F3
         j = (node / kTileN) % kTileN;
         k = node % kTileN;
 #pragma unroll
-        for (int w = 0; w < kXferWarps; ++w) {
+        for (int w = 0; w < kP2GWarps; ++w) {
           if (CKG_P2G_T1FULL) {
             T* q = tiles + w * kWarpVals + e;
             sum += *q;
