@@ -434,7 +434,7 @@ struct Context final : CtxBase {
     rs.partials = dalloc<uint32_t>(scan_tiles(nh) + 1);
     for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp}) *b = dalloc<uint32_t>(cap);
     ncount = dalloc<uint32_t>(1);
-    wcnt = dalloc<uint32_t>(cap / 32 + 1);
+    wcnt = dalloc<uint32_t>(cap / 32 + 8);  // also the merge tile bounds (one uint4 per 256 positions)
     dfree(scan_partials_n);
     scan_partials_n = dalloc<uint32_t>(scan_tiles(cap) + 1);
     if (!hcount) CKG_CUDA(cudaMallocHost(&hcount, sizeof(uint32_t)));
@@ -534,7 +534,8 @@ struct Context final : CtxBase {
   // read-back of the changed count picks identity / merge / full radix.
   void enqueue_sort() {
     PState<T> cs = state(cur);
-    key_footprint_kernel<T><<<grid_for((n + kKeyPer - 1) / kKeyPer, 256, 1 << 30), 256, 0, st>>>(
+    (quad() ? key_footprint_kernel<T, 1> : key_footprint_kernel<T, 0>)
+        <<<grid_for((n + kKeyPer - 1) / kKeyPer, 256, 1 << 30), 256, 0, st>>>(
         cs, T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko_valid ? ko : nullptr, chg, wcnt, quad() ? nullptr : cls8, dstat);
     launches += 1;
     if (ko_valid) {
@@ -893,7 +894,8 @@ struct Context final : CtxBase {
     status_reset_kernel<<<1, 32, 0, st>>>(dstat, 1);
     // sort: crossers counted on the device; <= kSmallSort of them are merged
     // into the stored order, more take the full radix (IF nodes)
-    key_footprint_kernel<T><<<grid_for((n + kKeyPer - 1) / kKeyPer, 256, 1 << 30), 256, 0, st>>>(
+    (quad() ? key_footprint_kernel<T, 1> : key_footprint_kernel<T, 0>)
+        <<<grid_for((n + kKeyPer - 1) / kKeyPer, 256, 1 << 30), 256, 0, st>>>(
         state(cur), T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko, chg, wcnt, quad() ? nullptr : cls8, dstat);
     const uint64_t nw = (n + 31) / 32;
     exclusive_scan(wcnt, cpre, nw, scan_partials_n, st);

@@ -42,6 +42,28 @@ __device__ __forceinline__ bool inset_ok(T x, T inv_dx, int res) {
   return s >= T(2) && s <= T(res - 2);
 }
 
+// Marks the footprint box of key block kb with extension bits ext (bit 2a:
+// one block lower on axis a, bit 2a+1: one block higher).
+__device__ __forceinline__ void mark_footprint_box(uint32_t* __restrict__ core, const int (&kb)[3], uint32_t ext,
+                                                   int D) {
+  // inset particles (s in [2, res-2]) have footprint cells in [1, res-1], so
+  // every box block lies inside the (res/4 + 2)^3 directory: no bounds checks
+  // Per axis the box is 1 or 2 blocks: the low extension needs s < 4 kb + 1/4
+  // and the high one s >= 4 kb + 11/4, never both.  So 2 x 2 x 2 predicated
+  // stores cover every box (no data-dependent loop).
+  const bool ex = (ext & 3u) != 0u, ey = ((ext >> 2) & 3u) != 0u, ez = ((ext >> 4) & 3u) != 0u;
+  const int64_t DD = int64_t(D) * D;
+  uint32_t* c0 = core + (int64_t(kb[0] - int(ext & 1u)) * D + (kb[1] - int((ext >> 2) & 1u))) * D +
+                 (kb[2] - int((ext >> 4) & 1u));
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if ((a == 0 || ex) && (b == 0 || ey) && (k == 0 || ez)) c0[a * DD + b * D + k] = 1u;
+}
+
 // One particle of the key pass (all 32 lanes of the warp call it for 32
 // consecutive particles; x and the stored key are loaded by the caller).
 template <typename T>
@@ -97,22 +119,62 @@ __device__ __forceinline__ void key_footprint_one(uint64_t i, bool live, const T
   const uint64_t gbox = ok ? ((uint64_t(key) << 8) | ext) : (~0ull - (threadIdx.x & 31));
   const uint32_t peers = __match_any_sync(0xffffffffu, gbox);
   if (!ok || (__ffs(peers) - 1) != int(threadIdx.x & 31)) return;
-  // inset particles (s in [2, res-2]) have footprint cells in [1, res-1], so
-  // every box block lies inside the (res/4 + 2)^3 directory: no bounds checks
-  // Per axis the box is 1 or 2 blocks: the low extension needs s < 4 kb + 1/4
-  // and the high one s >= 4 kb + 11/4, never both.  So 2 x 2 x 2 predicated
-  // stores cover every box (no data-dependent loop).
-  const bool ex = (ext & 3u) != 0u, ey = ((ext >> 2) & 3u) != 0u, ez = ((ext >> 4) & 3u) != 0u;
-  const int64_t DD = int64_t(D) * D;
-  uint32_t* c0 = core + (int64_t(kb[0] - int(ext & 1u)) * D + (kb[1] - int((ext >> 2) & 1u))) * D +
-                 (kb[2] - int((ext >> 4) & 1u));
+  mark_footprint_box(core, kb, ext, D);
+}
+
+// The compact-kernel key pass with one rounded-to-floor conversion per
+// grid offset and axis: with s = x * inv_dx (T-rounded, as the reference),
+//   ip = floor(s + 1/4)      -> key block ip >> 2 (simulation.hpp:255-266) and
+//                               the -1 grid's upper node ip + 1 (hi block)
+//   i2 = floor(2 (s - 1/4))  -> floor(s - 1/4) = i2 >> 1 (lo block i2 >> 3) and
+//                               the class bit frac(s - 1/4) >= 1/2 = i2 & 1
+// (2x is exact).  For inset particles (2 <= s <= res - 2) the key block needs
+// no clamp and lo / hi lie within one block of it, so the only failure is the
+// inset itself (grid.hpp:121-126).
+__device__ __forceinline__ int floor_int(double v) { return __double2int_rd(v); }
+__device__ __forceinline__ int floor_int(float v) { return __float2int_rd(v); }
+
+template <typename T>
+__device__ __forceinline__ void key_footprint_compact(uint64_t i, bool live, const T (&x)[3], uint32_t kov,
+                                                      uint64_t n, T inv_dx, int res, int D,
+                                                      uint32_t* __restrict__ keys, uint32_t* __restrict__ core,
+                                                      const uint32_t* __restrict__ ko,
+                                                      uint32_t* __restrict__ cbits, uint32_t* __restrict__ wcnt,
+                                                      uint8_t* __restrict__ cls, DevStatus* st) {
+  bool ok = live, changed = false;
+  uint32_t key = 0xffffffffu, ext = 0, q = 0;
+  int kb[3] = {0, 0, 0};
+  if (live) {
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-        if ((a == 0 || ex) && (b == 0 || ey) && (k == 0 || ez)) c0[a * DD + b * D + k] = 1u;
+    for (int a = 0; a < 3; ++a) {
+      const T s = mul_rn(x[a], inv_dx);
+      const int ip = floor_int(add_rn(s, T(0.25)));
+      const int i2 = floor_int(T(2) * sub_rn(s, T(0.25)));
+      const int b = ip >> 2;
+      kb[a] = b < 0 ? 0 : (b > D - 1 ? D - 1 : b);
+      q |= uint32_t(i2 & 1) << a;
+      ok = ok && s >= T(2) && s <= T(res - 2);
+      ext |= ((i2 >> 3) < kb[a] ? 1u : 0u) << (2 * a);
+      ext |= (((ip + 1) >> 2) > kb[a] ? 1u : 0u) << (2 * a + 1);
+    }
+    key = (uint32_t(kb[0]) * uint32_t(D) + uint32_t(kb[1])) * uint32_t(D) + uint32_t(kb[2]);
+    keys[i] = key;
+    if (cls) cls[i] = uint8_t(q);
+    if (ko) changed = key != kov;
+    if (!ok) atomicOr(&st->inset_fail, 1u);
+  }
+  if (ko) {
+    const uint32_t cb = __ballot_sync(0xffffffffu, changed);
+    if ((threadIdx.x & 31) == 0 && i < n) {
+      cbits[i >> 5] = cb;
+      wcnt[i >> 5] = uint32_t(__popc(cb));
+      if (cb) atomicAdd(&st->nchanged, uint32_t(__popc(cb)));
+    }
+  }
+  const uint64_t gbox = ok ? ((uint64_t(key) << 8) | ext) : (~0ull - (threadIdx.x & 31));
+  const uint32_t peers = __match_any_sync(0xffffffffu, gbox);
+  if (!ok || (__ffs(peers) - 1) != int(threadIdx.x & 31)) return;
+  mark_footprint_box(core, kb, ext, D);
 }
 
 // K1 key pass: block key (simulation.hpp:255-266), footprint boxes + inset
@@ -121,7 +183,7 @@ __device__ __forceinline__ void key_footprint_one(uint64_t i, bool live, const T
 // loads issued up front (memory-level parallelism: the pass is latency-bound
 // at one particle per thread).
 constexpr int kKeyPer = 2;
-template <typename T>
+template <typename T, int QUAD>
 __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv_dx, int res, int D, int quad,
                                                             uint32_t* __restrict__ keys,
                                                             uint32_t* __restrict__ core,
@@ -144,8 +206,12 @@ __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv
 #pragma unroll
   for (int r = 0; r < kKeyPer; ++r) {
     const uint64_t i = base + 32 * r;
-    key_footprint_one<T>(i, i < cur.n, x[r], kov[r], cur.n, inv_dx, res, D, quad, keys, core, ko, cbits, wcnt, cls,
-                         st);
+    if (QUAD)
+      key_footprint_one<T>(i, i < cur.n, x[r], kov[r], cur.n, inv_dx, res, D, quad, keys, core, ko, cbits, wcnt,
+                           cls, st);
+    else
+      key_footprint_compact<T>(i, i < cur.n, x[r], kov[r], cur.n, inv_dx, res, D, keys, core, ko, cbits, wcnt, cls,
+                               st);
   }
 }
 
@@ -170,20 +236,28 @@ __global__ void inset_fixup_kernel(PState<T> cur, const uint32_t* __restrict__ p
 // active(B) = OR_{delta in {0,1}^3} core(B - delta).
 __global__ void __launch_bounds__(256) dilate_kernel(const uint32_t* __restrict__ core,
                                                      uint32_t* __restrict__ act, int D) {
-  const uint64_t nd = uint64_t(D) * D * D;
-  const uint64_t d = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  // 32-bit index arithmetic (the directory has (res/4 + 2)^3 < 2^32 entries;
+  // 64-bit div/mod was most of this kernel's instructions)
+  const uint32_t ud = uint32_t(D), nd = ud * ud * ud;
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nd) return;
-  const int bz = int(d % uint64_t(D)), by = int((d / uint64_t(D)) % uint64_t(D)), bx = int(d / (uint64_t(D) * D));
-  uint32_t a = 0;
-#pragma unroll
-  for (int dx = 0; dx < 2; ++dx)
-#pragma unroll
-    for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-      for (int dz = 0; dz < 2; ++dz) {
-        const int x = bx - dx, y = by - dy, z = bz - dz;
-        if (x >= 0 && y >= 0 && z >= 0) a |= __ldg(core + (int64_t(x) * D + y) * D + z);
-      }
+  const uint32_t row = d / ud, bz = d - row * ud;
+  const uint32_t bx = row / ud, by = row - bx * ud;
+  const uint32_t sx = ud * ud;
+  uint32_t a = __ldg(core + d);
+  if (bz > 0) a |= __ldg(core + d - 1);
+  if (by > 0) {
+    a |= __ldg(core + d - ud);
+    if (bz > 0) a |= __ldg(core + d - ud - 1);
+  }
+  if (bx > 0) {
+    a |= __ldg(core + d - sx);
+    if (bz > 0) a |= __ldg(core + d - sx - 1);
+    if (by > 0) {
+      a |= __ldg(core + d - sx - ud);
+      if (bz > 0) a |= __ldg(core + d - sx - ud - 1);
+    }
+  }
   act[d] = a ? 1u : 0u;
 }
 
