@@ -434,7 +434,7 @@ struct Context final : CtxBase {
     rs.partials = dalloc<uint32_t>(scan_tiles(nh) + 1);
     for (uint32_t** b : {&ko, &chg, &cpre, &ck, &ci, &iota, &perm_buf, &skeys_tmp}) *b = dalloc<uint32_t>(cap);
     ncount = dalloc<uint32_t>(1);
-    wcnt = dalloc<uint32_t>(cap / 32 + 8);  // also the merge tile bounds (one uint4 per 256 positions)
+    wcnt = dalloc<uint32_t>(cap / 32 + 1);
     dfree(scan_partials_n);
     scan_partials_n = dalloc<uint32_t>(scan_tiles(cap) + 1);
     if (!hcount) CKG_CUDA(cudaMallocHost(&hcount, sizeof(uint32_t)));

@@ -81,10 +81,7 @@ __global__ void __launch_bounds__(256) merge_bounds_kernel(const uint32_t* __res
                                                            const uint32_t* __restrict__ ck,
                                                            const uint32_t* __restrict__ ci, uint32_t nc,
                                                            const uint32_t* __restrict__ ncp,
-                                                           uint32_t* __restrict__ tile_lo_words) {
-  // per tile: the bound and the (key, index) of changed entry `bound` (key ~0
-  // when none), so merge_unchanged_kernel's first comparison needs no load
-  uint4* tile_lo = reinterpret_cast<uint4*>(tile_lo_words);
+                                                           uint32_t* __restrict__ tile_lo) {
   if (ncp) nc = *ncp;  // device count (graph substeps)
   const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t base = t * kMergeTile;
@@ -97,8 +94,7 @@ __global__ void __launch_bounds__(256) merge_bounds_kernel(const uint32_t* __res
       break;
     }
   }
-  const uint32_t lo = first < n ? changed_lower(ck, ci, 0, nc, keys[first], base) : 0u;
-  tile_lo[t] = lo < nc ? make_uint4(lo, __ldg(ck + lo), __ldg(ci + lo), 0u) : make_uint4(lo, ~0u, ~0u, 0u);
+  tile_lo[t] = first < n ? changed_lower(ck, ci, 0, nc, keys[first], base) : 0u;
 }
 
 // Four consecutive stored positions per thread (one 16-byte key load; the
@@ -111,7 +107,7 @@ __global__ void __launch_bounds__(256) merge_unchanged_kernel(const uint32_t* __
                                                               const uint32_t* __restrict__ ck,
                                                               const uint32_t* __restrict__ ci, uint32_t nc,
                                                               const uint32_t* __restrict__ ncp,
-                                                              const uint32_t* __restrict__ tile_lo_words,
+                                                              const uint32_t* __restrict__ tile_lo,
                                                               uint32_t* __restrict__ perm,
                                                               uint32_t* __restrict__ skeys) {
   const uint64_t i0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kMergePer;
@@ -127,31 +123,18 @@ __global__ void __launch_bounds__(256) merge_unchanged_kernel(const uint32_t* __
 #pragma unroll
     for (int e = 0; e < kMergePer; ++e) k[e] = i0 + e < n ? keys[i0 + e] : 0u;
   }
-  // (lo, key and index of changed entry lo): the walk compares registers and
-  // loads only when it steps (rare: a crosser inside this tile's key range)
-  const uint4 tb = __ldg(reinterpret_cast<const uint4*>(tile_lo_words) + (i0 / kMergeTile));
-  uint32_t lo = tb.x, lk = tb.y, li = tb.z;
+  uint32_t lo = __ldg(tile_lo + (i0 / kMergeTile));
   const int sh = int(i0 & 31);
 #pragma unroll
   for (int e = 0; e < kMergePer; ++e) {
     const uint64_t i = i0 + e;
     if (i >= n || ((b >> (sh + e)) & 1u)) continue;
     int steps = 0;
-    while (lo < nc && steps < 8 && (lk < k[e] || (lk == k[e] && uint64_t(li) < i))) {
+    while (lo < nc && steps < 8 && changed_entry_before(ck, ci, lo, k[e], i)) {
       ++lo;
       ++steps;
-      if (lo < nc) {
-        lk = __ldg(ck + lo);
-        li = __ldg(ci + lo);
-      }
     }
-    if (steps == 8) {
-      lo = changed_lower(ck, ci, lo, nc, k[e], i);
-      if (lo < nc) {
-        lk = __ldg(ck + lo);
-        li = __ldg(ci + lo);
-      }
-    }
+    if (steps == 8) lo = changed_lower(ck, ci, lo, nc, k[e], i);
     const uint64_t pos = (i - (wo + uint32_t(__popc(b & ((1u << (sh + e)) - 1u))))) + lo;
     perm[pos] = uint32_t(i);
     skeys[pos] = k[e];
