@@ -52,7 +52,7 @@ def parse():
                     help="quadratic: the 27-node B-spline baseline (paper's comparison)")
     ap.add_argument("--precision", type=int, default=8, choices=[8, 4])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-chains", type=int, default=2,
+    ap.add_argument("--e2e-chains", type=int, default=3,
                     help="independent host-resident simulations stepped concurrently (one host thread each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-single", action="store_true",
