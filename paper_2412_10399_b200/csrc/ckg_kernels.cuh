@@ -383,7 +383,8 @@ struct Dual {
 // x/dx +- 1/4 round exactly (always, away from powers of two), and
 // sin/cos(2 pi (f + 1/2)) = -sin/cos(2 pi f).  Otherwise both are evaluated.
 template <typename T>
-__device__ __forceinline__ void axis_pair_dual(T x, T dx, T inv_dx, int pow2, Axis<T>& am, Axis<T>& ap) {
+__device__ __forceinline__ void axis_pair_dual(T x, T dx, T inv_dx, int pow2, Axis<T>& am, Axis<T>& ap,
+                                               T* snp_out = nullptr) {
   const T xd = over_dx(x, dx, inv_dx, pow2);
   const T sm = sub_rn(xd, T(-0.25)), sp = sub_rn(xd, T(0.25));
   const T fbm = dfloor(sm), fbp = dfloor(sp);
@@ -399,6 +400,7 @@ __device__ __forceinline__ void axis_pair_dual(T x, T dx, T inv_dx, int pow2, Ax
   }
   snp *= TwoPi<T>::inv;
   snm *= TwoPi<T>::inv;
+  if (snp_out) *snp_out = snp;
   am.base = static_cast<int>(fbm);
   am.w0 = T(1) - fm + snm;
   am.w1 = fm - snm;
@@ -418,6 +420,34 @@ __device__ __forceinline__ Dual<T> dual_stencil(T x, T y, T z, T dx, T inv_dx, i
   axis_pair_dual(y, dx, inv_dx, pow2, d.ax[0][1], d.ax[1][1]);
   axis_pair_dual(z, dx, inv_dx, pow2, d.ax[0][2], d.ax[1][2]);
   return d;
+}
+
+// dual_stencil that also hands out the +1 grid's scaled sines, so a caller
+// can rebuild that grid's axes later with axis_plus_carried (bit-identical to
+// ax[1]) without a second sincos.
+template <typename T>
+__device__ __forceinline__ Dual<T> dual_stencil_sn(T x, T y, T z, T dx, T inv_dx, int pow2, T (&snp)[3]) {
+  Dual<T> d;
+  axis_pair_dual(x, dx, inv_dx, pow2, d.ax[0][0], d.ax[1][0], &snp[0]);
+  axis_pair_dual(y, dx, inv_dx, pow2, d.ax[0][1], d.ax[1][1], &snp[1]);
+  axis_pair_dual(z, dx, inv_dx, pow2, d.ax[0][2], d.ax[1][2], &snp[2]);
+  return d;
+}
+
+// The +1 grid's axis from its carried scaled sine and gradient factor (the
+// same operations as axis_pair_dual's ap: bit-identical).
+template <typename T>
+__device__ __forceinline__ Axis<T> axis_plus_carried(T x, T dx, T inv_dx, int pow2, T snp, T g0p) {
+  const T sp = sub_rn(over_dx(x, dx, inv_dx, pow2), T(0.25));
+  const T fbp = dfloor(sp);
+  const T fp = sp - fbp;
+  Axis<T> a;
+  a.base = static_cast<int>(fbp);
+  a.w0 = T(1) - fp + snp;
+  a.w1 = fp - snp;
+  a.g0 = g0p;
+  a.xi0 = (T(a.base) + T(0.25)) * dx - x;
+  return a;
 }
 
 // Quadratic B-spline baseline (kernel.hpp:208-241): 3 nodes per axis on the

@@ -54,6 +54,17 @@ constexpr int kXferWarps = kXferThreads / 32;
 #ifndef CKG_P2G_ILV
 #define CKG_P2G_ILV 0  // 1: P2G fast path with both grids' updates of a node offset in flight together
 #endif
+// +1 grid axes in P2G: 0 re-evaluated with a second sincos per axis, 1 rebuilt
+// from the dual evaluation's scaled sine and gradient factor kept in registers
+// (10M bench, P2G: FP32 0.709 -> 0.699 ms; FP64 1.511 -> 1.525 ms from the
+// extra spills, so FP64 re-evaluates; a shared-memory stash cost FP64 L1:
+// 1.95 ms).
+#ifndef CKG_P2G_CARRY_F64
+#define CKG_P2G_CARRY_F64 0
+#endif
+#ifndef CKG_P2G_CARRY_F32
+#define CKG_P2G_CARRY_F32 1
+#endif
 #ifndef CKG_P2G_MINB
 #define CKG_P2G_MINB 2
 #endif
@@ -365,6 +376,8 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
       M3<T> Ap, Q, Bp;  // Ap = dt * V0 * tau, Q = m * C
       T Minv[4][4];
       Dual<T> ds;
+      constexpr bool kCarry = (sizeof(T) == 4 ? CKG_P2G_CARRY_F32 : CKG_P2G_CARRY_F64) != 0;
+      T c_sn[3] = {0, 0, 0}, c_g0[3] = {0, 0, 0};  // kCarry: +1 grid scaled sines, gradient factors
       if (valid) {
         // every field load is issued before the first use
         const uint64_t n = cur.stride;  // field stride (buffer capacity)
@@ -390,7 +403,13 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
         Ap.a[1][1] = t6[3];
         Ap.a[1][2] = Ap.a[2][1] = t6[4];
         Ap.a[2][2] = t6[5];
-        ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
+        if constexpr (kCarry) {
+          ds = dual_stencil_sn(x, y, z, dx, c.inv_dx, c.pow2, c_sn);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) c_g0[k] = ds.ax[1][k].g0;
+        } else {
+          ds = dual_stencil(x, y, z, dx, c.inv_dx, c.pow2);
+        }
         if (SCHEME != kSchemePic) {
           M3<T> Di;
           if (!apic_d_inverse(apic_D(ds, dx), Di)) {
@@ -421,9 +440,15 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
           ax[1] = ds.ax[0][1];
           ax[2] = ds.ax[0][2];
         } else {
-          ax[0] = axis_pair(x, dx, c.inv_dx, c.pow2, T(0.25));
-          ax[1] = axis_pair(y, dx, c.inv_dx, c.pow2, T(0.25));
-          ax[2] = axis_pair(z, dx, c.inv_dx, c.pow2, T(0.25));
+          if constexpr (kCarry) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              ax[k] = axis_plus_carried(k == 0 ? x : k == 1 ? y : z, dx, c.inv_dx, c.pow2, c_sn[k], c_g0[k]);
+          } else {
+            ax[0] = axis_pair(x, dx, c.inv_dx, c.pow2, T(0.25));
+            ax[1] = axis_pair(y, dx, c.inv_dx, c.pow2, T(0.25));
+            ax[2] = axis_pair(z, dx, c.inv_dx, c.pow2, T(0.25));
+          }
         }
         // tile edge and origin shift of this grid (see kT1)
         const int E = g ? kT1 : kPT, VS = g ? kT1Nodes : kPTNodes;
