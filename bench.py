@@ -468,6 +468,12 @@ def main():
         sim.close()
         try:
             single = single_precision_rate(args, cfg, local)
+            # the same algorithmic-bytes roofline for the FP32 transfer kernels
+            sb = algorithmic_bytes(n, nblocks, args.scheme, 4)
+            sp2g, sg2p = single["phase_ms"]["p2g"], single["phase_ms"]["g2p"]
+            single["p2g_g2p"] = {"p2g_gbs": sb[0] / (sp2g * 1e-3) / 1e9,
+                                 "g2p_gbs": sb[1] / (sg2p * 1e-3) / 1e9,
+                                 "combined_frac": (sb[0] + sb[1]) / ((sp2g + sg2p) * 1e-3) / 1e9 / peak}
         except Exception as e:  # reported, never silently substituted
             single = {"value": None, "error": str(e)}
     if rank == 0:

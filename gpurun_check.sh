@@ -1,6 +1,7 @@
 #!/bin/bash
-# full check: the whole GPU parity suite, then the default bench line
+# full check: the whole GPU parity suite, smoke(), then the default bench line
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-tail -5 gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; echo smoke=$?; tail -2 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo bench=$?
-tail -c 3000 gpurun_out/bench_full.log
+tail -c 3500 gpurun_out/bench_full.log

@@ -104,12 +104,31 @@ def full(path, out, traffic=None):
             if vals:
                 lines.append(f"  {label:26s} {sum(vals) / len(vals):14.4f} {units[i]}")
         short = name.split("::")[-1].split("<")[0]
+        def avg(m):
+            i = h.index(m)
+            return sum(float(r[i].replace(",", "")) for r in rs) / len(rs)
+
         if "dram__bytes_read.sum" in h:
-            ur = units[h.index("dram__bytes_read.sum")]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
-            rd = sum(float(r[h.index("dram__bytes_read.sum")].replace(",", "")) for r in rs) / len(rs)
-            wr = sum(float(r[h.index("dram__bytes_write.sum")].replace(",", "")) for r in rs) / len(rs)
-            tr[short.replace("_tile", "")] = (rd + wr) * scale
+            # each metric in its own unit (ncu picks Mbyte/Gbyte per value)
+            to_b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            rd = avg("dram__bytes_read.sum") * to_b.get(units[h.index("dram__bytes_read.sum")], 1)
+            wr = avg("dram__bytes_write.sum") * to_b.get(units[h.index("dram__bytes_write.sum")], 1)
+            tr[short.replace("_tile", "")] = rd + wr
+        # floating-point operation counts (thread-level SASS ops; FMA = 2 flops):
+        # per-cycle rates summed over SMSPs x elapsed SMSP cycles
+        cyc = "smsp__cycles_elapsed.avg"
+        if cyc in h:
+            for prec, ops in (("fp64", ("dadd", "dmul", "dfma")), ("fp32", ("fadd", "fmul", "ffma"))):
+                ms = [f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum.per_cycle_elapsed" for o in ops]
+                if not all(m in h for m in ms):
+                    continue
+                cnt = [avg(m) * avg(cyc) for m in ms]
+                fl = cnt[0] + cnt[1] + 2 * cnt[2]
+                if fl > 0:
+                    lines.append(f"  {prec + '_ops add/mul/fma':26s} {cnt[0]:.4e} / {cnt[1]:.4e} / {cnt[2]:.4e}")
+                    tu = {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9}
+                    secs = avg("gpu__time_duration.sum") * tu.get(units[h.index("gpu__time_duration.sum")], 1)
+                    lines.append(f"  {prec + '_flop':26s} {fl:14.4e} ({fl / secs / 1e12:.2f} TFLOP/s)")
     # stall reasons of the longest kernel
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
