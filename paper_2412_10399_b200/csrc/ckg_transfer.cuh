@@ -95,6 +95,30 @@ constexpr int kPTNodes = kPT * kPT * kPT;  // 125
 constexpr int kT1 = CKG_P2G_T1FULL ? kTileN : kPT;
 constexpr int kT1Nodes = kT1 * kT1 * kT1;
 constexpr int kWarpVals = 4 * kPTNodes + 4 * kT1Nodes;
+// Warp-tile slot layout.  A class round's 32 lanes cover two lx planes of a
+// 4 x 4 (ly, lz) window, which the node offsets shift over the plane; the
+// dense index (lx E + ly) E + lz puts such windows on repeated banks.  FP32
+// (CKG_P2G_SWZ_F32): rows of 8 slots with lz XOR-swizzled by bit 1 of ly and
+// planes of 48 slots (16 mod 32 banks), so every window is conflict-free;
+// 1.5x the shared memory.  Correct (GPU parity suite green) but slower: the
+// 10M bench's FP32 P2G goes 0.695 -> 1.004 ms (L1 lost to the larger tiles,
+// 80 -> 140 B spills), so it is off; FP64 could not fit it at all.
+#ifndef CKG_P2G_SWZ_F32
+#define CKG_P2G_SWZ_F32 0
+#endif
+template <typename T>
+struct P2GTile {
+  static constexpr bool kSwz = sizeof(T) == 4 && CKG_P2G_SWZ_F32 && CKG_P2G_T1FULL;
+  static constexpr int R0 = kSwz ? 8 : kPT, P0 = kSwz ? 48 : kPT * kPT;  // -1 grid row / plane stride
+  static constexpr int R1 = kSwz ? 8 : kT1, P1 = kSwz ? 48 : kT1 * kT1;  // +1 grid
+  static constexpr int N0 = kPT * P0, N1 = kT1 * P1;                     // slots per value
+  static constexpr int kVals = 4 * N0 + 4 * N1;
+  __device__ static __forceinline__ int col(int ly, int lz) { return kSwz ? (lz ^ ((ly & 2) << 1)) : lz; }
+  __device__ static __forceinline__ int slot(int g, int lx, int ly, int lz) {
+    if constexpr (!kSwz) return g ? (lx * kT1 + ly) * kT1 + lz : (lx * kPT + ly) * kPT + lz;
+    return g ? lx * P1 + ly * R1 + col(ly, lz) : lx * P0 + ly * R0 + col(ly, lz);
+  }
+};
 template <typename T>
 __device__ __forceinline__ void tile_add4(T* p, const T (&o)[4], int vs) {
   // all four loads issued before the first add
@@ -115,7 +139,7 @@ constexpr int kP2GWarps = 8 / CKG_P2G_CPW;
 constexpr int kP2GThreads = 32 * kP2GWarps;
 template <typename T>
 constexpr size_t p2g_smem_bytes() {
-  return size_t(kP2GWarps) * kWarpVals * sizeof(T);
+  return size_t(kP2GWarps) * P2GTile<T>::kVals * sizeof(T);
 }
 
 __device__ __forceinline__ void decode_key(uint32_t key, int D, int& bx, int& by, int& bz) {
@@ -298,8 +322,9 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
   __shared__ uint32_t s_recb[3][kRecWords];
   __shared__ uint32_t s_itemb[3];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  T* wt = tiles + warp * kWarpVals;
-  for (int e = tid; e < kP2GWarps * kWarpVals; e += kP2GThreads) tiles[e] = T(0);
+  using L = P2GTile<T>;
+  T* wt = tiles + warp * L::kVals;
+  for (int e = tid; e < kP2GWarps * L::kVals; e += kP2GThreads) tiles[e] = T(0);
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const uint32_t lt = lanemask_lt();
   const int D = c.D;
@@ -451,7 +476,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
           }
         }
         // tile edge and origin shift of this grid (see kT1)
-        const int E = g ? kT1 : kPT, VS = g ? kT1Nodes : kPTNodes;
+        const int E = g ? kT1 : kPT, VS = g ? L::N1 : L::N0;
         const int shx = g ? (CKG_P2G_T1FULL ? 1 : cx) : 0, shy = g ? (CKG_P2G_T1FULL ? 1 : cy) : 0,
                   shz = g ? (CKG_P2G_T1FULL ? 1 : cz) : 0;
         const int lx = ax[0].base - (4 * bx - shx), ly = ax[1].base - (4 * by - shy), lz = ax[2].base - (4 * bz - shz);
@@ -503,7 +528,8 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
             o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
           }
         };
-        T* p0 = wt + g * 4 * kPTNodes + (lx * E + ly) * E + lz;
+        T* tb = wt + g * 4 * L::N0;  // this grid's tile
+        T* p0 = wt + g * 4 * kPTNodes + (lx * E + ly) * E + lz;  // dense layout
         if (maxrank == 0) {
           // fast path: every lane owns a distinct base cell in this warp, so
           // at a fixed node offset all lanes write distinct nodes
@@ -516,7 +542,10 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
                 for (int u = 0; u < 2; ++u) {
                   T o[4];
                   contrib(s, t, u, o);
-                  tile_add4(p0 + (s * E + t) * E + u, o, VS);
+                  if constexpr (L::kSwz)
+                    tile_add4(tb + L::slot(g, lx + s, ly + t, lz + u), o, VS);
+                  else
+                    tile_add4(p0 + (s * E + t) * E + u, o, VS);
                   // node (s,t,u) of one lane can be node (0,0,0) of its
                   // neighbour: order the read-modify-writes across lanes
                   __syncwarp(tmask);
@@ -529,7 +558,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
             const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
             T o[4];
             contrib(s, t, u, o);
-            T* p = p0 + (s * E + t) * E + u;
+            T* p = L::kSwz ? tb + L::slot(g, lx + s, ly + t, lz + u) : p0 + (s * E + t) * E + u;
             for (uint32_t layer = 0; layer <= maxrank; ++layer) {
               if (in_tile && rank == layer) tile_add4(p, o, VS);
               __syncwarp();
@@ -566,40 +595,55 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
     // Slot 0: all class tiles share origin 4b (5^3).  Slot 1: the 6^3 halo
     // from 4b - 1 (T1FULL: every warp's tile is that halo; else warp w's
     // 5^3 window covers offsets [1 - c, 5 - c] per axis).
-    for (int e = tid; e < 4 * kPTNodes + 4 * kTileNodes; e += kP2GThreads) {
+    constexpr int F1 = CKG_P2G_T1FULL ? L::N1 : kTileNodes;  // +1 grid flush slots per value
+    for (int e = tid; e < 4 * L::N0 + 4 * F1; e += kP2GThreads) {
       T sum = T(0);
       int g, v, i, j, k;
-      if (e < 4 * kPTNodes) {
+      if (e < 4 * L::N0) {
         g = 0;
-        v = e / kPTNodes;
-        const int node = e % kPTNodes;
-        i = node / (kPT * kPT);
-        j = (node / kPT) % kPT;
-        k = node % kPT;
+        v = e / L::N0;
+        const int sl = e % L::N0;
+        if constexpr (L::kSwz) {
+          i = sl / L::P0;
+          j = (sl % L::P0) / L::R0;
+          k = L::col(j, sl % L::R0);
+          if (j >= kPT || k >= kPT) continue;  // padding slot
+        } else {
+          i = sl / (kPT * kPT);
+          j = (sl / kPT) % kPT;
+          k = sl % kPT;
+        }
 #pragma unroll
         for (int w = 0; w < kP2GWarps; ++w) {
-          T* q = tiles + w * kWarpVals + e;
+          T* q = tiles + w * L::kVals + e;
           sum += *q;
           *q = T(0);
         }
       } else {
         g = 1;
-        const int e1 = e - 4 * kPTNodes;
-        v = e1 / kTileNodes;
-        const int node = e1 % kTileNodes;
-        i = node / (kTileN * kTileN);
-        j = (node / kTileN) % kTileN;
-        k = node % kTileN;
+        const int e1 = e - 4 * L::N0;
+        v = e1 / F1;
+        const int sl = e1 % F1;
+        if constexpr (L::kSwz) {
+          i = sl / L::P1;
+          j = (sl % L::P1) / L::R1;
+          k = L::col(j, sl % L::R1);
+          if (j >= kT1 || k >= kT1) continue;  // padding slot
+        } else {
+          i = sl / (kTileN * kTileN);
+          j = (sl / kTileN) % kTileN;
+          k = sl % kTileN;
+        }
 #pragma unroll
         for (int w = 0; w < kP2GWarps; ++w) {
           if (CKG_P2G_T1FULL) {
-            T* q = tiles + w * kWarpVals + e;
+            T* q = tiles + w * L::kVals + e;
             sum += *q;
             *q = T(0);
           } else {
             const int li = i - 1 + (w & 1), lj = j - 1 + ((w >> 1) & 1), lk = k - 1 + ((w >> 2) & 1);
             if (li >= 0 && lj >= 0 && lk >= 0 && li < kPT && lj < kPT && lk < kPT) {
-              T* q = tiles + w * kWarpVals + 4 * kPTNodes + v * kT1Nodes + (li * kPT + lj) * kPT + lk;
+              T* q = tiles + w * L::kVals + 4 * kPTNodes + v * kT1Nodes + (li * kPT + lj) * kPT + lk;
               sum += *q;
               *q = T(0);
             }
