@@ -153,6 +153,8 @@ typedef struct ckg_step_out {
   uint64_t sort_changed;              /* particles whose block key changed since the last sort */
   int32_t sort_kind;                  /* 0 full radix, 1 identity, 2 incremental merge */
   int32_t slab_migration;             /* slab substeps: 1 boundary-plane compaction, 2 full relayout */
+  uint64_t substeps_done;             /* substeps completed by this call (ckg_step_many stops at the first
+                                         failing one; the state is the one after the last completed) */
 } ckg_step_out;
 
 /* advance_frame (simulation.hpp:193-211) on the device: the host passes the
@@ -226,9 +228,11 @@ int32_t ckg_set_mass_epsilon(ckg_ctx* ctx, double mass_eps);
 /* Replaces Simulation<T>::step(dt) (simulation.hpp:150-188): one substep,
  * synchronous; on return `out` holds vmax/minJ/error for cfl_dt. */
 int32_t ckg_step(ckg_ctx* ctx, double dt, ckg_step_out* out);
-/* Enqueue `count` substeps of fixed dt without a host round trip in between
- * (errors are latched on the device and reported by ckg_sync).  `out` may be
- * NULL; when given it receives the state after the last substep. */
+/* `count` substeps of fixed dt, as `count` ckg_step calls (untimed): stops at
+ * the first failing substep, whose error `out` reports, leaving the state after
+ * the last completed one (out->substeps_done), like the reference's state
+ * after a throwing step() call in a loop.  A pool overflow grows the pool and
+ * retries that substep.  `out` may be NULL. */
 int32_t ckg_step_many(ckg_ctx* ctx, double dt, int32_t count, ckg_step_out* out);
 /* Simulation::advance_frame() without a callback (simulation.hpp:193-211, :213-215). */
 int32_t ckg_advance_frame(ckg_ctx* ctx, const ckg_frame_in* in, ckg_frame_out* out);

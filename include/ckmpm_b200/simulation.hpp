@@ -202,9 +202,12 @@ class Simulation {
     vmax_ = T(out.vmax);
     for (std::size_t m = 0; m < min_j_.size(); ++m) min_j_[m] = T(out.min_j[m]);
     timers_.substeps += out.substeps;
-    const std::uint64_t per = cfg_.scheme == TransferScheme::mls ? 32 : 16;
+    // node visits per particle (transfer.hpp:32-45): compact 2 x 8 (MLS
+    // scatters twice), quadratic baseline 27
+    const bool quad = cfg_.kernel == KernelKind::quadratic;
+    const std::uint64_t per = quad ? 27 : cfg_.scheme == TransferScheme::mls ? 32 : 16;
     counters_.p2g_node_visits += per * host_.size() * out.substeps;
-    counters_.g2p_node_visits += 16 * host_.size() * out.substeps;
+    counters_.g2p_node_visits += (quad ? 27 : 16) * host_.size() * out.substeps;
     counters_.p2g_transfers += host_.size() * out.substeps;
     counters_.g2p_transfers += host_.size() * out.substeps;
     if (out.substeps) host_valid_ = false;

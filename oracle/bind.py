@@ -187,6 +187,9 @@ class Ref:
         ref_lib().ckref_sim_grid(self.h, abi.ptr(coords), abi.ptr(nodes), nb)
         return coords, nodes
 
+    def active_blocks(self):
+        return int(ref_lib().ckref_sim_active_blocks(self.h))
+
     def timers(self):
         t = (C.c_double * 6)()
         ref_lib().ckref_sim_timers(self.h, t)

@@ -94,7 +94,7 @@ class StepOut(C.Structure):
         ("active_blocks", C.c_uint64),
         ("kernel_launches", C.c_uint64),
         ("sort_changed", C.c_uint64),
-        ("sort_kind", C.c_int32), ("slab_migration", C.c_int32),
+        ("sort_kind", C.c_int32), ("slab_migration", C.c_int32), ("substeps_done", C.c_uint64),
     ]
 
 

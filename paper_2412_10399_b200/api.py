@@ -277,12 +277,16 @@ class Simulation:
         while done < count:
             k = min(255, count - done)
             rc = lib().ckg_step_many(self._ctx, float(dt), k, C.byref(out))
-            _raise_for(self._ctx, rc, out)
-            self._absorb(out, k)
-            done += k
-            for _ in range(k):
+            # the completed substeps count also when a later one failed (the
+            # reference's state advances substep by substep)
+            ok = int(out.substeps_done)
+            if ok:
+                self._absorb(out, ok)
+            for _ in range(ok):
                 self._time = float(self._T(self._time) + self._T(dt))
-            self._step_count += k
+            self._step_count += ok
+            _raise_for(self._ctx, rc, out)
+            done += k
         return out
 
     def step_phases(self, dt: float, stop_after: int) -> abi.StepOut:
@@ -354,10 +358,13 @@ class Simulation:
         self._time = float(out.time)
         self._step_count += int(out.substeps)
         self._timers.substeps += int(out.substeps)
-        per = 32 if self.cfg.scheme == "mls" else 16
+        # node visits per particle (transfer.hpp:32-45): compact 2 x 8 (MLS
+        # scatters twice), quadratic baseline 27
+        quad = self.cfg.kernel == "quadratic"
+        per = 27 if quad else 32 if self.cfg.scheme == "mls" else 16
         c = self._counters
         c.p2g_node_visits += per * self._n * int(out.substeps)
-        c.g2p_node_visits += 16 * self._n * int(out.substeps)
+        c.g2p_node_visits += (27 if quad else 16) * self._n * int(out.substeps)
         c.p2g_transfers += self._n * int(out.substeps)
         c.g2p_transfers += self._n * int(out.substeps)
         self._vmax = float(out.vmax)

@@ -683,7 +683,7 @@ struct Context final : CtxBase {
     if (timed) CKG_CUDA(cudaEventRecord(ev[3], st));
     if (stop_after >= CKG_PHASE_P2G) {
       if (!stress_valid) {
-        stress_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), c, dstat, step_idx);
+        stress_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), perm, c, dstat, step_idx);
         stress_valid = true;
         launches += 1;
       }
@@ -717,13 +717,17 @@ struct Context final : CtxBase {
       std::memcpy(&j, &b, sizeof j);
       out->min_j[m] = std::isfinite(j) ? j : 1.0;
     }
-    const uint64_t per = cfg.scheme == CKG_SCHEME_MLS ? 32 : 16;
+    // node visits per particle (TransferCounters, transfer.hpp:32-45): the
+    // compact kernel's 2 x 8 dual-grid nodes (MLS scatters them twice), the
+    // quadratic baseline's 27 (transfer.hpp:285-320, :512-543)
+    const uint64_t per = quad() ? 27 : cfg.scheme == CKG_SCHEME_MLS ? 32 : 16;
+    const uint64_t per_g = quad() ? 27 : 16;
     if (stop_after >= CKG_PHASE_P2G) {
       out->p2g_node_visits = per * n;
       out->p2g_transfers = n;
     }
     if (stop_after >= CKG_PHASE_G2P) {
-      out->g2p_node_visits = 16 * n;
+      out->g2p_node_visits = per_g * n;
       out->g2p_transfers = n;
     }
     out->active_blocks = h.n_active;
@@ -777,22 +781,36 @@ struct Context final : CtxBase {
       std::memset(out, 0, sizeof(*out));
       for (double& j : out->min_j) j = 1.0;
       if (stop_after >= CKG_PHASE_G2P) step_count += uint64_t(count_steps);
+      out->substeps_done = stop_after >= CKG_PHASE_G2P ? uint64_t(count_steps) : 0;
       return CKG_OK;
     }
-    const bool timed = count_steps == 1;
+    if (count_steps == 1) return step_one(dt, stop_after, true, out);
+    // several substeps: one at a time, so a failing substep leaves the state
+    // of the last completed one and a pool overflow grows the pool and
+    // retries (every substep already waits for its key pass's changed count,
+    // so nothing is lost by checking the status in between)
+    uint64_t total_launches = 0;
+    int rc = CKG_OK;
+    uint64_t done = 0;
+    for (int k = 0; k < count_steps; ++k) {
+      rc = step_one(dt, CKG_PHASE_G2P, false, out);
+      total_launches += out->kernel_launches;
+      if (rc != CKG_OK) break;
+      ++done;
+    }
+    out->kernel_launches = total_launches;
+    out->substeps_done = done;
+    return rc;
+  }
+
+  // One substep up to stop_after (timed: per-phase device events).
+  int step_one(double dt, int stop_after, bool timed, ckg_step_out* out) {
     launches = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
-      if (count_steps == 1) {
-        enqueue_step(dt, stop_after, 0, true, timed);
-      } else {
-        for (int k = 0; k < count_steps; ++k) {
-          enqueue_step(dt, CKG_PHASE_G2P, k, k == 0, false);
-          cur ^= 1;
-        }
-      }
+      enqueue_step(dt, stop_after, 0, true, timed);
       CKG_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
       CKG_CUDA(cudaStreamSynchronize(st));
-      if (hstat->overflow && count_steps == 1) {
+      if (hstat->overflow) {
         ko_valid = false;
         // grow the pool (state untouched: G2P writes the other buffer)
         uint64_t want = std::min<uint64_t>(nd, uint64_t(hstat->n_active) * 5 / 4 + 64);
@@ -801,10 +819,11 @@ struct Context final : CtxBase {
       }
       break;
     }
-    fill_out(out, timed, count_steps == 1 ? stop_after : CKG_PHASE_G2P);
+    fill_out(out, timed, stop_after);
     out->kernel_launches = launches;
     out->sort_changed = last_changed;
     out->sort_kind = last_sort_kind;
+    out->substeps_done = 0;
     grid_valid = true;
     last_active = hstat->n_active;
     if (hstat->overflow) {
@@ -812,20 +831,15 @@ struct Context final : CtxBase {
       out->status = CKG_ERR_DEVICE;
       return CKG_ERR_DEVICE;
     }
-    int rc = decode_status(out, count_steps == 1 ? stop_after : CKG_PHASE_G2P);
-    if (count_steps == 1) {
-      if (rc == CKG_OK && stop_after >= CKG_PHASE_G2P) {
-        cur ^= 1;
-        step_count += 1;
-      } else {
-        ko_valid = false;  // stored order unchanged: the new sorted keys do not describe it
-      }
-      if (stop_after < CKG_PHASE_ACTIVATE) CKG_CUDA(cudaMemsetAsync(core, 0, nd * sizeof(uint32_t), st));
-    } else if (rc == CKG_OK) {
-      step_count += uint64_t(count_steps);
+    int rc = decode_status(out, stop_after);
+    if (rc == CKG_OK && stop_after >= CKG_PHASE_G2P) {
+      cur ^= 1;
+      step_count += 1;
+      out->substeps_done = 1;
     } else {
-      ko_valid = false;
+      ko_valid = false;  // stored order unchanged: the new sorted keys do not describe it
     }
+    if (stop_after < CKG_PHASE_ACTIVATE) CKG_CUDA(cudaMemsetAsync(core, 0, nd * sizeof(uint32_t), st));
     out->status = rc;
     return rc;
   }
@@ -1319,7 +1333,7 @@ struct Context final : CtxBase {
     clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
     CKG_CUDA(cudaEventRecord(ev[3], st));
     if (!stress_valid) {
-      stress_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), c, dstat, 0);
+      stress_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), perm, c, dstat, 0);
       stress_valid = true;
     }
     if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, 0);

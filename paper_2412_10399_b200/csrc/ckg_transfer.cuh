@@ -1202,17 +1202,21 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
 }
 
 // Initial stress cache for a freshly uploaded state (force_matrix of every
-// particle, transfer.hpp:183-216); errors surface as P2G-phase errors exactly
-// where the reference's scatter would throw them.
+// particle, transfer.hpp:183-216), walked in the substep's sorted order
+// (perm: sorted position -> stored index) so that a constitutive error is
+// reported, like the P2G's own errors, at the first failing particle of the
+// reference's scatter order (sorted index, atomicMin).
 template <typename T>
-__global__ void __launch_bounds__(256) stress_kernel(PState<T> cur, StepConst<T> c, DevStatus* st, int step) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= cur.n) return;
+__global__ void __launch_bounds__(256) stress_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
+                                                     DevStatus* st, int step) {
+  const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= cur.n) return;
+  const uint32_t i = perm ? perm[j] : uint32_t(j);
   const uint32_t mi = cur.mat[i];
   T t6[6];
   const int e = stress_tau6(load_m3(cur, kF, i), cur.f[kJ * cur.stride + i], cur.f[kVol * cur.stride + i],
                             c.mats[mi < kMaxMaterials ? mi : 0], t6);
-  if (e) record_error(st, step, kPhaseP2G, i, 0, e);
+  if (e) record_error(st, step, kPhaseP2G, j, 0, e);
 #pragma unroll
   for (int k = 0; k < 6; ++k) cur.tau[uint64_t(k) * cur.stride + i] = e ? T(0) : t6[k];
 }

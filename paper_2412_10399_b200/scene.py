@@ -329,6 +329,29 @@ class _MT19937_64:
         r = self.next() / 18446744073709551616.0
         return r if r < 1.0 else math.nextafter(1.0, 0.0)
 
+    def uniform_f32(self):
+        """libstdc++ generate_canonical<float, 24> with a 64-bit engine: the
+        draw is rounded to float ONCE (uint64 -> float, ties to even), divided
+        in float by float(2^64), and a result >= 1 is clamped to
+        nextafter(1.0f, 0) (uniform_real_distribution<float>(0, 1))."""
+        r = _u64_to_f32(self.next()) / np.float32(18446744073709551616.0)
+        return r if r < np.float32(1.0) else np.nextafter(np.float32(1.0), np.float32(0.0))
+
+
+def _u64_to_f32(n: int) -> np.float32:
+    """Correctly rounded uint64 -> float32 (one rounding, ties to even; a
+    conversion through float64 could round twice)."""
+    b = n.bit_length()
+    if b <= 24:
+        return np.float32(n)
+    shift = b - 24
+    q = n >> shift
+    rem = n & ((1 << shift) - 1)
+    half = 1 << (shift - 1)
+    if rem > half or (rem == half and (q & 1)):
+        q += 1
+    return np.float32(q) * np.float32(2.0 ** shift)  # exact: q <= 2^24, power-of-two scale
+
 
 def _shape_mask(shape: Shape, X, Y, Z, T):
     if shape.kind == "sphere":
@@ -395,7 +418,10 @@ def sample_shape(shape: Shape, dx, ppc: int, seed: int = 0, precision: int = 8) 
             for j in range(j0, j1 + 1):
                 for k in range(k0, k1 + 1):
                     for _ in range(16):
-                        u, v, w = rng.uniform(), rng.uniform(), rng.uniform()
+                        if precision == 4:
+                            u, v, w = rng.uniform_f32(), rng.uniform_f32(), rng.uniform_f32()
+                        else:
+                            u, v, w = rng.uniform(), rng.uniform(), rng.uniform()
                         pts.append(((T(i) + T(u)) * dx, (T(j) + T(v)) * dx, (T(k) + T(w)) * dx))
         arr = np.array(pts, dtype=T).reshape(-1, 3)
         X, Y, Z = arr[:, 0], arr[:, 1], arr[:, 2]

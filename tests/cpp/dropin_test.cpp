@@ -260,10 +260,13 @@ int rod() {
       max_xy = std::max({max_xy, std::abs(L.x - L0.x), std::abs(L.y - L0.y)});
     });
   }
-  bool pass = pin_ok && max_z / lz0 <= 1e-2 && max_xy / lz0 <= 1e-4;
+  // the reference's gate is z <= 1e-2, xy <= 1e-4; its own FP64 run measures
+  // 3.72e-11 / 5.20e-11, so the device is held to 1e-9
+  bool pass = pin_ok && max_z / lz0 <= 1e-9 && max_xy / lz0 <= 1e-9;
   std::printf(
       "{\"test\":\"rod\",\"pass\":%s,\"lz0\":%.6e,\"z_drift_rate\":%.3e,\"xy_leakage\":%.3e,\"substeps\":%llu,"
-      "\"gate\":\"criterion 4: pin 4.9639e-3 +-1%%, z<=1e-2, xy<=1e-4; reference measured 3.72e-11 / 5.20e-11\"}\n",
+      "\"gate\":\"criterion 4 (pin 4.9639e-3 +-1%%, z<=1e-2, xy<=1e-4) tightened to the reference's measured level: "
+      "z, xy <= 1e-9 (reference 3.72e-11 / 5.20e-11)\"}\n",
       pass ? "true" : "false", lz0, max_z / lz0, max_xy / lz0, (unsigned long long)sim.step_count());
   return pass ? 0 : 1;
 }
@@ -281,8 +284,9 @@ int spheres() {
       max_err = std::max(max_err, norm_inf(sv - sv0) / norm);
     });
   }
-  bool pass = max_err <= 1e-4;
-  std::printf("{\"test\":\"spheres\",\"pass\":%s,\"drift_rate\":%.3e,\"substeps\":%llu,\"gate\":1e-4}\n",
+  // reference gate 1e-4 (acceptance_main.cpp:231-238); held to 1e-9 here
+  bool pass = max_err <= 1e-9;
+  std::printf("{\"test\":\"spheres\",\"pass\":%s,\"drift_rate\":%.3e,\"substeps\":%llu,\"gate\":1e-9}\n",
               pass ? "true" : "false", max_err, (unsigned long long)sim.step_count());
   return pass ? 0 : 1;
 }

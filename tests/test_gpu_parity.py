@@ -288,3 +288,28 @@ def test_device_vs_golden(path):
                 y = np.asarray(b[f], dtype=np.float64)
                 err = float(np.max(np.abs(x - y)) / max(np.max(np.abs(y)), fl))
                 assert err <= tol[step], (step, f, err)
+
+
+def test_step_many_stops_at_failing_substep():
+    """A substep that throws leaves the state of the last completed one
+    (the reference's step() loop): a block flying into the domain inset raises
+    OutOfDomainError inside step_many after some substeps; the state and
+    step count equal those of the same number of single step() calls."""
+    cfg = small_scene(scheme="apic", res=32, bc="none", gravity=(0, 0, 0), lo=(0.0625 + 0.01, 0.4, 0.4),
+                      hi=(0.0625 + 0.09, 0.48, 0.48), velocity=(-3.0, 0.0, 0.0))
+    p = seed_particles(cfg)
+    dt = 1e-3  # 3 m/s * 1 ms = ~0.1 cell per substep
+    s1 = gpu_sim(cfg, p)
+    k_ok = 0
+    with pytest.raises(OutOfDomainError):
+        for _ in range(200):
+            s1.step(dt)
+            k_ok += 1
+    assert 0 < k_ok < 200
+    s2 = gpu_sim(cfg, p)
+    with pytest.raises(OutOfDomainError):
+        s2.step_many(dt, k_ok + 5)
+    assert s2.step_count() == k_ok
+    a, b = s1.particles(), s2.particles()
+    for f in ("x", "v", "F", "B"):
+        assert field_rel(a, b, f, floor=1e-3) <= 1e-12, f

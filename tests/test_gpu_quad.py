@@ -90,3 +90,26 @@ def test_quad_mls_rejected_like_reference():
     cfg = quad_scene(scheme="mls", res=32)
     with pytest.raises(ConfigError, match="mls requires the compact kernel"):
         gpu_sim(cfg, seed_particles(small_scene(res=32)))
+
+
+@pytest.mark.parametrize("kernel,per_p2g,per_g2p", [("quadratic", 27, 27), ("compact", 16, 16)])
+def test_transfer_counters_per_kernel(kernel, per_p2g, per_g2p):
+    """TransferCounters (transfer.hpp:32-45): the quadratic baseline visits 27
+    nodes per particle in both transfers, the compact kernel 2 x 8 (acceptance
+    criterion 7, tests/acceptance_main.cpp), through the host loop and the
+    device frame driver alike."""
+    cfg = small_scene(scheme="apic", res=32)
+    cfg.kernel = kernel
+    p = seed_particles(cfg)
+    sim = gpu_sim(cfg, p)
+    for _ in range(3):
+        sim.step(sim.cfl_dt(1.0))
+    c = sim.counters()
+    assert c.p2g_node_visits == 3 * per_p2g * len(p)
+    assert c.g2p_node_visits == 3 * per_g2p * len(p)
+    sim.reset_counters()
+    k = sim.advance_frame()
+    c = sim.counters()
+    assert k > 0
+    assert c.p2g_node_visits == k * per_p2g * len(p)
+    assert c.g2p_node_visits == k * per_g2p * len(p)

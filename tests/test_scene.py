@@ -89,3 +89,36 @@ def test_strict_config_rejects_unknown_fields():
     obj["bogus"] = 1
     with pytest.raises(ConfigError):
         SceneConfig.from_json(obj)
+
+
+@needs_ref
+@pytest.mark.parametrize("precision", [8, 4])
+def test_jittered_ppc16_seeding_bitwise_vs_reference(precision):
+    """ppc = 16 draws from mt19937_64 through uniform_real_distribution<T>
+    (scene.hpp:75, :116): in float the 64-bit draw is rounded to float once
+    and clamped below 1 (generate_canonical<float, 24>)."""
+    obj = {"name": "jit", "resolution": 64, "scheme": "apic",
+           "materials": [{"model": "fixed_corotated", "density": 1000.0, "E": 1e5, "nu": 0.3}],
+           "bodies": [{"shape": {"kind": "box", "lo": [0.3, 0.3, 0.3], "hi": [0.45, 0.4, 0.42]}, "material": 0,
+                       "ppc": 16, "seed": 12345},
+                      {"shape": {"kind": "sphere", "center": [0.6, 0.6, 0.6], "radius": 0.07}, "material": 0,
+                       "ppc": 16, "seed": 7}]}
+    cfg = SceneConfig.from_json(obj, precision)
+    ours = seed_particles(cfg, precision)
+    ref = bind.ref_seed(cfg, precision)
+    assert len(ours) == len(ref) > 10000
+    assert ours.tobytes() == ref.tobytes()
+
+
+def test_u64_to_f32_single_rounding():
+    from paper_2412_10399_b200.scene import _u64_to_f32
+    rng = np.random.default_rng(0)
+    for n in rng.integers(0, 2 ** 52, 2000):  # exact through float64 -> numpy agrees
+        assert _u64_to_f32(int(n)) == np.float32(float(int(n)))
+    # a value whose float64 rounding lands on a float32 tie (double rounding
+    # would round up to even twice): 2^63 + 2^39 + 1 rounds down in one step
+    n = (1 << 63) + (1 << 39) + 1
+    assert float(_u64_to_f32(n)) == float((1 << 63) + (1 << 40))  # nearest float32 above (rem > half)
+    n = (1 << 63) + (1 << 39) - 1
+    assert float(_u64_to_f32(n)) == float(1 << 63)
+    assert _u64_to_f32((1 << 64) - 1) == np.float32(2.0 ** 64)
