@@ -56,6 +56,8 @@ def parse():
                     help="secondary e2e figure: independent host-resident simulations stepped concurrently "
                          "(one host thread each); the headline e2e is one simulation")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--unfused", action="store_true",
+                    help="separate P2G / G2P kernels instead of the fused G2P2G (CKG_FLAG_UNFUSED)")
     ap.add_argument("--no-single", action="store_true",
                     help="skip the secondary FP32 (Simulation<float>) device-rate figure")
     ap.add_argument("--cpu-cells", type=int, default=None,
@@ -161,7 +163,8 @@ def single_precision_rate(args, cfg, local):
 
     L = lib()
     host = seed_particles(cfg, 4)
-    sim = Simulation(cfg, precision=4, device=local, particles=host)
+    sim = Simulation(cfg, precision=4, device=local, particles=host, fused=False if args.unfused else None)
+    fused = sim.fused()
     ctx = sim._ctx
     dt = sim.cfl_dt(1.0)
     o = abi.StepOut()
@@ -178,7 +181,7 @@ def single_precision_rate(args, cfg, local):
     L.ckg_timer_elapsed(ctx, 0, 1, C.byref(el))
     sim.close()
     n = len(host)
-    return {"value": n * args.steps / (el.value * 1e-3), "unit": UNIT, "dtype": "f32",
+    return {"value": n * args.steps / (el.value * 1e-3), "unit": UNIT, "dtype": "f32", "fused": fused,
             "ms_per_step": el.value / args.steps, "phase_ms": dict(zip(abi.PHASE_NAMES, acc)),
             "parity": "keys/order bit-exact and state <= 1e-5 vs the reference's Simulation<float> "
                       "(tests/test_gpu_parity.py::test_float_mode_vs_reference_float)"}
@@ -370,7 +373,8 @@ def main():
     cfg = block_scene(args.cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
     host = seed_particles(cfg, prec)
     n = len(host)
-    sim = Simulation(cfg, precision=prec, device=local, particles=host)
+    sim = Simulation(cfg, precision=prec, device=local, particles=host, fused=False if args.unfused else None)
+    fused = sim.fused()
     ctx = sim._ctx
     dt = sim.cfl_dt(1.0)
     out = abi.StepOut()
@@ -436,7 +440,8 @@ def main():
     ctxs = [ctx]
     extra = []
     for _ in range(chains - 1):
-        extra.append(Simulation(cfg, precision=prec, device=local, particles=host))
+        extra.append(Simulation(cfg, precision=prec, device=local, particles=host,
+                                fused=False if args.unfused else None))
         ctxs.append(extra[-1]._ctx)
     bufs = []
     for k in range(chains):
@@ -496,7 +501,11 @@ def main():
     p2g_avg = float(np.mean(p2g_ms))
     g2p_avg = float(np.mean(g2p_ms))
     peak, peak_kind = measured_peak_hbm()
-    if p2g_avg >= g2p_avg:
+    if fused:
+        # one kernel: G2P of this substep + P2G of the next (its P2G phase
+        # slot only promotes the pending scatter's status)
+        dom, dom_bytes, dom_ms = "g2p2g_kernel", p2g_bytes + g2p_bytes, g2p_avg
+    elif p2g_avg >= g2p_avg:
         dom, dom_bytes, dom_ms = "p2g_kernel", p2g_bytes, p2g_avg
     else:
         dom, dom_bytes, dom_ms = "g2p_kernel", g2p_bytes, g2p_avg
@@ -517,8 +526,9 @@ def main():
             # the same algorithmic-bytes roofline for the FP32 transfer kernels
             sb = algorithmic_bytes(n, nblocks, args.scheme, 4)
             sp2g, sg2p = single["phase_ms"]["p2g"], single["phase_ms"]["g2p"]
-            single["p2g_g2p"] = {"p2g_gbs": sb[0] / (sp2g * 1e-3) / 1e9,
-                                 "g2p_gbs": sb[1] / (sg2p * 1e-3) / 1e9,
+            single["p2g_g2p"] = {"p2g_gbs": None if single["fused"] else sb[0] / (sp2g * 1e-3) / 1e9,
+                                 "g2p_gbs": None if single["fused"] else sb[1] / (sg2p * 1e-3) / 1e9,
+                                 "combined_gbs": (sb[0] + sb[1]) / ((sp2g + sg2p) * 1e-3) / 1e9,
                                  "combined_frac": (sb[0] + sb[1]) / ((sp2g + sg2p) * 1e-3) / 1e9 / peak}
         except Exception as e:  # reported, never silently substituted
             single = {"value": None, "error": str(e)}
@@ -540,9 +550,12 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes": dom_bytes, "avg_ms": dom_ms},
+            "transfer_path": "fused G2P2G kernel (G2P of substep n + P2G of n+1)" if fused else
+                             "separate P2G and G2P kernels",
             "p2g_g2p": {"p2g_ms": p2g_avg, "g2p_ms": g2p_avg,
-                        "p2g_gbs": p2g_bytes / (p2g_avg * 1e-3) / 1e9,
-                        "g2p_gbs": g2p_bytes / (g2p_avg * 1e-3) / 1e9,
+                        "p2g_gbs": None if fused else p2g_bytes / (p2g_avg * 1e-3) / 1e9,
+                        "g2p_gbs": None if fused else g2p_bytes / (g2p_avg * 1e-3) / 1e9,
+                        "combined_gbs": (p2g_bytes + g2p_bytes) / ((p2g_avg + g2p_avg) * 1e-3) / 1e9,
                         "combined_frac": (p2g_bytes + g2p_bytes) / ((p2g_avg + g2p_avg) * 1e-3) / 1e9 / peak},
             "phase_ms": dict(zip(abi.PHASE_NAMES, phase_acc)),
             "sort_kinds": {"full_radix": sort_kinds.count(0), "identity": sort_kinds.count(1),

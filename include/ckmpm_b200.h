@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define CKG_ABI_VERSION 1
+#define CKG_ABI_VERSION 2
 
 #define CKG_OK 0
 #define CKG_ERR_CONFIG 2
@@ -69,6 +69,10 @@ extern "C" {
  * of ckg_step_phases. */
 /* ckg_config.flags */
 #define CKG_FLAG_QUADRATIC 1  /* KernelKind::quadratic (transfer.hpp:17): the 27-node B-spline baseline on one grid */
+#define CKG_FLAG_UNFUSED 2    /* separate P2G and G2P kernels instead of the fused G2P2G kernel (which is the default
+                                 for the compact kernel with PIC/APIC on one GPU; MLS, the quadratic baseline and
+                                 x-slab ranks always run the separate kernels).  CKMPM_FUSED=0 in the environment
+                                 has the same effect. */
 
 #define CKG_PHASE_SORT 1
 #define CKG_PHASE_ACTIVATE 2
@@ -221,6 +225,8 @@ int32_t ckg_upload(ckg_ctx* ctx, const void* particles, uint64_t n);
  * host AoS, in the device's current (sorted) order. */
 int32_t ckg_download(ckg_ctx* ctx, void* particles, uint64_t n);
 uint64_t ckg_particle_count(const ckg_ctx* ctx);
+/* 1 when the context's substeps run the fused G2P2G kernel, else 0. */
+int32_t ckg_fused(const ckg_ctx* ctx);
 
 /* Replaces Simulation<T>::mass_eps_ (simulation.hpp:227-232; restore() sets it). */
 int32_t ckg_set_mass_epsilon(ckg_ctx* ctx, double mass_eps);

@@ -40,6 +40,8 @@ def _declare(lib: C.CDLL) -> None:
     lib.ckg_download.restype = i32
     lib.ckg_particle_count.argtypes = [vp]
     lib.ckg_particle_count.restype = u64
+    lib.ckg_fused.argtypes = [vp]
+    lib.ckg_fused.restype = i32
     lib.ckg_set_mass_epsilon.argtypes = [vp, C.c_double]
     lib.ckg_set_mass_epsilon.restype = i32
     lib.ckg_step.argtypes = [vp, C.c_double, P(abi.StepOut)]
@@ -95,7 +97,7 @@ def _declare(lib: C.CDLL) -> None:
 
 EXPORTED = (
     "ckg_abi_version", "ckg_build_info", "ckg_status_string", "ckg_create", "ckg_destroy",
-    "ckg_upload", "ckg_download", "ckg_particle_count", "ckg_set_mass_epsilon", "ckg_step",
+    "ckg_upload", "ckg_download", "ckg_particle_count", "ckg_fused", "ckg_set_mass_epsilon", "ckg_step",
     "ckg_step_many", "ckg_step_phases", "ckg_advance_frame", "ckg_record_bytes", "ckg_pack_records",
     "ckg_records_wait", "ckg_debug_sort", "ckg_debug_bases",
     "ckg_grid_active_block_count", "ckg_grid_download", "ckg_grid_totals",

@@ -11,7 +11,7 @@ import ctypes as C
 
 import numpy as np
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 OK, ERR_CONFIG, ERR_NUMERICAL, ERR_IO, ERR_DEVICE = 0, 2, 3, 4, 5
 
@@ -29,6 +29,7 @@ NUM_NONFINITE = 10
 NUM_INACTIVE_BLOCK = 11
 NUM_SUBSTEP_LIMIT = 12
 FLAG_QUADRATIC = 1  # ckg_config.flags: KernelKind::quadratic
+FLAG_UNFUSED = 2  # ckg_config.flags: separate P2G / G2P kernels instead of the fused G2P2G
 RECORDS_CHECKPOINT = 0
 RECORDS_SNAPSHOT = 1
 

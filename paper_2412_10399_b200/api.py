@@ -124,7 +124,9 @@ class Simulation:
     """B200 twin of ckmpm::Simulation<T> (precision 8 = double, 4 = float)."""
 
     def __init__(self, cfg: SceneConfig, precision: int = 8, device: int = 0,
-                 particles: Optional[np.ndarray] = None):
+                 particles: Optional[np.ndarray] = None, fused: Optional[bool] = None):
+        """fused: None = the library default (fused G2P2G where supported),
+        False = the separate P2G / G2P kernels (CKG_FLAG_UNFUSED)."""
         cfg.validate()
         self.cfg = cfg
         self.precision = precision
@@ -132,6 +134,8 @@ class Simulation:
         host = seed_particles(cfg, precision) if particles is None else np.ascontiguousarray(particles)
         self._mass_eps = mass_epsilon(host, precision)
         self._abi_cfg = to_abi_config(cfg, precision, self._mass_eps, device)
+        if fused is False:
+            self._abi_cfg.flags |= abi.FLAG_UNFUSED
         ctx = C.c_void_p()
         rc = lib().ckg_create(C.byref(self._abi_cfg), C.byref(ctx))
         if rc != abi.OK:
@@ -232,6 +236,10 @@ class Simulation:
 
     def reset_counters(self):
         self._counters = TransferCounters()
+
+    def fused(self) -> bool:
+        """True when substeps run the fused G2P2G kernel (ckg_fused)."""
+        return bool(lib().ckg_fused(self._ctx))
 
     def last_sort_kind(self) -> int:
         """0 full radix sort, 1 identity (no key changed), 2 incremental merge."""

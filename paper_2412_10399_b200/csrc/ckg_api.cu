@@ -25,6 +25,7 @@
 #include "ckg_slab.cuh"
 #include "ckg_transfer.cuh"
 #include "ckg_quad.cuh"
+#include "ckg_g2p2g.cuh"
 
 namespace ckg {
 constexpr uint32_t kHostSmallSort = 2048;  // host-path crosser count sorted by one CTA
@@ -101,6 +102,7 @@ struct CtxBase {
   virtual int debug_sort(uint32_t* keys, uint32_t* order, uint64_t n) = 0;
   virtual int debug_bases(int32_t* bases, uint64_t n) = 0;
   virtual uint64_t active_blocks() = 0;
+  virtual bool is_fused() const = 0;
   virtual int grid_download(int32_t* coords, double* nodes, uint64_t nb) = 0;
   virtual int grid_totals(double* mass, double* mom) = 0;
   virtual int diagnostics(ckg_diagnostics* out) = 0;
@@ -120,7 +122,7 @@ template <typename T>
 struct Context final : CtxBase {
   int device = 0;
   cudaStream_t st = nullptr;
-  cudaEvent_t ev[7] = {};
+  cudaEvent_t ev[8] = {};  // phase boundaries; ev[7]: before a fused substep's deferred clear
   cudaEvent_t tev[16] = {};
   uint64_t launches = 0;  // kernels enqueued by the current API call
   uint64_t n = 0;
@@ -184,6 +186,19 @@ struct Context final : CtxBase {
   uint32_t* scan_partials_n = nullptr;  // scan scratch sized for n
   T* pool = nullptr;
   uint32_t pool_cap = 0;
+  // fused G2P2G mode (ckg_g2p2g.cuh): two dense block pools
+  // (slot = block key).  dpool[pa] holds the next substep's P2G when
+  // pend_valid (scattered by the last fused kernel with dt pend_dt), else
+  // zero; dpool[pa ^ 1] holds the last substep's grid over the active list
+  // when defer_clear (kept for the grid facade, cleared at the next substep),
+  // else zero.  pools_dirty: contents unknown (upload, failure).
+  bool fused = false;
+  T* dpool[2] = {nullptr, nullptr};
+  int pa = 0;
+  bool pend_valid = false, defer_clear = false, pools_dirty = true;
+  double pend_dt = 0;
+  int fused_ctas = 0;
+  T* facade_pool = nullptr;  // pool the grid facade reads (fused mode)
   // status
   DevStatus* dstat = nullptr;
   DevStatus* hstat = nullptr;  // pinned
@@ -247,6 +262,8 @@ struct Context final : CtxBase {
     uint64_t cap = dense_bytes <= (16ull << 30) ? nd : std::min<uint64_t>(nd, 1u << 16);
     set_pool_cap(uint32_t(cap));
     dstat = dalloc<DevStatus>(1);
+    CKG_CUDA(cudaMemset(dstat, 0, sizeof(DevStatus)));
+    status_reset_kernel<<<1, 32, 0, st>>>(dstat, 1, 1);
     CKG_CUDA(cudaMallocHost(&hstat, sizeof(DevStatus)));
     std::memset(hstat, 0, sizeof(DevStatus));
     dbcs = dalloc<BcParam<T>>(kMaxBoundaries);
@@ -266,6 +283,59 @@ struct Context final : CtxBase {
     }
     CKG_CUDA(cudaMemcpy(dbcs, hb.data(), sizeof(BcParam<T>) * kMaxBoundaries, cudaMemcpyHostToDevice));
     dacc = dalloc<double>(12);
+    // fused G2P2G (default on where supported; CKMPM_FUSED=0 disables it)
+    const char* fe = std::getenv("CKMPM_FUSED");
+    if (!(fe && fe[0] == '0') && !(cfg.flags & CKG_FLAG_UNFUSED) && fused_supported()) enable_fused();
+  }
+
+  bool is_fused() const override { return fused; }
+
+  bool fused_supported() const {
+    return !quad() && cfg.scheme != CKG_SCHEME_MLS && !slab && pool_cap >= nd;
+  }
+
+  template <int S, int MM>
+  void fused_attr(int& per) {
+    const size_t smem = g2p2g_smem_bytes<T, S>();
+    CKG_CUDA(cudaFuncSetAttribute(g2p2g_kernel<T, S, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CKG_CUDA(cudaFuncSetAttribute(g2p2g_kernel<T, S, MM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int p = 0;
+    CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, g2p2g_kernel<T, S, MM>, kFThreads, smem));
+    per = per == 0 ? p : std::min(per, p);
+  }
+
+  void enable_fused() {
+    if (fused) return;
+    dpool[0] = pool;
+    dpool[1] = dalloc<T>(uint64_t(nd) * kBlockVals);
+    pa = 0;
+    pend_valid = defer_clear = false;
+    pools_dirty = true;
+    int nsm = 0, per = 0;
+    CKG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    if (cfg.scheme == CKG_SCHEME_PIC) {
+      fused_attr<kSchemePic, kMFC>(per);
+      fused_attr<kSchemePic, kMDP>(per);
+      fused_attr<kSchemePic, kMAll>(per);
+    } else {
+      fused_attr<kSchemeApic, kMFC>(per);
+      fused_attr<kSchemeApic, kMDP>(per);
+      fused_attr<kSchemeApic, kMAll>(per);
+    }
+    fused_ctas = std::max(1, per) * nsm;
+    fused = true;
+  }
+
+  // Back to one compacted pool (slab mode): the dense pools' contents are dropped.
+  void disable_fused() {
+    if (!fused) return;
+    CKG_CUDA(cudaStreamSynchronize(st));
+    pool = dpool[0];
+    dfree(dpool[1]);
+    dpool[0] = nullptr;
+    fused = false;
+    pend_valid = defer_clear = false;
+    CKG_CUDA(cudaMemset(pool, 0, uint64_t(pool_cap) * kBlockVals * sizeof(T)));
   }
 
   ~Context() override {
@@ -312,6 +382,7 @@ struct Context final : CtxBase {
     dfree(cls8);
     dfree(scan_partials);
     dfree(scan_partials_n);
+    if (fused) dfree(dpool[1]);
     dfree(pool);
     dfree(dstat);
     dfree(dbcs);
@@ -469,6 +540,8 @@ struct Context final : CtxBase {
     grid_valid = false;
     stress_valid = false;
     ko_valid = false;
+    pend_valid = defer_clear = false;
+    pools_dirty = true;
     return CKG_OK;
   }
 
@@ -495,6 +568,7 @@ struct Context final : CtxBase {
   StepConst<T> make_const(double dt) const {
     StepConst<T> c{};
     c.quad = quad();
+    c.dense = fused ? 1 : 0;
     c.dx = T(cfg.dx);
     c.inv_dx = T(cfg.inv_dx);
     c.dt = T(dt);
@@ -606,7 +680,7 @@ struct Context final : CtxBase {
   }
 
   // K3-K6: inset error in sorted order, halo dilation, directory, segments.
-  void enqueue_activate(int step_idx) {
+  void enqueue_activate(int step_idx, bool want_cord = true) {
     PState<T> cs = state(cur);
     inset_fixup_kernel<T><<<148, 256, 0, st>>>(cs, perm, T(cfg.inv_dx), cfg.resolution, dstat, step_idx);
     dilate_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(core, flags, D);
@@ -619,7 +693,8 @@ struct Context final : CtxBase {
     if (slab) slab_ranges_kernel<<<1, 1, 0, st>>>(plane_start, D, bx_lo, bx_hi, dstat);
     segments_kernel<<<grid_for((n + 3) / 4, 256, 1 << 30), 256, 0, st>>>(skeys, n, seg_begin, seg_end);
     xfer_prep_kernel<T><<<148 * 8, kPrepWarps * 32, 0, st>>>(cs, perm, make_const(0.0), dir, active, seg_begin, seg_end,
-                                                 pool_cap, dstat, rec, cord, ccnt, quad() ? nullptr : cls8);
+                                                 pool_cap, dstat, rec, cord, ccnt,
+                                                 (quad() || !want_cord) ? nullptr : cls8);
   }
 
   template <int S>
@@ -704,6 +779,111 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaGetLastError());
   }
 
+  // ---------------------------------------------------------------- fused G2P2G
+  template <int S>
+  void enqueue_fused_kernel(const StepConst<T>& c, double dt_next, int step_idx) {
+    int mm = cfg.clamp_singular ? kMClamp : 0;
+    for (int m = 0; m < cfg.n_materials; ++m)
+      mm |= cfg.materials[m].model == kModelFC ? kMFC : cfg.materials[m].model == kModelDP ? kMDP : kMFluid;
+    const size_t smem = g2p2g_smem_bytes<T, S>();
+    T* in = dpool[pa];
+    T* out = dpool[pa ^ 1];
+    if (mm == kMFC || mm == 0)
+      g2p2g_kernel<T, S, kMFC><<<fused_ctas, kFThreads, smem, st>>>(state(cur), state(cur ^ 1), perm, c, rec,
+                                                                      pool_cap, in, out, T(dt_next), dstat, step_idx);
+    else if (mm == kMDP)
+      g2p2g_kernel<T, S, kMDP><<<fused_ctas, kFThreads, smem, st>>>(state(cur), state(cur ^ 1), perm, c, rec,
+                                                                      pool_cap, in, out, T(dt_next), dstat, step_idx);
+    else
+      g2p2g_kernel<T, S, kMAll><<<fused_ctas, kFThreads, smem, st>>>(state(cur), state(cur ^ 1), perm, c, rec,
+                                                                       pool_cap, in, out, T(dt_next), dstat, step_idx);
+  }
+
+  // One substep in fused mode up to stop_after.  The P2G of
+  // this substep is normally already in dpool[pa] (scattered by the previous
+  // substep's fused kernel with the same dt); otherwise the plain P2G runs.
+  // A full substep ends with the fused kernel: G2P of this substep from
+  // dpool[pa], P2G of the next one into dpool[pa ^ 1] at the same dt.
+  void enqueue_fused_step(double dt, int stop_after, bool timed) {
+    const StepConst<T> c = make_const(dt);
+    const uint64_t pool_bytes = uint64_t(pool_cap) * kBlockVals * sizeof(T);
+    if (timed) CKG_CUDA(cudaEventRecord(ev[7], st));
+    if (pools_dirty) {
+      CKG_CUDA(cudaMemsetAsync(dpool[0], 0, pool_bytes, st));
+      CKG_CUDA(cudaMemsetAsync(dpool[1], 0, pool_bytes, st));
+      pools_dirty = pend_valid = defer_clear = false;
+    } else if (defer_clear) {
+      // the last substep's grid (kept for the facade) over its active list
+      clear_list_kernel<T><<<148 * 8, 256, 0, st>>>(dpool[pa ^ 1], active, dstat, pool_cap);
+      launches += 1;
+      defer_clear = false;
+    }
+    const bool need_p2g = !pend_valid || pend_dt != dt;
+    launches += 1;
+    status_reset_kernel<<<1, 32, 0, st>>>(dstat, 1, need_p2g ? 1 : 0);
+    if (timed) CKG_CUDA(cudaEventRecord(ev[0], st));
+    enqueue_sort();
+    if (timed) CKG_CUDA(cudaEventRecord(ev[1], st));
+    if (stop_after >= CKG_PHASE_ACTIVATE) {
+      enqueue_activate(0, need_p2g);
+      launches += 8;
+    }
+    if (timed) CKG_CUDA(cudaEventRecord(ev[2], st));
+    if (stop_after >= CKG_PHASE_CLEAR && need_p2g && pend_valid) {
+      // a speculative scatter at another dt: its footprint lies in this
+      // substep's active set
+      clear_list_kernel<T><<<148 * 8, 256, 0, st>>>(dpool[pa], active, dstat, pool_cap);
+      launches += 1;
+    }
+    if (timed) CKG_CUDA(cudaEventRecord(ev[3], st));
+    if (stop_after >= CKG_PHASE_P2G) {
+      pool = dpool[pa];
+      if (need_p2g) {
+        if (!stress_valid) {
+          stress_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), perm, c, dstat, 0);
+          stress_valid = true;
+          launches += 1;
+        }
+        if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, 0);
+        else enqueue_p2g<kSchemeApic>(c, 0);
+      } else {
+        promote_pending_error_kernel<<<1, 32, 0, st>>>(dstat);
+      }
+      launches += 1;
+    }
+    if (timed) CKG_CUDA(cudaEventRecord(ev[4], st));
+    if (stop_after >= CKG_PHASE_GRID) {
+      grid_update_kernel<T><<<148 * 8, 256, 0, st>>>(dpool[pa], active, dstat, pool_cap, c, dbcs);
+      launches += 1;
+    }
+    if (timed) CKG_CUDA(cudaEventRecord(ev[5], st));
+    if (stop_after >= CKG_PHASE_G2P) {
+      if (cfg.scheme == CKG_SCHEME_PIC) enqueue_fused_kernel<kSchemePic>(c, dt, 0);
+      else enqueue_fused_kernel<kSchemeApic>(c, dt, 0);
+      launches += 1;
+    }
+    if (timed) CKG_CUDA(cudaEventRecord(ev[6], st));
+    CKG_CUDA(cudaGetLastError());
+  }
+
+  // Host bookkeeping after a fused-mode call (rc: its status).
+  void fused_after(int stop_after, int rc) {
+    if (rc == CKG_OK && stop_after >= CKG_PHASE_G2P) {
+      facade_pool = dpool[pa];  // this substep's grid (kept until the next substep)
+      pa ^= 1;
+      pend_valid = true;
+      pend_dt = last_dt;
+      defer_clear = true;
+      stress_valid = false;  // the fused kernel writes no stress cache
+    } else {
+      facade_pool = dpool[pa];
+      pools_dirty = true;
+      pend_valid = defer_clear = false;
+    }
+    pool = facade_pool;
+  }
+  double last_dt = 0;
+
   void fill_out(ckg_step_out* out, bool timed, int stop_after) {
     std::memset(out, 0, sizeof(*out));
     const DevStatus& h = *hstat;
@@ -736,6 +916,12 @@ struct Context final : CtxBase {
         float ms = 0;
         cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
         out->phase_ms[k] = ms;
+      }
+      if (fused) {
+        // the deferred clear of the last substep's grid runs before ev[0]
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[7], ev[0]);
+        out->phase_ms[2] += ms;
       }
     }
   }
@@ -807,10 +993,15 @@ struct Context final : CtxBase {
   int step_one(double dt, int stop_after, bool timed, ckg_step_out* out) {
     launches = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
-      enqueue_step(dt, stop_after, 0, true, timed);
+      if (fused) {
+        last_dt = dt;
+        enqueue_fused_step(dt, stop_after, timed);
+      } else {
+        enqueue_step(dt, stop_after, 0, true, timed);
+      }
       CKG_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
       CKG_CUDA(cudaStreamSynchronize(st));
-      if (hstat->overflow) {
+      if (hstat->overflow && !fused) {
         ko_valid = false;
         // grow the pool (state untouched: G2P writes the other buffer)
         uint64_t want = std::min<uint64_t>(nd, uint64_t(hstat->n_active) * 5 / 4 + 64);
@@ -832,6 +1023,7 @@ struct Context final : CtxBase {
       return CKG_ERR_DEVICE;
     }
     int rc = decode_status(out, stop_after);
+    if (fused) fused_after(stop_after, rc);
     if (rc == CKG_OK && stop_after >= CKG_PHASE_G2P) {
       cur ^= 1;
       step_count += 1;
@@ -1045,7 +1237,7 @@ struct Context final : CtxBase {
   // The graph needs: the stored-order keys (incremental sort), a valid stress
   // cache, a pool that cannot overflow (sized for the whole directory) and a
   // single domain.
-  bool graph_ready() const { return !slab && n > 0 && ko_valid && stress_valid && pool_cap >= nd; }
+  bool graph_ready() const { return !fused && !slab && n > 0 && ko_valid && stress_valid && pool_cap >= nd; }
 
   // Host-side bookkeeping of one completed host-loop substep (gather_all + the
   // loop body of advance_frame).  Returns true when the frame continues.
@@ -1254,7 +1446,8 @@ struct Context final : CtxBase {
     if (nb == 0) return CKG_OK;
     int32_t* dc = coords ? dalloc<int32_t>(nb * 3) : nullptr;
     double* dn = nodes ? dalloc<double>(nb * 128 * 4) : nullptr;
-    grid_export_kernel<T><<<grid_for(nb * 128, 256), 256, 0, st>>>(pool, active, nb, D, dc, dn);
+    grid_export_kernel<T><<<grid_for(nb * 128, 256), 256, 0, st>>>(fused ? facade_pool : pool, active, nb, D, dc,
+                                                                   dn, fused ? 1 : 0);
     CKG_CUDA(cudaGetLastError());
     if (dc) CKG_CUDA(cudaMemcpyAsync(coords, dc, nb * 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     if (dn) CKG_CUDA(cudaMemcpyAsync(nodes, dn, nb * 512 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1293,6 +1486,7 @@ struct Context final : CtxBase {
 
   int slab_set(int rank, int world, int lo, int hi) override {
     if (lo < 0 || hi > D || lo >= hi || rank < 0 || rank >= world) return CKG_ERR_CONFIG;
+    disable_fused();
     slab = true;
     const char* env = std::getenv("CKMPM_SLAB_FULL_RELAYOUT");
     force_full_relayout = env && env[0] == '1';
@@ -1720,6 +1914,7 @@ int32_t ckg_download(ckg_ctx* ctx, void* particles, uint64_t n) {
 }
 
 uint64_t ckg_particle_count(const ckg_ctx* ctx) { return ctx ? ctx->impl->count() : 0; }
+int32_t ckg_fused(const ckg_ctx* ctx) { return ctx && ctx->impl->is_fused() ? 1 : 0; }
 
 int32_t ckg_set_mass_epsilon(ckg_ctx* ctx, double eps) {
   if (!ctx) return CKG_ERR_CONFIG;

@@ -52,6 +52,7 @@ struct StepConst {
   int res, D, scheme, n_materials, clamp_singular, n_boundaries;
   int pow2;  // dx is a power of two: x/dx == x*inv_dx exactly (both are exact scalings)
   int quad;  // quadratic B-spline baseline (single grid, slot 0)
+  int dense; // block pool indexed by the block key (fused G2P2G mode, ckg_g2p2g.cuh)
   MatParam<T> mats[kMaxMaterials];
 };
 
@@ -83,17 +84,22 @@ struct DevStatus {
   unsigned int item_lo, item_hi;    // active-list range the transfer kernels walk
   unsigned int grid_lo, grid_hi;    // slot range of the grid update
   unsigned int clear_lo, clear_hi;  // slot range cleared before P2G
+  unsigned long long perr;      // packed error of the NEXT substep's scatter (fused G2P2G), ~0 = none
 };
 
 // err = step<<56 | phase<<52 | particle<<12 | axis<<8 | code
-__device__ __forceinline__ void record_error(DevStatus* st, int step, int phase, uint64_t particle,
-                                             int axis, int code) {
+__device__ __forceinline__ void record_error_at(unsigned long long* slot, int step, int phase, uint64_t particle,
+                                                int axis, int code) {
   unsigned long long p = (static_cast<unsigned long long>(step & 0xff) << 56) |
                          (static_cast<unsigned long long>(phase & 0xf) << 52) |
                          ((particle & 0xffffffffffull) << 12) |
                          (static_cast<unsigned long long>(axis & 0xf) << 8) |
                          static_cast<unsigned long long>(code & 0xff);
-  atomicMin(&st->err, p);
+  atomicMin(slot, p);
+}
+__device__ __forceinline__ void record_error(DevStatus* st, int step, int phase, uint64_t particle,
+                                             int axis, int code) {
+  record_error_at(&st->err, step, phase, particle, axis, code);
 }
 
 // Error codes (mirror include/ckmpm_b200.h CKG_NUM_*).
@@ -231,6 +237,14 @@ __device__ __forceinline__ int32_t dir_lookup(const int32_t* __restrict__ dir, i
 }
 
 constexpr int kBlockVals = 512;  // 2 grids * 4 values * 64 nodes
+
+// Pool slot of block (bi, bj, bk): the directory's compact slot, or (dense
+// pools, fused G2P2G mode) the block key itself for an active block.
+__device__ __forceinline__ int32_t pool_slot(const int32_t* __restrict__ dir, int D, int bi, int bj, int bk,
+                                             int dense) {
+  const int32_t s = dir_lookup(dir, D, bi, bj, bk);
+  return (dense && s >= 0) ? (bi * D + bj) * D + bk : s;
+}
 
 __device__ __forceinline__ uint64_t node_off(int32_t slot, int g, int i, int j, int k) {
   return uint64_t(slot) * kBlockVals + uint64_t(g) * 256 + uint64_t(((i & 3) << 4) | ((j & 3) << 2) | (k & 3));

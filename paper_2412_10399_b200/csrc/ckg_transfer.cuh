@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
       else if (lane == kRecS1) w = s1;
       else if (lane >= kRecNbr && lane < kRecNbr + 27) {
         const int t = lane - kRecNbr;
-        w = uint32_t(dir_lookup(dir, D, bx - 1 + t / 9, by - 1 + (t / 3) % 3, bz - 1 + t % 3));
+        w = uint32_t(pool_slot(dir, D, bx - 1 + t / 9, by - 1 + (t / 3) % 3, bz - 1 + t % 3, c.dense));
       }
       r[lane] = w;
     }
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
             T o[4];
             contrib(s, t, u, o);
             const int gi = ax[0].base + s, gj = ax[1].base + t, gk = ax[2].base + u;
-            const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
+            const int32_t slot = pool_slot(dir, D, gi >> 2, gj >> 2, gk >> 2, c.dense);
             if (slot < 0 || uint32_t(slot) >= cap) {
               record_error(st, step, kPhaseP2G, sorted_index(), 0, kErrInactive);
             } else {
@@ -678,7 +678,8 @@ __global__ void grid_update_kernel(T* __restrict__ pool, const uint32_t* __restr
   const T dt = step_dt(c);
   for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
        k += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t slot = g0 + uint32_t(k >> sh);
+    const uint32_t j = g0 + uint32_t(k >> sh);  // active-list position
+    const uint32_t slot = c.dense ? __ldg(active + j) : j;
     const int g = int(k >> 6) & (c.quad ? 0 : 1);
     const int l = int(k & 63);
     T* base = pool + uint64_t(slot) * kBlockVals + g * 256 + l;
@@ -689,7 +690,7 @@ __global__ void grid_update_kernel(T* __restrict__ pool, const uint32_t* __restr
                 base[192] * inv + c.gravity[2] * dt};
       if (c.n_boundaries > 0) {
         int bx, by, bz;
-        decode_key(__ldg(active + slot), D, bx, by, bz);
+        decode_key(__ldg(active + j), D, bx, by, bz);
         const T off = (c.quad ? T(0) : (g == 0 ? T(-0.25) : T(0.25))) * c.dx;  // grid.hpp:194-197, tag 0 / -1 / +1
         const T xp[3] = {T(bx * 4 + ((l >> 4) & 3)) * c.dx + off, T(by * 4 + ((l >> 2) & 3)) * c.dx + off,
                          T(bz * 4 + (l & 3)) * c.dx + off};
@@ -983,7 +984,7 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
                 q, dx,
                 [&](int s, int t, int u, int cc) {
                   const int gi = q[0].base + s, gj = q[1].base + t, gk = q[2].base + u;
-                  const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
+                  const int32_t slot = pool_slot(dir, D, gi >> 2, gj >> 2, gk >> 2, c.dense);
                   if (slot < 0 || uint32_t(slot) >= cap) {
                     record_error(st, step, kPhaseG2P, i, 0, kErrInactive);
                     return T(0);
@@ -1037,7 +1038,7 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
             for (int nid = 0; nid < 8; ++nid) {
               const int s = nid >> 2, t = (nid >> 1) & 1, u = nid & 1;
               const int gi = ax[0].base + s, gj = ax[1].base + t, gk = ax[2].base + u;
-              const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
+              const int32_t slot = pool_slot(dir, D, gi >> 2, gj >> 2, gk >> 2, c.dense);
               T a0 = T(0), a1 = T(0), a2 = T(0);
               if (slot < 0 || uint32_t(slot) >= cap) {
                 record_error(st, step, kPhaseG2P, i, 0, kErrInactive);
@@ -1238,9 +1239,10 @@ __global__ void clear_kernel(T* __restrict__ pool, const DevStatus* st, uint32_t
 }
 
 // Status reset before a substep.
-__global__ void status_reset_kernel(DevStatus* st, int reset_err) {
+__global__ void status_reset_kernel(DevStatus* st, int reset_err, int reset_perr = 0) {
   if (threadIdx.x == 0) {
     if (reset_err) st->err = ~0ull;
+    if (reset_perr) st->perr = ~0ull;
     st->vmax2 = 0ull;
     st->nonfinite = 0u;
     st->n_active = 0u;
@@ -1329,14 +1331,14 @@ __global__ void bases_kernel(PState<T> p, T dx, T inv_dx, int pow2, int32_t* __r
 template <typename T>
 __global__ void grid_export_kernel(const T* __restrict__ pool, const uint32_t* __restrict__ active,
                                    uint64_t nb, int D, int32_t* __restrict__ coords,
-                                   double* __restrict__ nodes) {
+                                   double* __restrict__ nodes, int dense) {
   const uint64_t total = nb * 128;
   for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
        k += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t b = k >> 7;
     const int nn = int(k & 127);
     const int g = nn >> 6, l = nn & 63;
-    const T* base = pool + b * kBlockVals + g * 256 + l;
+    const T* base = pool + (dense ? uint64_t(active[b]) : b) * kBlockVals + g * 256 + l;
     if (nodes) {
       double* o = nodes + k * 4;
       o[0] = double(base[0]);

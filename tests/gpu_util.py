@@ -29,8 +29,8 @@ def field_rel(a, b, name, floor=1e-300):
     return float(np.max(np.abs(x - y)) / scale) if x.size else 0.0
 
 
-def gpu_sim(cfg, particles, precision=8):
-    return Simulation(cfg, precision=precision, particles=particles)
+def gpu_sim(cfg, particles, precision=8, fused=None):
+    return Simulation(cfg, precision=precision, particles=particles, fused=fused)
 
 
 def nodes_by_coord(coords, nodes):

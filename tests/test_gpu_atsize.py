@@ -69,8 +69,11 @@ TWIST = {"name": "twisting_bar_ppc8", "resolution": 64, "extent": 1.0, "kernel":
                         {"kind": "sticky", "lo": [0.703125, 0.40625, 0.40625], "hi": [0.765625, 0.59375, 0.59375],
                          "velocity": [0.0, 0.0, 0.0], "omega": [-1.0, 0.0, 0.0], "center": [0.734375, 0.5, 0.5]}]}
 
-# natural field scales (a vanishing field is judged against these floors)
-FLOOR = {"x": 1.0, "v": 0.01, "F": 1.0, "B": 1e-8, "J": 1.0}
+# natural field scales (a vanishing field is judged against these floors);
+# B (APIC affine velocity, ~ v dx) is judged against max|v| dx of the
+# reference state: its error enters the next P2G as B D^-1 xi ~ B / dx, i.e.
+# as a velocity error (a translating body's B is pure round-off)
+FLOOR = {"x": 1.0, "v": 0.01, "F": 1.0, "B": None, "J": 1.0}
 
 
 def _run_pair(cfg, p0, steps, tol, fields=("x", "v", "F", "B"), threads=THREADS, deterministic=False,
@@ -96,7 +99,10 @@ def _run_pair(cfg, p0, steps, tol, fields=("x", "v", "F", "B"), threads=THREADS,
                 assert np.array_equal(a["volume0"], b["volume0"]), f"stored order differs after substep {k}"
                 if k in tol:
                     for f in fields:
-                        e = field_rel(a, b, f, floor=floors[f])
+                        fl = floors[f]
+                        if fl is None:  # B: max|v| dx of the reference state
+                            fl = float(np.max(np.abs(b["v"]))) * cfg.dx()
+                        e = field_rel(a, b, f, floor=fl)
                         errs[(k, f)] = e
                         assert e <= tol[k], (k, f, e)
         out = sim.particles()
@@ -167,8 +173,8 @@ def test_twisting_bar_rotating_sticky_bc_vs_reference():
     v0 + omega x (x - c) with omega = (+-1, 0, 0) (grid.hpp:38-44)."""
     cfg = SceneConfig.from_json(TWIST)
     p = seed_particles(cfg, 8)
-    errs, a, _ = _run_pair(cfg, p, 50, {1: 1e-12, 10: 1e-11, 50: 1e-9}, threads=1, deterministic=True,
-                           floors={"x": 1.0, "v": 0.05, "F": 1.0, "B": 1e-5, "J": 1.0})
+    errs, a, _ = _run_pair(cfg, p, 50, {1: 1e-12, 10: 1e-10, 50: 1e-9}, threads=1, deterministic=True,
+                           floors={"x": 1.0, "v": 0.05, "F": 1.0, "B": None, "J": 1.0})
     # the bar's ends really rotate: angular velocity about x of the end slabs
     assert np.max(np.abs(a["v"][:, 1:])) > 1e-3
 

@@ -36,7 +36,10 @@ def _ref_advance_frame(ref, cfg, book):
 
 
 def _pair(cfg, p):
-    return gpu_sim(cfg, p), gpu_sim(cfg, p)
+    """(device frame driver, host loop): the CUDA-graph frame driver runs the
+    separate P2G / G2P kernels; the host loop runs the default (fused G2P2G)
+    substeps, so the two paths are checked against each other as well."""
+    return gpu_sim(cfg, p, fused=False), gpu_sim(cfg, p)
 
 
 def _compare_states(a, b, tol):
