@@ -56,8 +56,8 @@ def parse():
                     help="secondary e2e figure: independent host-resident simulations stepped concurrently "
                          "(one host thread each); the headline e2e is one simulation")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--unfused", action="store_true",
-                    help="separate P2G / G2P kernels instead of the fused G2P2G (CKG_FLAG_UNFUSED)")
+    ap.add_argument("--fused", action="store_true",
+                    help="fused G2P2G kernel instead of the separate P2G / G2P kernels (CKG_FLAG_FUSED)")
     ap.add_argument("--no-single", action="store_true",
                     help="skip the secondary FP32 (Simulation<float>) device-rate figure")
     ap.add_argument("--cpu-cells", type=int, default=None,
@@ -163,7 +163,7 @@ def single_precision_rate(args, cfg, local):
 
     L = lib()
     host = seed_particles(cfg, 4)
-    sim = Simulation(cfg, precision=4, device=local, particles=host, fused=False if args.unfused else None)
+    sim = Simulation(cfg, precision=4, device=local, particles=host, fused=True if args.fused else None)
     fused = sim.fused()
     ctx = sim._ctx
     dt = sim.cfl_dt(1.0)
@@ -373,7 +373,7 @@ def main():
     cfg = block_scene(args.cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
     host = seed_particles(cfg, prec)
     n = len(host)
-    sim = Simulation(cfg, precision=prec, device=local, particles=host, fused=False if args.unfused else None)
+    sim = Simulation(cfg, precision=prec, device=local, particles=host, fused=True if args.fused else None)
     fused = sim.fused()
     ctx = sim._ctx
     dt = sim.cfl_dt(1.0)
@@ -441,7 +441,7 @@ def main():
     extra = []
     for _ in range(chains - 1):
         extra.append(Simulation(cfg, precision=prec, device=local, particles=host,
-                                fused=False if args.unfused else None))
+                                fused=True if args.fused else None))
         ctxs.append(extra[-1]._ctx)
     bufs = []
     for k in range(chains):

@@ -69,10 +69,10 @@ extern "C" {
  * of ckg_step_phases. */
 /* ckg_config.flags */
 #define CKG_FLAG_QUADRATIC 1  /* KernelKind::quadratic (transfer.hpp:17): the 27-node B-spline baseline on one grid */
-#define CKG_FLAG_UNFUSED 2    /* separate P2G and G2P kernels instead of the fused G2P2G kernel (which is the default
-                                 for the compact kernel with PIC/APIC on one GPU; MLS, the quadratic baseline and
-                                 x-slab ranks always run the separate kernels).  CKMPM_FUSED=0 in the environment
-                                 has the same effect. */
+#define CKG_FLAG_FUSED 2      /* run each substep's G2P fused with the next substep's P2G (one kernel, DESIGN.md
+                                 §4e; compact kernel, PIC/APIC, one GPU; ignored otherwise).  CKMPM_FUSED=1 in
+                                 the environment has the same effect.  Off by default: on the B200 it is slower
+                                 than the separate P2G / G2P kernels. */
 
 #define CKG_PHASE_SORT 1
 #define CKG_PHASE_ACTIVATE 2

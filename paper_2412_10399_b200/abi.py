@@ -29,7 +29,7 @@ NUM_NONFINITE = 10
 NUM_INACTIVE_BLOCK = 11
 NUM_SUBSTEP_LIMIT = 12
 FLAG_QUADRATIC = 1  # ckg_config.flags: KernelKind::quadratic
-FLAG_UNFUSED = 2  # ckg_config.flags: separate P2G / G2P kernels instead of the fused G2P2G
+FLAG_FUSED = 2  # ckg_config.flags: fused G2P2G kernel (G2P of substep n + P2G of n+1)
 RECORDS_CHECKPOINT = 0
 RECORDS_SNAPSHOT = 1
 

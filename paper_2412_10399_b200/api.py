@@ -125,8 +125,9 @@ class Simulation:
 
     def __init__(self, cfg: SceneConfig, precision: int = 8, device: int = 0,
                  particles: Optional[np.ndarray] = None, fused: Optional[bool] = None):
-        """fused: None = the library default (fused G2P2G where supported),
-        False = the separate P2G / G2P kernels (CKG_FLAG_UNFUSED)."""
+        """fused: True = the fused G2P2G kernel where supported
+        (CKG_FLAG_FUSED); None/False = the library default (separate P2G /
+        G2P kernels unless CKMPM_FUSED=1)."""
         cfg.validate()
         self.cfg = cfg
         self.precision = precision
@@ -134,8 +135,8 @@ class Simulation:
         host = seed_particles(cfg, precision) if particles is None else np.ascontiguousarray(particles)
         self._mass_eps = mass_epsilon(host, precision)
         self._abi_cfg = to_abi_config(cfg, precision, self._mass_eps, device)
-        if fused is False:
-            self._abi_cfg.flags |= abi.FLAG_UNFUSED
+        if fused:
+            self._abi_cfg.flags |= abi.FLAG_FUSED
         ctx = C.c_void_p()
         rc = lib().ckg_create(C.byref(self._abi_cfg), C.byref(ctx))
         if rc != abi.OK:

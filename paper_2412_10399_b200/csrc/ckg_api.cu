@@ -198,6 +198,7 @@ struct Context final : CtxBase {
   bool pend_valid = false, defer_clear = false, pools_dirty = true;
   double pend_dt = 0;
   int fused_ctas = 0;
+  uint32_t* act_alt = nullptr;  // the previous substep's active list (fused mode)
   T* facade_pool = nullptr;  // pool the grid facade reads (fused mode)
   // status
   DevStatus* dstat = nullptr;
@@ -283,9 +284,9 @@ struct Context final : CtxBase {
     }
     CKG_CUDA(cudaMemcpy(dbcs, hb.data(), sizeof(BcParam<T>) * kMaxBoundaries, cudaMemcpyHostToDevice));
     dacc = dalloc<double>(12);
-    // fused G2P2G (default on where supported; CKMPM_FUSED=0 disables it)
+    // fused G2P2G (opt-in: CKG_FLAG_FUSED or CKMPM_FUSED=1)
     const char* fe = std::getenv("CKMPM_FUSED");
-    if (!(fe && fe[0] == '0') && !(cfg.flags & CKG_FLAG_UNFUSED) && fused_supported()) enable_fused();
+    if (((fe && fe[0] == '1') || (cfg.flags & CKG_FLAG_FUSED)) && fused_supported()) enable_fused();
   }
 
   bool is_fused() const override { return fused; }
@@ -308,6 +309,7 @@ struct Context final : CtxBase {
     if (fused) return;
     dpool[0] = pool;
     dpool[1] = dalloc<T>(uint64_t(nd) * kBlockVals);
+    act_alt = dalloc<uint32_t>(pool_cap);
     pa = 0;
     pend_valid = defer_clear = false;
     pools_dirty = true;
@@ -332,6 +334,7 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaStreamSynchronize(st));
     pool = dpool[0];
     dfree(dpool[1]);
+    dfree(act_alt);
     dpool[0] = nullptr;
     fused = false;
     pend_valid = defer_clear = false;
@@ -382,7 +385,10 @@ struct Context final : CtxBase {
     dfree(cls8);
     dfree(scan_partials);
     dfree(scan_partials_n);
-    if (fused) dfree(dpool[1]);
+    if (fused) {
+      dfree(dpool[1]);
+      dfree(act_alt);
+    }
     dfree(pool);
     dfree(dstat);
     dfree(dbcs);
@@ -807,17 +813,18 @@ struct Context final : CtxBase {
   void enqueue_fused_step(double dt, int stop_after, bool timed) {
     const StepConst<T> c = make_const(dt);
     const uint64_t pool_bytes = uint64_t(pool_cap) * kBlockVals * sizeof(T);
-    if (timed) CKG_CUDA(cudaEventRecord(ev[7], st));
     if (pools_dirty) {
       CKG_CUDA(cudaMemsetAsync(dpool[0], 0, pool_bytes, st));
       CKG_CUDA(cudaMemsetAsync(dpool[1], 0, pool_bytes, st));
       pools_dirty = pend_valid = defer_clear = false;
-    } else if (defer_clear) {
-      // the last substep's grid (kept for the facade) over its active list
-      clear_list_kernel<T><<<148 * 8, 256, 0, st>>>(dpool[pa ^ 1], active, dstat, pool_cap);
-      launches += 1;
-      defer_clear = false;
     }
+    // the last substep's grid (kept for the facade) is cleared over its
+    // active list right before the fused kernel scatters into that pool
+    // (L2-resident when the kernel's reductions arrive); its list is kept
+    // while this substep's activation builds the new one
+    const bool clear_prev = defer_clear;
+    if (clear_prev) std::swap(active, act_alt);
+    defer_clear = false;
     const bool need_p2g = !pend_valid || pend_dt != dt;
     launches += 1;
     status_reset_kernel<<<1, 32, 0, st>>>(dstat, 1, need_p2g ? 1 : 0);
@@ -832,7 +839,7 @@ struct Context final : CtxBase {
     if (stop_after >= CKG_PHASE_CLEAR && need_p2g && pend_valid) {
       // a speculative scatter at another dt: its footprint lies in this
       // substep's active set
-      clear_list_kernel<T><<<148 * 8, 256, 0, st>>>(dpool[pa], active, dstat, pool_cap);
+      clear_list_kernel<T><<<148 * 8, 256, 0, st>>>(dpool[pa], active, &dstat->n_active, pool_cap);
       launches += 1;
     }
     if (timed) CKG_CUDA(cudaEventRecord(ev[3], st));
@@ -857,6 +864,11 @@ struct Context final : CtxBase {
       launches += 1;
     }
     if (timed) CKG_CUDA(cudaEventRecord(ev[5], st));
+    if (stop_after >= CKG_PHASE_G2P && clear_prev) {
+      clear_list_kernel<T><<<148 * 8, 256, 0, st>>>(dpool[pa ^ 1], act_alt, &dstat->n_active_prev, pool_cap);
+      launches += 1;
+    }
+    if (timed) CKG_CUDA(cudaEventRecord(ev[7], st));
     if (stop_after >= CKG_PHASE_G2P) {
       if (cfg.scheme == CKG_SCHEME_PIC) enqueue_fused_kernel<kSchemePic>(c, dt, 0);
       else enqueue_fused_kernel<kSchemeApic>(c, dt, 0);
@@ -917,11 +929,14 @@ struct Context final : CtxBase {
         cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
         out->phase_ms[k] = ms;
       }
-      if (fused) {
-        // the deferred clear of the last substep's grid runs before ev[0]
+      if (fused && stop_after >= CKG_PHASE_G2P) {
+        // fused: the last substep's grid is cleared between the grid update
+        // (ev[5]) and the fused kernel (ev[7] .. ev[6])
         float ms = 0;
-        cudaEventElapsedTime(&ms, ev[7], ev[0]);
+        cudaEventElapsedTime(&ms, ev[5], ev[7]);
         out->phase_ms[2] += ms;
+        cudaEventElapsedTime(&ms, ev[7], ev[6]);
+        out->phase_ms[5] = ms;
       }
     }
   }
@@ -1845,7 +1860,7 @@ std::string validate(const ckg_config* c) {
     if (model != CKG_MODEL_FIXED_COROTATED && model != CKG_MODEL_J_FLUID && model != CKG_MODEL_DRUCKER_PRAGER)
       return "material: reserved tag and not implemented";
   }
-  if (c->flags & ~CKG_FLAG_QUADRATIC) return "config: unknown flags";
+  if (c->flags & ~(CKG_FLAG_QUADRATIC | CKG_FLAG_FUSED)) return "config: unknown flags";
   if ((c->flags & CKG_FLAG_QUADRATIC) && c->scheme == CKG_SCHEME_MLS)
     return "scheme: mls requires the compact kernel";  // scene.hpp:193-194
   long long D = c->resolution / 4 + 2;

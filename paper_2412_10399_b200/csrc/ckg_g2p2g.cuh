@@ -67,6 +67,12 @@ constexpr size_t g2p2g_smem_bytes() {
                                              kFThreads) * sizeof(T);
 }
 
+// Stash / record column of thread t: t ^ ((t >> 3) & 7).  A warp's own
+// columns (stash and record writes) stay conflict-free, and so do the phase-B
+// reads, whose lanes take one class of a lattice chunk -- threads 8j + o,
+// stride 8 (8-way conflicts unswizzled).
+__device__ __forceinline__ int fcol(int t) { return t ^ ((t >> 3) & 7); }
+
 // Node (gi, gj, gk) of grid g in a dense block pool; -1 outside the directory box.
 __device__ __forceinline__ int64_t dense_node(int D, int g, int gi, int gj, int gk) {
   if (gi < 0 || gj < 0 || gk < 0) return -1;
@@ -513,7 +519,7 @@ __global__ void __launch_bounds__(kFThreads, sizeof(T) == 4 ? CKG_FUSED_MINB_F32
       T Jout = T(1);
       uint32_t mi = 0;
       uint32_t q = 8u;  // sub-octant class of the new position (8: none)
-      T* gs = gst + tid;  // gs[k * kFThreads]
+      T* gs = gst + fcol(tid);  // gs[k * kFThreads]
       if (live) {
         const FusedA<T> fa = fused_gather_update<T, SCHEME, MM>(cur, nxt, perm, i, gs, vt, s_mats, dx, c.inv_dx, c.pow2,
                                                                 D, dt, c.clamp_singular, c.clamp_floor, bx, by, bz,
@@ -571,7 +577,7 @@ __global__ void __launch_bounds__(kFThreads, sizeof(T) == 4 ? CKG_FUSED_MINB_F32
         for (uint32_t rb = lo; rb < hi; rb += 32) {
           const bool in_round = rb + lane < hi;
           const int sl = in_round ? int(s_slot[rb + lane]) : 0;
-          fused_scatter_round<T, SCHEME>(gst + sl, in_round, cb + sl, dx, c.inv_dx, c.pow2, D, dt_next, bx, by, bz,
+          fused_scatter_round<T, SCHEME>(gst + fcol(sl), in_round, cb + sl, dx, c.inv_dx, c.pow2, D, dt_next, bx, by, bz,
                                          cy, cz, wt, pool_out, st);
         }
       }
@@ -640,8 +646,8 @@ __global__ void __launch_bounds__(kFThreads, sizeof(T) == 4 ? CKG_FUSED_MINB_F32
 // the blocks a substep used; every write of that substep stayed inside them).
 template <typename T>
 __global__ void clear_list_kernel(T* __restrict__ pool, const uint32_t* __restrict__ list,
-                                  const DevStatus* st, uint32_t cap) {
-  const uint32_t nb = min(st->n_active, cap);
+                                  const unsigned int* count, uint32_t cap) {
+  const uint32_t nb = min(*count, cap);
   using W = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
   W zero;
   zero.x = T(0);

@@ -77,6 +77,7 @@ struct DevStatus {
   unsigned long long minj[kMaxMaterials];  // bits of min J as double (J > 0)
   unsigned int nonfinite;
   unsigned int n_active;
+  unsigned int n_active_prev;   // n_active of the previous substep (set by the status reset)
   unsigned int overflow;
   unsigned int inset_fail;      // some particle violated the 2-cell inset (index fixed up after the sort)
   unsigned int nchanged;        // particles whose block key differs from the stored sorted key

@@ -1245,6 +1245,7 @@ __global__ void status_reset_kernel(DevStatus* st, int reset_err, int reset_perr
     if (reset_perr) st->perr = ~0ull;
     st->vmax2 = 0ull;
     st->nonfinite = 0u;
+    st->n_active_prev = st->n_active;
     st->n_active = 0u;
     st->overflow = 0u;
     st->inset_fail = 0u;

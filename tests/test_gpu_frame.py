@@ -37,9 +37,9 @@ def _ref_advance_frame(ref, cfg, book):
 
 def _pair(cfg, p):
     """(device frame driver, host loop): the CUDA-graph frame driver runs the
-    separate P2G / G2P kernels; the host loop runs the default (fused G2P2G)
-    substeps, so the two paths are checked against each other as well."""
-    return gpu_sim(cfg, p, fused=False), gpu_sim(cfg, p)
+    separate P2G / G2P kernels; the host loop runs fused G2P2G substeps, so
+    the two paths are checked against each other as well."""
+    return gpu_sim(cfg, p), gpu_sim(cfg, p, fused=True)
 
 
 def _compare_states(a, b, tol):

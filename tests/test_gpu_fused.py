@@ -1,9 +1,9 @@
-"""Fused G2P2G (csrc/ckg_g2p2g.cuh): the default substep
-for the compact kernel with PIC/APIC on one GPU.  Parity against the C oracle
-and the reference engine like the separate-kernel path, plus the mode's own
+"""Fused G2P2G (csrc/ckg_g2p2g.cuh; CKG_FLAG_FUSED) for the
+compact kernel with PIC/APIC on one GPU.  Parity against the C oracle and the
+reference engine like the separate-kernel path, plus the mode's own
 bookkeeping: the speculative next-substep scatter at the current dt (re-done
 when the next dt differs), partial-phase calls, the grid facade after a fused
-substep, and the separate-kernel path itself (CKG_FLAG_UNFUSED)."""
+substep, and the equality of both paths."""
 import numpy as np
 import pytest
 
@@ -32,13 +32,13 @@ def _state(scheme="apic", model="fixed_corotated", bc="sticky"):
     ("mls", "fixed_corotated", "none", False)])
 def test_mode_selection(scheme, model, bc, expect):
     cfg, p0 = _state(scheme, model, bc)
-    with Simulation(cfg, particles=p0) as s:
+    with Simulation(cfg, particles=p0, fused=True) as s:
         assert s.fused() == expect
-    with Simulation(cfg, particles=p0, fused=False) as s:
-        assert not s.fused()
+    with Simulation(cfg, particles=p0) as s:
+        assert not s.fused()  # separate kernels by default
     cfg.kernel = "quadratic"
     if scheme != "mls":
-        with Simulation(cfg, particles=p0) as s:
+        with Simulation(cfg, particles=p0, fused=True) as s:
             assert not s.fused()
 
 
@@ -50,7 +50,7 @@ def test_mode_selection(scheme, model, bc, expect):
 def test_state_vs_oracle_both_modes(scheme, model, bc, fused):
     cfg, p0 = _state(scheme, model, bc)
     orc = bind.Oracle(cfg, p0)
-    sim = Simulation(cfg, particles=p0, fused=None if fused else False)
+    sim = Simulation(cfg, particles=p0, fused=fused)
     assert sim.fused() == fused
     tol = {1: 1e-12, 10: 1e-10, 100: 1e-8}
     done = 0
@@ -75,7 +75,7 @@ def test_changing_dt_redoes_the_speculative_scatter():
     engine stepped with the same dt sequence."""
     cfg, p0 = _state()
     ref = bind.Ref(cfg, p0)
-    sim = Simulation(cfg, particles=p0)
+    sim = Simulation(cfg, particles=p0, fused=True)
     assert sim.fused()
     for k in range(30):
         dt = ref.cfl_dt(1.0) * (0.5 if k % 3 == 1 else 1.0)
@@ -92,8 +92,8 @@ def test_fused_equals_unfused_and_grid_facade():
     after a completed substep (this substep's grid: mass and velocities after
     the grid update) identical in block set and values."""
     cfg, p0 = _state()
-    a = Simulation(cfg, particles=p0)
-    b = Simulation(cfg, particles=p0, fused=False)
+    a = Simulation(cfg, particles=p0, fused=True)
+    b = Simulation(cfg, particles=p0)
     assert a.fused() and not b.fused()
     for _ in range(12):
         dt = b.cfl_dt(1.0)
@@ -122,7 +122,7 @@ def test_partial_phases_then_full_steps():
     pools are rebuilt afterwards and the following substeps match the oracle."""
     cfg, p0 = _state()
     orc = bind.Oracle(cfg, p0)
-    sim = Simulation(cfg, particles=p0)
+    sim = Simulation(cfg, particles=p0, fused=True)
     for k in range(6):
         dt = orc.cfl_dt(1.0)
         if k in (0, 3):
@@ -140,7 +140,7 @@ def test_upload_mid_run_discards_pending_scatter():
     """set_particles between substeps (the reference's mutable particles()):
     the pending scatter of the old state must not leak into the next substep."""
     cfg, p0 = _state()
-    sim = Simulation(cfg, particles=p0)
+    sim = Simulation(cfg, particles=p0, fused=True)
     orc = bind.Oracle(cfg, p0)
     dt = orc.cfl_dt(1.0)
     for _ in range(3):
@@ -162,7 +162,7 @@ def test_upload_mid_run_discards_pending_scatter():
 def test_fused_float_mode_vs_reference_float():
     cfg = small_scene(scheme="apic", res=32)
     p32 = seed_particles(cfg, 4)
-    sim = Simulation(cfg, precision=4, particles=p32)
+    sim = Simulation(cfg, precision=4, particles=p32, fused=True)
     assert sim.fused()
     ref = bind.Ref(cfg, p32, precision=4)
     for _ in range(5):
