@@ -437,6 +437,11 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   }
 
+  template <typename K>
+  void g2p_attr(K* kernel) {
+    CKG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g2p_dyn_smem<T>())));
+  }
+
   template <int S>
   void occupancy_for() {
     int nsm = 0, per = 0;
@@ -447,7 +452,10 @@ struct Context final : CtxBase {
                          CKG_P2G_CPW * (sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB));
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kP2GThreads, smem));
     if (cfg.scheme == S) p2g_ctas = std::max(1, per) * nsm;
-    CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S>, kG2PThreads, 0));
+    g2p_attr(g2p_tile_kernel<T, S, 0, kMFC>);
+    g2p_attr(g2p_tile_kernel<T, S, 0, kMDP>);
+    g2p_attr(g2p_tile_kernel<T, S>);
+    CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S>, kG2PThreads, g2p_dyn_smem<T>()));
     if (cfg.scheme == S) g2p_ctas = std::max(1, per) * nsm;
     if constexpr (S != kSchemeMls) {
       if (quad() && cfg.scheme == S) {
@@ -456,7 +464,9 @@ struct Context final : CtxBase {
         set_two_cta_carveout(p2g_quad_kernel<T, S>, qs);
         CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_quad_kernel<T, S>, kXferThreads, qs));
         p2gq_ctas = std::max(1, per) * nsm;
-        CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S, 1>, kG2PThreads, 0));
+        g2p_attr(g2p_tile_kernel<T, S, 1>);
+        CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S, 1>, kG2PThreads,
+                                                               g2p_dyn_smem<T>()));
         g2pq_ctas = std::max(1, per) * nsm;
       }
     }
@@ -718,7 +728,7 @@ struct Context final : CtxBase {
   void enqueue_g2p(const StepConst<T>& c, int step_idx) {
     if (quad()) {
       if constexpr (S != kSchemeMls)
-        g2p_tile_kernel<T, S, 1><<<g2pq_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir,
+        g2p_tile_kernel<T, S, 1><<<g2pq_ctas, kG2PThreads, g2p_dyn_smem<T>(), st>>>(state(cur), state(cur ^ 1), perm, c, dir,
                                                                      rec, pool, pool_cap, dstat, step_idx);
       return;
     }
@@ -727,13 +737,13 @@ struct Context final : CtxBase {
     for (int m = 0; m < cfg.n_materials; ++m)
       mm |= cfg.materials[m].model == kModelFC ? kMFC : cfg.materials[m].model == kModelDP ? kMDP : kMFluid;
     if (mm == kMFC || mm == 0)
-      g2p_tile_kernel<T, S, 0, kMFC><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir,
+      g2p_tile_kernel<T, S, 0, kMFC><<<g2p_ctas, kG2PThreads, g2p_dyn_smem<T>(), st>>>(state(cur), state(cur ^ 1), perm, c, dir,
                                                                        rec, pool, pool_cap, dstat, step_idx);
     else if (mm == kMDP)
-      g2p_tile_kernel<T, S, 0, kMDP><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir,
+      g2p_tile_kernel<T, S, 0, kMDP><<<g2p_ctas, kG2PThreads, g2p_dyn_smem<T>(), st>>>(state(cur), state(cur ^ 1), perm, c, dir,
                                                                        rec, pool, pool_cap, dstat, step_idx);
     else
-      g2p_tile_kernel<T, S><<<g2p_ctas, kG2PThreads, 0, st>>>(state(cur), state(cur ^ 1), perm, c, dir, rec, pool,
+      g2p_tile_kernel<T, S><<<g2p_ctas, kG2PThreads, g2p_dyn_smem<T>(), st>>>(state(cur), state(cur ^ 1), perm, c, dir, rec, pool,
                                                                 pool_cap, dstat, step_idx);
   }
 

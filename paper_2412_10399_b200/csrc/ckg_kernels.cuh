@@ -183,28 +183,25 @@ __device__ __forceinline__ int axis_base(T x, T dx, T inv_dx, int pow2, T kq) {
 // |2 pi t| <= pi/4 is below 1e-16 relative; ~1-2 ulp overall, branch-free, two
 // independent FMA chains (the library sincospi costs ~70 instructions with its
 // general range reduction).
+// Polynomial coefficients in the constant bank: DFMA reads c[bank][off]
+// operands directly, where literal FP64 constants cost two uniform-register
+// moves (UMOV) per use in every unrolled evaluation.
+__constant__ double kSinPoly[8] = {-0.7181223017785006, 3.819952584848282,  -15.09464257682299, 42.058693944897655,
+                                   -76.70585975306139,  81.60524927607506,  -41.34170224039976, 6.283185307179586};
+__constant__ double kCosPoly[9] = {0.28200596845579123, -1.714390711088672, 7.903536371318469,
+                                   -26.4262567833744,   60.24464137187666,  -85.45681720669373,
+                                   64.9393940226683,    -19.739208802178716, 1.0};
 __device__ __forceinline__ void sincos_2pi(double f, double* s, double* c) {
   const double r = f - rint(f);
   const double qd = rint(4.0 * r);
   const double t = fma(qd, -0.25, r);
   const double t2 = t * t;
-  double ps = -0.7181223017785006;
-  ps = fma(ps, t2, 3.819952584848282);
-  ps = fma(ps, t2, -15.09464257682299);
-  ps = fma(ps, t2, 42.058693944897655);
-  ps = fma(ps, t2, -76.70585975306139);
-  ps = fma(ps, t2, 81.60524927607506);
-  ps = fma(ps, t2, -41.34170224039976);
-  ps = fma(ps, t2, 6.283185307179586);
-  double pc = 0.28200596845579123;
-  pc = fma(pc, t2, -1.714390711088672);
-  pc = fma(pc, t2, 7.903536371318469);
-  pc = fma(pc, t2, -26.4262567833744);
-  pc = fma(pc, t2, 60.24464137187666);
-  pc = fma(pc, t2, -85.45681720669373);
-  pc = fma(pc, t2, 64.9393940226683);
-  pc = fma(pc, t2, -19.739208802178716);
-  pc = fma(pc, t2, 1.0);
+  double ps = kSinPoly[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) ps = fma(ps, t2, kSinPoly[k]);
+  double pc = kCosPoly[0];
+#pragma unroll
+  for (int k = 1; k < 9; ++k) pc = fma(pc, t2, kCosPoly[k]);
   const double sn = t * ps;
   const int q = int(qd) & 3;  // quadrant: angle = 2 pi t + q pi/2
   *s = (q == 0) ? sn : (q == 1) ? pc : (q == 2) ? -sn : -pc;
@@ -226,6 +223,51 @@ __device__ __forceinline__ Axis<T> axis_pair(T x, T dx, T inv_dx, int pow2, T kq
   a.w1 = f - sn;
   a.g0 = (cs - T(1)) * inv_dx;
   a.xi0 = (T(a.base) + kq) * dx - x;
+  return a;
+}
+
+// One axis of one grid from a given sin/cos(2 pi f) (unscaled): the same
+// operations as axis_pair after its sincos.
+template <typename T>
+__device__ __forceinline__ Axis<T> axis_with(T x, T dx, T inv_dx, int pow2, T kq, T sn, T cs) {
+  const T s = sub_rn(over_dx(x, dx, inv_dx, pow2), kq);
+  const T fb = dfloor(s);
+  Axis<T> a;
+  a.base = static_cast<int>(fb);
+  const T f = s - fb;
+  sn = sn * TwoPi<T>::inv;
+  a.w0 = T(1) - f + sn;
+  a.w1 = f - sn;
+  a.g0 = (cs - T(1)) * inv_dx;
+  a.xi0 = (T(a.base) + kq) * dx - x;
+  return a;
+}
+
+// The -1 grid's axis (kq = -1/4) from the +1 grid's sincos when the two
+// fractions differ by exactly 1/2 (sin/cos(2 pi (f + 1/2)) = -sin/cos(2 pi f),
+// as axis_pair_dual); *snp / *csp return the +1 grid's (unscaled) values.
+template <typename T>
+__device__ __forceinline__ Axis<T> axis_pair_lo(T x, T dx, T inv_dx, int pow2, T* snp, T* csp) {
+  const T xd = over_dx(x, dx, inv_dx, pow2);
+  const T sm = sub_rn(xd, T(-0.25)), sp = sub_rn(xd, T(0.25));
+  const T fbm = dfloor(sm), fbp = dfloor(sp);
+  const T fm = sm - fbm, fp = sp - fbp;
+  T sn, cs;
+  sincos_2pi(fp, snp, csp);
+  const T d = fm - fp;
+  if (d == T(0.5) || d == T(-0.5)) {
+    sn = -*snp;
+    cs = -*csp;
+  } else {
+    sincos_2pi(fm, &sn, &cs);
+  }
+  Axis<T> a;
+  a.base = static_cast<int>(fbm);
+  sn = sn * TwoPi<T>::inv;
+  a.w0 = T(1) - fm + sn;
+  a.w1 = fm - sn;
+  a.g0 = (cs - T(1)) * inv_dx;
+  a.xi0 = (T(a.base) + T(-0.25)) * dx - x;
   return a;
 }
 

@@ -48,6 +48,9 @@ constexpr int kXferWarps = kXferThreads / 32;
 #ifndef CKG_G2P_DUAL
 #define CKG_G2P_DUAL 0
 #endif
+#ifndef CKG_G2P_DUAL_SINCOS
+#define CKG_G2P_DUAL_SINCOS 1  // G2P: one sincos per axis for both grids
+#endif
 #ifndef CKG_P2G_EXP
 #define CKG_P2G_EXP 0  // development experiments only (1: no node ordering, 2: no tile RMW)
 #endif
@@ -75,6 +78,10 @@ constexpr int kXferWarps = kXferThreads / 32;
 #define CKG_G2P_MINB_F32 4
 #endif
 constexpr int kG2PThreads = CKG_G2P_THREADS;
+template <typename T>
+constexpr size_t g2p_dyn_smem() {
+  return CKG_G2P_DUAL_SINCOS ? size_t(6) * kG2PThreads * sizeof(T) : 0;
+}
 constexpr int kG2PWarps = kG2PThreads / 32;
 constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full lattice block)
 
@@ -307,6 +314,71 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
   }
 }
 
+// One grid's 8-node scatter of one particle (scatter_one, transfer.hpp:
+// 235-283) in separable form: with w = wx_s wy_t wz_u, grad w = (gx_s wy_t
+// wz_u, wx_s gy_t wz_u, wx_s wy_t gz_u) (g1 = -g0 per axis) and the node
+// momentum base b = u0 + dx (s, t, u) . Q_a, the contribution
+// w b - A grad w regroups exactly into
+//   mass(s,t,u)  = (m wx_s) (wy_t wz_u)
+//   mom_a(s,t,u) = X_a(s) (wy_t wz_u) + wx_s (Y_a(t) wz_u + wy_t Z_a(u)),
+//   X_a(s) = wx_s (u0_a + s dx Q_a0) - A_a0 gx_s,  Y_a(t) = t dx Q_a1 wy_t - A_a1 gy_t,
+//   Z_a(u) = u dx Q_a2 wz_u - A_a2 gz_u
+// (~130 FP64 operations per grid instead of ~200; same sum up to the
+// rounding of the regrouping).  Node offsets are visited in the order
+// (t, u) outer, s inner so each Y/Z pair is formed once.
+#ifndef CKG_P2G_SEPARABLE
+#define CKG_P2G_SEPARABLE 1
+#endif
+template <typename T, int SCHEME, bool SWZ>
+__device__ __forceinline__ void scatter_separable(const Axis<T> (&ax)[3], T m, const T (&u0)[3], const M3<T>& Q,
+                                                  const M3<T>& Ap, T dx, T* tb, T* p0, int g, int lx, int ly,
+                                                  int lz, int E, int VS, uint32_t tmask) {
+  const T wx0 = ax[0].w0, wx1 = ax[0].w1, wy0 = ax[1].w0, wy1 = ax[1].w1, wz0 = ax[2].w0, wz1 = ax[2].w1;
+  const T gx = ax[0].g0, gy = ax[1].g0, gz = ax[2].g0;
+  T X0[3], X1[3], Y0[3], Y1[3], Z0[3], Z1[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const T u = u0[a];
+    X0[a] = wx0 * u - Ap.a[a][0] * gx;
+    Y0[a] = -(Ap.a[a][1] * gy);
+    Z0[a] = -(Ap.a[a][2] * gz);
+    if constexpr (SCHEME != kSchemePic) {
+      X1[a] = wx1 * fma(Q.a[a][0], dx, u) + Ap.a[a][0] * gx;
+      Y1[a] = (Q.a[a][1] * dx) * wy1 + Ap.a[a][1] * gy;
+      Z1[a] = (Q.a[a][2] * dx) * wz1 + Ap.a[a][2] * gz;
+    } else {
+      X1[a] = wx1 * u + Ap.a[a][0] * gx;
+      Y1[a] = Ap.a[a][1] * gy;
+      Z1[a] = Ap.a[a][2] * gz;
+    }
+  }
+  const T mw0 = m * wx0, mw1 = m * wx1;
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const T wyt = t ? wy1 : wy0, wzu = u ? wz1 : wz0;
+      const T wyz = wyt * wzu;
+      T YZ[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) YZ[a] = (t ? Y1[a] : Y0[a]) * wzu + wyt * (u ? Z1[a] : Z0[a]);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        T o[4];
+        o[0] = (s ? mw1 : mw0) * wyz;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) o[1 + a] = (s ? X1[a] : X0[a]) * wyz + (s ? wx1 : wx0) * YZ[a];
+        if constexpr (SWZ)
+          tile_add4(tb + P2GTile<T>::slot(g, lx + s, ly + t, lz + u), o, VS);
+        else
+          tile_add4(p0 + (s * E + t) * E + u, o, VS);
+        // node (s,t,u) of one lane can be another offset's node of its
+        // neighbour: order the read-modify-writes across lanes
+        __syncwarp(tmask);
+      }
+    }
+}
+
 template <typename T, int SCHEME>
 __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB))
     p2g_tile_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
@@ -406,11 +478,11 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
       if (valid) {
         // every field load is issued before the first use
         const uint64_t n = cur.stride;  // field stride (buffer capacity)
+        T v3[3], t6[6];
         x = __ldg(cur.f + kX * n + src);
         y = __ldg(cur.f + (kX + 1) * n + src);
         z = __ldg(cur.f + (kX + 2) * n + src);
         m = __ldg(cur.f + kMass * n + src);
-        T v3[3], t6[6];
 #pragma unroll
         for (int k = 0; k < 3; ++k) v3[k] = __ldg(cur.f + (kV + k) * n + src);
 #pragma unroll
@@ -534,6 +606,9 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
           // fast path: every lane owns a distinct base cell in this warp, so
           // at a fixed node offset all lanes write distinct nodes
           if (in_tile) {
+            if constexpr (SCHEME != kSchemeMls && CKG_P2G_SEPARABLE) {
+              scatter_separable<T, SCHEME, L::kSwz>(ax, m, u0, Q, Ap, dx, tb, p0, g, lx, ly, lz, E, VS, tmask);
+            } else {
 #pragma unroll
             for (int s = 0; s < 2; ++s)
 #pragma unroll
@@ -550,6 +625,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
                   // neighbour: order the read-modify-writes across lanes
                   __syncwarp(tmask);
                 }
+            }
           }
         } else {
           // shared base cells: serialise by rank layers (rolled loop)
@@ -862,6 +938,9 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
   // per-thread prefetch (cp.async, issued before the gather) of the state the
   // particle update reads after it: F (9), J, mass, V0
   __shared__ T pst[12][kG2PThreads];
+  // (dynamic) per-thread +1 grid sin/cos (unscaled) of the three axes, see
+  // the gather (CKG_G2P_DUAL_SINCOS)
+  extern __shared__ __align__(16) unsigned char g2p_dyn[];
   __shared__ uint32_t s_rec[kRecNbr + 27];
   __shared__ uint32_t s_item;
   __shared__ T wmax[kG2PWarps];
@@ -967,6 +1046,9 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
         }
         mi = __ldg(cur.mat + src);
         T* gs = &gst[0][tid];  // gs[k * kG2PThreads]
+#if CKG_G2P_DUAL_SINCOS
+        T* sc6 = reinterpret_cast<T*>(g2p_dyn) + tid;  // sc6[k * kG2PThreads], k < 6
+#endif
         if (KQ) {
           // quadratic baseline: 27 nodes of grid slot 0 (transfer.hpp:512-543)
           T v[3];
@@ -1006,8 +1088,30 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
 #pragma unroll
         for (int g = 0; g < (KQ ? 0 : 2); ++g) {
           const T kq = g == 0 ? T(-0.25) : T(0.25);
+#if CKG_G2P_DUAL_SINCOS
+          // one sincos per axis for both grids: the -1 and +1 grid fractions
+          // differ by exactly 1/2 (sin/cos flip sign; axis_pair_dual), the
+          // +1 grid's values wait in the thread's shared-memory stash
+          Axis<T> ax[3];
+          {
+            const T p3[3] = {x, y, z};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              if (g == 0) {
+                T snp, csp;
+                ax[a] = axis_pair_lo(p3[a], dx, c.inv_dx, c.pow2, &snp, &csp);
+                sc6[(2 * a) * kG2PThreads] = snp;
+                sc6[(2 * a + 1) * kG2PThreads] = csp;
+              } else {
+                ax[a] = axis_with(p3[a], dx, c.inv_dx, c.pow2, T(0.25), sc6[(2 * a) * kG2PThreads],
+                                  sc6[(2 * a + 1) * kG2PThreads]);
+              }
+            }
+          }
+#else
           const Axis<T> ax[3] = {axis_pair(x, dx, c.inv_dx, c.pow2, kq), axis_pair(y, dx, c.inv_dx, c.pow2, kq),
                                  axis_pair(z, dx, c.inv_dx, c.pow2, kq)};
+#endif
           const int lx = ax[0].base - (4 * bx - g), ly = ax[1].base - (4 * by - g), lz = ax[2].base - (4 * bz - g);
           const bool in_tile =
               lx >= 0 && ly >= 0 && lz >= 0 && lx <= kTileN - 2 && ly <= kTileN - 2 && lz <= kTileN - 2;
