@@ -371,7 +371,7 @@ __device__ __forceinline__ int return_map_dp(M3<T>& F, T alpha, T mu, T lambda, 
   if (!(det(F) > T(0))) return kErrReturnMap;
   M3<T> U, V;
   V3<T> sg;
-  svd3(F, U, sg, V);
+  svd3_inl(F, U, sg, V);
   T e0 = dlog(sg.x), e1 = dlog(sg.y), e2 = dlog(sg.z);
   T tr = e0 + e1 + e2;
   bool project = true;

@@ -280,6 +280,116 @@ __device__ __noinline__ void svd3(const M3<T>& F, M3<T>& U, V3<T>& sigma, M3<T>&
   sigma = {dot(u0, b[0]), dot(u1, b[1]), dot(u2, b[2])};
 }
 
+// One Jacobi rotation on the (p,q) pair without the division by a_pq of
+// jacobi_rotate: with d = a_qq - a_pp, t = tan of the rotation angle is
+//   t = sgn(theta) 2|a_pq| / (|d| + sqrt(d^2 + 4 a_pq^2)),  theta = d / (2 a_pq)
+// (the same root as math.hpp:211-213 multiplied through by |2 a_pq|, so a
+// zero a_pq gives t = 0, the identity rotation, with no branch).
+template <int p, int q, typename T>
+__device__ __forceinline__ void jacobi_rotate_nb(M3<T>& A, M3<T>& V) {
+  constexpr int r = 3 - p - q;
+  const T app = A.a[p][p], aqq = A.a[q][q], apq = A.a[p][q];
+  const T d = aqq - app, a2 = T(2) * dabs(apq);
+  const T den = dabs(d) + dsqrt(d * d + a2 * a2);
+  T t = den > T(0) ? a2 / den : T(0);
+  if (d * apq < T(0)) t = -t;  // sgn(theta); theta = +-0 counts as positive (math.hpp:212)
+  const T c = T(1) / dsqrt(t * t + T(1));
+  const T sn = t * c;
+  A.a[p][p] = c * c * app - T(2) * sn * c * apq + sn * sn * aqq;
+  A.a[q][q] = sn * sn * app + T(2) * sn * c * apq + c * c * aqq;
+  A.a[p][q] = A.a[q][p] = T(0);
+  const T arp = A.a[r][p], arq = A.a[r][q];
+  A.a[r][p] = A.a[p][r] = c * arp - sn * arq;
+  A.a[r][q] = A.a[q][r] = sn * arp + c * arq;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const T vip = V.a[i][p], viq = V.a[i][q];
+    V.a[i][p] = c * vip - sn * viq;
+    V.a[i][q] = sn * vip + c * viq;
+  }
+}
+
+// svd3 (math.hpp:249-292) for the hot path (Drucker-Prager return map in
+// G2P): inlined and register-resident (no call, no by-reference outputs in
+// local memory), the reference's cyclic Jacobi of F^T F with its stopping
+// test before every sweep (a settled sand grain's F^T F is diagonal to
+// round-off and exits at once; measured: four unconditional sweeps cost the
+// 10M DP block's G2P 1.79 -> 2.68 ms) and branch-free rotations.  U, sigma
+// follow svd3.
+template <typename T>
+__device__ __forceinline__ void svd3_inl(const M3<T>& F, M3<T>& U, V3<T>& sigma, M3<T>& V_out) {
+  M3<T> A;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      A.a[i][j] = F.a[0][i] * F.a[0][j] + F.a[1][i] * F.a[1][j] + F.a[2][i] * F.a[2][j];
+  M3<T> V = m3_identity<T>();
+#pragma unroll 1
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    const T off = dabs(A.a[0][1]) + dabs(A.a[0][2]) + dabs(A.a[1][2]);
+    const T dg = dabs(A.a[0][0]) + dabs(A.a[1][1]) + dabs(A.a[2][2]);
+    if (off <= Lim<T>::eps * (dg + Lim<T>::tiny)) break;
+    jacobi_rotate_nb<0, 1>(A, V);
+    jacobi_rotate_nb<0, 2>(A, V);
+    jacobi_rotate_nb<1, 2>(A, V);
+  }
+  // descending eigenvalues (insertion-sort tie behaviour), det V = +1
+  int i0 = 0, i1 = 1, i2 = 2;
+  T a0 = A.a[0][0], a1 = A.a[1][1], a2 = A.a[2][2];
+  if (a1 > a0) { T t = a0; a0 = a1; a1 = t; int ti = i0; i0 = i1; i1 = ti; }
+  if (a2 > a1) {
+    T t = a1; a1 = a2; a2 = t; int ti = i1; i1 = i2; i2 = ti;
+    if (a1 > a0) { T t2 = a0; a0 = a1; a1 = t2; int tj = i0; i0 = i1; i1 = tj; }
+  }
+  M3<T> Vs;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const T c0 = V.a[r][0], c1 = V.a[r][1], c2 = V.a[r][2];
+    Vs.a[r][0] = i0 == 0 ? c0 : (i0 == 1 ? c1 : c2);
+    Vs.a[r][1] = i1 == 0 ? c0 : (i1 == 1 ? c1 : c2);
+    Vs.a[r][2] = i2 == 0 ? c0 : (i2 == 1 ? c1 : c2);
+  }
+  if (det(Vs) < T(0)) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) Vs.a[r][2] = -Vs.a[r][2];
+  }
+  V_out = Vs;
+  V3<T> b[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    b[c] = {F.a[0][0] * Vs.a[0][c] + F.a[0][1] * Vs.a[1][c] + F.a[0][2] * Vs.a[2][c],
+            F.a[1][0] * Vs.a[0][c] + F.a[1][1] * Vs.a[1][c] + F.a[1][2] * Vs.a[2][c],
+            F.a[2][0] * Vs.a[0][c] + F.a[2][1] * Vs.a[1][c] + F.a[2][2] * Vs.a[2][c]};
+  const T sc = dsqrt(a0 < T(0) ? T(0) : a0);
+  const T tiny = sc * T(1e-12) + Lim<T>::tiny;
+  V3<T> u0 = b[0];
+  const T n0 = dsqrt(dot(u0, u0));
+  if (n0 > tiny) {
+    const T s = T(1) / n0;
+    u0 = {u0.x * s, u0.y * s, u0.z * s};
+  } else {
+    u0 = {T(1), T(0), T(0)};
+  }
+  const T d = dot(b[1], u0);
+  V3<T> u1 = {b[1].x - u0.x * d, b[1].y - u0.y * d, b[1].z - u0.z * d};
+  const T n1 = dsqrt(dot(u1, u1));
+  if (n1 > tiny) {
+    const T s = T(1) / n1;
+    u1 = {u1.x * s, u1.y * s, u1.z * s};
+  } else {
+    const V3<T> seed = dabs(u0.x) < T(0.9) ? V3<T>{T(1), T(0), T(0)} : V3<T>{T(0), T(1), T(0)};
+    u1 = cross(u0, seed);
+    const T s = T(1) / dsqrt(dot(u1, u1));
+    u1 = {u1.x * s, u1.y * s, u1.z * s};
+  }
+  const V3<T> u2 = cross(u0, u1);
+  U.a[0][0] = u0.x; U.a[1][0] = u0.y; U.a[2][0] = u0.z;
+  U.a[0][1] = u1.x; U.a[1][1] = u1.y; U.a[2][1] = u1.z;
+  U.a[0][2] = u2.x; U.a[1][2] = u2.y; U.a[2][2] = u2.z;
+  sigma = {dot(u0, b[0]), dot(u1, b[1]), dot(u2, b[2])};
+}
+
 // polar_rotation (math.hpp:300-321): scaled Newton R <- (gR + (gR)^-T)/2 with
 // the reference's stopping rule; SVD construction for near-singular input.
 template <typename T>

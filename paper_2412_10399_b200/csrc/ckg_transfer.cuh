@@ -336,9 +336,19 @@ __device__ __forceinline__ void scatter_separable(const Axis<T> (&ax)[3], T m, c
   const T wx0 = ax[0].w0, wx1 = ax[0].w1, wy0 = ax[1].w0, wy1 = ax[1].w1, wz0 = ax[2].w0, wz1 = ax[2].w1;
   const T gx = ax[0].g0, gy = ax[1].g0, gz = ax[2].g0;
   T X0[3], X1[3], Y0[3], Y1[3], Z0[3], Z1[3];
+  // MLS: the force is already folded into u0 / Q (no gradient term)
+  constexpr bool kGrad = SCHEME != kSchemeMls;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const T u = u0[a];
+    if constexpr (!kGrad) {
+      X0[a] = wx0 * u;
+      X1[a] = wx1 * fma(Q.a[a][0], dx, u);
+      Y0[a] = Z0[a] = T(0);
+      Y1[a] = (Q.a[a][1] * dx) * wy1;
+      Z1[a] = (Q.a[a][2] * dx) * wz1;
+      continue;
+    }
     X0[a] = wx0 * u - Ap.a[a][0] * gx;
     Y0[a] = -(Ap.a[a][1] * gy);
     Z0[a] = -(Ap.a[a][2] * gz);
@@ -522,6 +532,26 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
             record_error(st, step, kPhaseP2G, sorted_index(), 0, kErrSingularMls);
             valid = false;
           }
+          // scatter_force_mls_one (transfer.hpp:335-369) adds -A' w (M^-1
+          // P(xi))_{1..3} per node, P(xi) = (1, xi): with K = A' M^-1_{1..3,:}
+          // (3 x 4) that is -w (K_0 + K_{1..3} xi), an affine function of the
+          // node offset like the APIC term w (m v + Q xi).  Folded into the
+          // latter (Q <- Q - K_{1..3}, m v <- m v - K_0) the MLS node
+          // contribution is the APIC one without a gradient term.
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            T k4[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              k4[k] = Ap.a[a][0] * Minv[1][k] + Ap.a[a][1] * Minv[2][k] + Ap.a[a][2] * Minv[3][k];
+            mv[a] -= k4[0];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) Q.a[a][j] -= k4[1 + j];
+          }
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) Ap.a[a][b] = T(0);
         }
       }
       // ---- scatter, grid by grid.  Only one grid's stencil is live during
@@ -574,18 +604,12 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
           const T wxs = s ? ax[0].w1 : ax[0].w0, wyt = t ? ax[1].w1 : ax[1].w0, wzu = u ? ax[2].w1 : ax[2].w0;
           const T wyz = wyt * wzu;
           const T w = wxs * wyz;
-          T gw0, gw1, gw2;
-          if (SCHEME != kSchemeMls) {
+          T gw0 = T(0), gw1 = T(0), gw2 = T(0);
+          if (SCHEME != kSchemeMls) {  // MLS: force folded into u0 / Q above
             const T gxs = s ? -ax[0].g0 : ax[0].g0, gyt = t ? -ax[1].g0 : ax[1].g0, gzu = u ? -ax[2].g0 : ax[2].g0;
             gw0 = gxs * wyz;
             gw1 = wxs * (gyt * wzu);
             gw2 = wxs * (wyt * gzu);
-          } else {
-            const T P1 = ax[0].xi0 + (s ? dx : T(0)), P2 = ax[1].xi0 + (t ? dx : T(0)),
-                    P3 = ax[2].xi0 + (u ? dx : T(0));
-            gw0 = w * (Minv[1][0] + Minv[1][1] * P1 + Minv[1][2] * P2 + Minv[1][3] * P3);
-            gw1 = w * (Minv[2][0] + Minv[2][1] * P1 + Minv[2][2] * P2 + Minv[2][3] * P3);
-            gw2 = w * (Minv[3][0] + Minv[3][1] * P1 + Minv[3][2] * P2 + Minv[3][3] * P3);
           }
           o[0] = w * m;
 #pragma unroll
@@ -597,7 +621,8 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
               if (t) b = fma(Q.a[a][1], dx, b);
               if (u) b = fma(Q.a[a][2], dx, b);
             }
-            o[1 + a] = w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
+            o[1 + a] = SCHEME == kSchemeMls ? w * b
+                                             : w * b - (Ap.a[a][0] * gw0 + Ap.a[a][1] * gw1 + Ap.a[a][2] * gw2);
           }
         };
         T* tb = wt + g * 4 * L::N0;  // this grid's tile
@@ -606,7 +631,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
           // fast path: every lane owns a distinct base cell in this warp, so
           // at a fixed node offset all lanes write distinct nodes
           if (in_tile) {
-            if constexpr (SCHEME != kSchemeMls && CKG_P2G_SEPARABLE) {
+            if constexpr (CKG_P2G_SEPARABLE) {
               scatter_separable<T, SCHEME, L::kSwz>(ax, m, u0, Q, Ap, dx, tb, p0, g, lx, ly, lz, E, VS, tmask);
             } else {
 #pragma unroll
