@@ -114,7 +114,10 @@ typedef struct ckg_config {
   double gravity[3];
   double mass_eps;       /* Simulation::compute_mass_epsilon (simulation.hpp:227-232) */
   int32_t clamp_singular;
-  int32_t deterministic; /* fixed-order reduction mode */
+  int32_t deterministic; /* the reference's serial-scatter switch (simulation.hpp:326-327): P2G node sums are
+                            formed in a fixed order (per-block tiles summed by key-block offset, out-of-tile
+                            records in particle order), so single-domain runs are bitwise reproducible on
+                            the same GPU (not bitwise equal to the CPU engine); x-slab ranks ignore it */
   double clamp_floor;
   int32_t n_materials;
   int32_t n_boundaries;

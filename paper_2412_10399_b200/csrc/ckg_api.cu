@@ -199,6 +199,22 @@ struct Context final : CtxBase {
   double pend_dt = 0;
   int fused_ctas = 0;
   uint32_t* act_alt = nullptr;  // the previous substep's active list (fused mode)
+  // deterministic mode (cfg.deterministic; det_gather_kernel): per active
+  // block P2G tiles summed in a fixed order, out-of-tile records applied in
+  // particle order.  Single domain only.
+  bool det = false;
+  T* dtile = nullptr;
+  uint32_t dcap = 0;
+  DetSpill<T>* dspill = nullptr;
+  DetBuf<T> detbuf() const {
+    if (!det || slab) return DetBuf<T>{nullptr, 0u, nullptr, 0u};
+    return DetBuf<T>{dtile, dcap, dspill, uint32_t(kDetSpillMax)};
+  }
+  void set_det_cap(uint32_t c) {
+    dfree(dtile);
+    dcap = c;
+    dtile = dalloc<T>(uint64_t(c) * kDetVals);
+  }
   T* facade_pool = nullptr;  // pool the grid facade reads (fused mode)
   // status
   DevStatus* dstat = nullptr;
@@ -284,6 +300,11 @@ struct Context final : CtxBase {
     }
     CKG_CUDA(cudaMemcpy(dbcs, hb.data(), sizeof(BcParam<T>) * kMaxBoundaries, cudaMemcpyHostToDevice));
     dacc = dalloc<double>(12);
+    if (c.deterministic) {
+      det = true;
+      set_det_cap(std::min<uint32_t>(pool_cap, 1u << 16));
+      dspill = dalloc<DetSpill<T>>(kDetSpillMax);
+    }
     // fused G2P2G (opt-in: CKG_FLAG_FUSED or CKMPM_FUSED=1)
     const char* fe = std::getenv("CKMPM_FUSED");
     if (((fe && fe[0] == '1') || (cfg.flags & CKG_FLAG_FUSED)) && fused_supported()) enable_fused();
@@ -292,7 +313,7 @@ struct Context final : CtxBase {
   bool is_fused() const override { return fused; }
 
   bool fused_supported() const {
-    return !quad() && cfg.scheme != CKG_SCHEME_MLS && !slab && pool_cap >= nd;
+    return !quad() && cfg.scheme != CKG_SCHEME_MLS && !slab && !det && pool_cap >= nd;
   }
 
   template <int S, int MM>
@@ -389,6 +410,8 @@ struct Context final : CtxBase {
       dfree(dpool[1]);
       dfree(act_alt);
     }
+    dfree(dtile);
+    dfree(dspill);
     dfree(pool);
     dfree(dstat);
     dfree(dbcs);
@@ -721,8 +744,14 @@ struct Context final : CtxBase {
             state(cur), perm, c, dir, active, seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
       return;
     }
+    const DetBuf<T> db = detbuf();
     p2g_tile_kernel<T, S><<<p2g_ctas, kP2GThreads, p2g_smem_bytes<T>(), st>>>(
-        state(cur), perm, c, dir, rec, cord, ccnt, pool, pool_cap, dstat, step_idx);
+        state(cur), perm, c, dir, rec, cord, ccnt, pool, pool_cap, dstat, step_idx, db);
+    if (db.tile) {
+      det_gather_kernel<T><<<148 * 8, 256, 0, st>>>(pool, active, dir, db.tile, db.cap, dstat, pool_cap, D);
+      det_spill_kernel<T><<<1, 1024, 0, st>>>(pool, dir, db.spill, dstat, pool_cap, D);
+      launches += 2;
+    }
   }
   template <int S>
   void enqueue_g2p(const StepConst<T>& c, int step_idx) {
@@ -770,7 +799,8 @@ struct Context final : CtxBase {
     if (timed) CKG_CUDA(cudaEventRecord(ev[1], st));
     if (stop_after >= CKG_PHASE_ACTIVATE) enqueue_activate(step_idx);
     if (timed) CKG_CUDA(cudaEventRecord(ev[2], st));
-    if (stop_after >= CKG_PHASE_CLEAR) clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
+    // (deterministic mode: the tile gather writes every node of the active blocks)
+    if (stop_after >= CKG_PHASE_CLEAR && !detbuf().tile) clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
     if (timed) CKG_CUDA(cudaEventRecord(ev[3], st));
     if (stop_after >= CKG_PHASE_P2G) {
       if (!stress_valid) {
@@ -1026,11 +1056,13 @@ struct Context final : CtxBase {
       }
       CKG_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
       CKG_CUDA(cudaStreamSynchronize(st));
-      if (hstat->overflow && !fused) {
+      if ((hstat->overflow & 3u) && !fused) {
         ko_valid = false;
-        // grow the pool (state untouched: G2P writes the other buffer)
-        uint64_t want = std::min<uint64_t>(nd, uint64_t(hstat->n_active) * 5 / 4 + 64);
-        set_pool_cap(uint32_t(want));
+        // grow the pool / the deterministic tile buffer (state untouched:
+        // G2P writes the other buffer)
+        const uint64_t want = std::min<uint64_t>(nd, uint64_t(hstat->n_active) * 5 / 4 + 64);
+        if (hstat->overflow & 1u) set_pool_cap(uint32_t(want));
+        if (hstat->overflow & 2u) set_det_cap(uint32_t(std::min<uint64_t>(want, pool_cap)));
         continue;
       }
       break;
@@ -1042,6 +1074,11 @@ struct Context final : CtxBase {
     out->substeps_done = 0;
     grid_valid = true;
     last_active = hstat->n_active;
+    if (hstat->overflow & 4u) {
+      last_error = "deterministic mode: more than 4096 out-of-tile particles in one substep";
+      out->status = CKG_ERR_DEVICE;
+      return CKG_ERR_DEVICE;
+    }
     if (hstat->overflow) {
       last_error = "grid block pool capacity exceeded";
       out->status = CKG_ERR_DEVICE;
@@ -1262,7 +1299,9 @@ struct Context final : CtxBase {
   // The graph needs: the stored-order keys (incremental sort), a valid stress
   // cache, a pool that cannot overflow (sized for the whole directory) and a
   // single domain.
-  bool graph_ready() const { return !fused && !slab && n > 0 && ko_valid && stress_valid && pool_cap >= nd; }
+  bool graph_ready() const {
+    return !fused && !det && !slab && n > 0 && ko_valid && stress_valid && pool_cap >= nd;
+  }
 
   // Host-side bookkeeping of one completed host-loop substep (gather_all + the
   // loop body of advance_frame).  Returns true when the frame continues.

@@ -86,6 +86,7 @@ struct DevStatus {
   unsigned int grid_lo, grid_hi;    // slot range of the grid update
   unsigned int clear_lo, clear_hi;  // slot range cleared before P2G
   unsigned long long perr;      // packed error of the NEXT substep's scatter (fused G2P2G), ~0 = none
+  unsigned int spill_n;         // deterministic mode: out-of-tile P2G records
 };
 
 // err = step<<56 | phase<<52 | particle<<12 | axis<<8 | code

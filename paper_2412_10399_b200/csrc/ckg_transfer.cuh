@@ -113,6 +113,25 @@ constexpr int kWarpVals = 4 * kPTNodes + 4 * kT1Nodes;
 #ifndef CKG_P2G_SWZ_F32
 #define CKG_P2G_SWZ_F32 0
 #endif
+// Deterministic-mode buffers (det_gather_kernel): per active block its summed
+// P2G tile in the flush layout (-1 grid 4 x 5^3, then +1 grid 4 x 6^3), and
+// the out-of-tile particle contributions.
+constexpr int kDetVals = 4 * kPTNodes + 4 * kTileNodes;  // 1364
+template <typename T>
+struct DetSpill {
+  uint32_t idx;  // sorted particle index
+  int g;         // grid
+  int base[3];   // stencil base
+  T v[8][4];     // m, px, py, pz of the 8 nodes
+};
+template <typename T>
+struct DetBuf {
+  T* tile;  // null: REDG mode
+  uint32_t cap;
+  DetSpill<T>* spill;
+  uint32_t spill_cap;
+};
+
 template <typename T>
 struct P2GTile {
   static constexpr bool kSwz = sizeof(T) == 4 && CKG_P2G_SWZ_F32 && CKG_P2G_T1FULL;
@@ -394,7 +413,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
     p2g_tile_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
                     const uint32_t* __restrict__ cord, const uint4* __restrict__ ccnt,
-                    T* __restrict__ pool, uint32_t cap, DevStatus* st, int step) {
+                    T* __restrict__ pool, uint32_t cap, DevStatus* st, int step, DetBuf<T> det) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tiles = reinterpret_cast<T*>(smem_raw);
   // Items are claimed two ahead: while item k is processed, warp 0's claim of
@@ -666,7 +685,28 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
             }
           }
         }
-        if (valid && !in_tile) {
+        if (valid && !in_tile && det.tile) {
+          // deterministic mode: the contribution is recorded and applied in
+          // sorted-particle order after the tile gather (det_spill_kernel)
+          const uint32_t k = atomicAdd(&st->spill_n, 1u);
+          if (k >= det.spill_cap) {
+            atomicOr(&st->overflow, 4u);
+          } else {
+            DetSpill<T>& e = det.spill[k];
+            e.idx = sorted_index();
+            e.g = g;
+            e.base[0] = ax[0].base;
+            e.base[1] = ax[1].base;
+            e.base[2] = ax[2].base;
+#pragma unroll 1
+            for (int nid = 0; nid < 8; ++nid) {
+              T o[4];
+              contrib(nid >> 2, (nid >> 1) & 1, nid & 1, o);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) e.v[nid][q] = o[q];
+            }
+          }
+        } else if (valid && !in_tile) {
           // footprint outside the block tile: direct REDs through the directory
 #pragma unroll 1
           for (int nid = 0; nid < 8; ++nid) {
@@ -751,7 +791,13 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
           }
         }
       }
-      if (sum != T(0)) {
+      if (det.tile) {
+        // deterministic mode: the block's summed tile is stored as is; the
+        // nodes are summed over the neighbouring tiles in a fixed order by
+        // det_gather_kernel
+        if (item < det.cap) det.tile[uint64_t(item) * kDetVals + e] = sum;
+        else if (e == 0) atomicOr(&st->overflow, 2u);
+      } else if (sum != T(0)) {
         const int gi = 4 * bx - g + i, gj = 4 * by - g + j, gk = 4 * bz - g + k;
         const int64_t off = nbr_offset(nbr, g, gi, gj, gk, bx, by, bz);
         if (off < 0 || uint64_t(off) >= uint64_t(cap) * kBlockVals)
@@ -759,6 +805,115 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
         else
           atomicAdd(pool + off + v * 64, sum);
       }
+    }
+  }
+}
+
+// Deterministic mode (cfg.deterministic; the reference switches to its serial
+// scatter, simulation.hpp:326-327): every node of every active block is the
+// sum of the covering blocks' P2G tiles in a fixed order -- key block
+// offsets ascending in x, then y, then z -- instead of REDG arrival order.
+// A node at local index l of its block on the -1 grid (tile 5^3 from 4b) is
+// covered by the tiles of b = B (slot l) and, for l = 0, b = B - 1 (slot 4);
+// on the +1 grid (tile 6^3 from 4b - 1) by b = B - 1 (l = 0, slot 5), b = B
+// (slot l + 1) and b = B + 1 (l = 3, slot 0).  Bitwise run-to-run
+// reproducible on the same GPU (not bitwise equal to the CPU engine).
+template <typename T>
+__global__ void det_gather_kernel(T* __restrict__ pool, const uint32_t* __restrict__ active,
+                                  const int32_t* __restrict__ dir, const T* __restrict__ dtile, uint32_t dcap,
+                                  const DevStatus* st, uint32_t cap, int D) {
+  const uint32_t na = min(min(st->grid_hi, cap), dcap);
+  const uint32_t n0 = st->grid_lo;
+  const uint64_t total = na > n0 ? uint64_t(na - n0) * 128 : 0;
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t slot = n0 + uint32_t(k >> 7);
+    const int g = int(k >> 6) & 1, l = int(k & 63);
+    const int li = (l >> 4) & 3, lj = (l >> 2) & 3, lk = l & 3;
+    int Bx, By, Bz;
+    decode_key(__ldg(active + slot), D, Bx, By, Bz);
+    const int L[3] = {li, lj, lk};
+    // covering key blocks per axis (ascending) and the node's slot in their tile
+    int ob[3][3], os[3][3], no[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      int m = 0;
+      if (g == 0) {
+        if (L[a] == 0) { ob[a][m] = -1; os[a][m] = 4; ++m; }
+        ob[a][m] = 0; os[a][m] = L[a]; ++m;
+      } else {
+        if (L[a] == 0) { ob[a][m] = -1; os[a][m] = 5; ++m; }
+        ob[a][m] = 0; os[a][m] = L[a] + 1; ++m;
+        if (L[a] == 3) { ob[a][m] = 1; os[a][m] = 0; ++m; }
+      }
+      no[a] = m;
+    }
+    T sum[4] = {T(0), T(0), T(0), T(0)};
+    for (int ix = 0; ix < no[0]; ++ix)
+      for (int iy = 0; iy < no[1]; ++iy)
+        for (int iz = 0; iz < no[2]; ++iz) {
+          const int32_t nb = dir_lookup(dir, D, Bx + ob[0][ix], By + ob[1][iy], Bz + ob[2][iz]);
+          if (nb < 0 || uint32_t(nb) >= dcap) continue;
+          const T* t = dtile + uint64_t(nb) * kDetVals;
+          int e;
+          if (g == 0) e = (os[0][ix] * kPT + os[1][iy]) * kPT + os[2][iz];
+          else e = 4 * kPTNodes + (os[0][ix] * kTileN + os[1][iy]) * kTileN + os[2][iz];
+          const int vs = g == 0 ? kPTNodes : kTileNodes;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) sum[v] += __ldg(t + e + v * vs);
+        }
+    T* base = pool + uint64_t(slot) * kBlockVals + g * 256 + l;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) base[v * 64] = sum[v];
+  }
+}
+
+// Deterministic mode: the rare out-of-tile contributions (multiply/divide
+// rounding disagreement at a non-power-of-two dx), applied after the gather
+// in sorted-particle order by one CTA (bitonic sort of the records, then a
+// serial pass).
+constexpr int kDetSpillMax = 4096;
+template <typename T>
+__global__ void __launch_bounds__(1024) det_spill_kernel(T* __restrict__ pool, const int32_t* __restrict__ dir,
+                                                         const DetSpill<T>* __restrict__ spill, DevStatus* st,
+                                                         uint32_t cap, int D) {
+  __shared__ unsigned long long key[kDetSpillMax];
+  const uint32_t n = min(st->spill_n, uint32_t(kDetSpillMax));
+  if (n == 0) return;
+  uint32_t m = 1;
+  while (m < n) m <<= 1;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
+    key[i] = i < n ? (static_cast<unsigned long long>(spill[i].idx) << 32) | (uint64_t(spill[i].g) << 31) | i
+                   : ~0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= m; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const uint32_t p = i ^ j;
+        if (p > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long a = key[i], b = key[p];
+          if ((a > b) == up) {
+            key[i] = b;
+            key[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  if (threadIdx.x != 0) return;
+  for (uint32_t r = 0; r < n; ++r) {
+    const DetSpill<T>& e = spill[key[r] & 0x7fffffffu];
+    for (int nid = 0; nid < 8; ++nid) {
+      const int gi = e.base[0] + (nid >> 2), gj = e.base[1] + ((nid >> 1) & 1), gk = e.base[2] + (nid & 1);
+      const int32_t slot = dir_lookup(dir, D, gi >> 2, gj >> 2, gk >> 2);
+      if (slot < 0 || uint32_t(slot) >= cap) {
+        record_error(st, 0, kPhaseP2G, e.idx, 0, kErrInactive);
+        continue;
+      }
+      T* nd = pool + node_off(slot, e.g, gi, gj, gk);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nd[q * 64] += e.v[nid][q];
     }
   }
 }
@@ -1374,6 +1529,7 @@ __global__ void status_reset_kernel(DevStatus* st, int reset_err, int reset_perr
     if (reset_perr) st->perr = ~0ull;
     st->vmax2 = 0ull;
     st->nonfinite = 0u;
+    st->spill_n = 0u;
     st->n_active_prev = st->n_active;
     st->n_active = 0u;
     st->overflow = 0u;
