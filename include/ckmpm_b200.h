@@ -303,8 +303,14 @@ int32_t ckg_diagnostics_compute(ckg_ctx* ctx, ckg_diagnostics* out);
  *   ckg_slab_p2g      global activation from the reduced flags, clear, P2G;
  *                     block counts of planes {bx_lo-1, bx_lo, bx_hi-1, bx_hi}
  *   ckg_slab_halo     op 0 pack a plane, 1 add into it, 2 overwrite it
- *                     (block = 2 grids x 4 values x 64 nodes of T)
- *   ckg_slab_grid     grid update of own planes
+ *                     (block = 2 grids x 4 values x 64 nodes of T);
+ *                     deterministic mode: op 3 pack the plane's P2G tiles,
+ *                     4 overwrite them (ckg_slab_tile_words() T per block):
+ *                     the boundary planes' tiles replace the ghost-node
+ *                     reduce-add, so the owner sums every node in the
+ *                     single-domain order (bitwise equal to one domain)
+ *   ckg_slab_grid     (deterministic mode: fixed-order tile sums, then) grid
+ *                     update of own planes
  *   ckg_slab_g2p      G2P; counts of particles leaving left / right
  *   ckg_slab_pack     survivors compacted after nl_in incoming; migrant records
  *                     (ckg_slab_record_words() T words each) into left/right
@@ -320,6 +326,8 @@ int32_t ckg_slab_pack(ckg_ctx* ctx, uint64_t nl_in, void* left, void* right);
 int32_t ckg_slab_finish(ckg_ctx* ctx, const void* left, uint64_t nl, const void* right, uint64_t nr,
                         ckg_step_out* out);
 int32_t ckg_slab_record_words(void);
+/* Words (T) per block of a deterministic-mode P2G tile message (ckg_slab_halo ops 3/4). */
+int32_t ckg_slab_tile_words(void);
 
 /* Device-side timing on the context's stream (the stream every kernel of
  * this context is launched on): record marker `slot` (0..15); elapsed ms

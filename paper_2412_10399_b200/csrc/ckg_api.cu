@@ -207,7 +207,7 @@ struct Context final : CtxBase {
   uint32_t dcap = 0;
   DetSpill<T>* dspill = nullptr;
   DetBuf<T> detbuf() const {
-    if (!det || slab) return DetBuf<T>{nullptr, 0u, nullptr, 0u};
+    if (!det) return DetBuf<T>{nullptr, 0u, nullptr, 0u};
     return DetBuf<T>{dtile, dcap, dspill, uint32_t(kDetSpillMax)};
   }
   void set_det_cap(uint32_t c) {
@@ -747,11 +747,9 @@ struct Context final : CtxBase {
     const DetBuf<T> db = detbuf();
     p2g_tile_kernel<T, S><<<p2g_ctas, kP2GThreads, p2g_smem_bytes<T>(), st>>>(
         state(cur), perm, c, dir, rec, cord, ccnt, pool, pool_cap, dstat, step_idx, db);
-    if (db.tile) {
-      det_gather_kernel<T><<<148 * 8, 256, 0, st>>>(pool, active, dir, db.tile, db.cap, dstat, pool_cap, D);
-      det_spill_kernel<T><<<1, 1024, 0, st>>>(pool, dir, db.spill, dstat, pool_cap, D);
-      launches += 2;
-    }
+    // deterministic mode: the fixed-order tile sums (x-slab ranks first
+    // exchange their boundary planes' tiles: slab_grid runs the gather)
+    if (db.tile && !slab) enqueue_det_gather();
   }
   template <int S>
   void enqueue_g2p(const StepConst<T>& c, int step_idx) {
@@ -774,6 +772,13 @@ struct Context final : CtxBase {
     else
       g2p_tile_kernel<T, S><<<g2p_ctas, kG2PThreads, g2p_dyn_smem<T>(), st>>>(state(cur), state(cur ^ 1), perm, c, dir, rec, pool,
                                                                 pool_cap, dstat, step_idx);
+  }
+
+  void enqueue_det_gather() {
+    const DetBuf<T> db = detbuf();
+    det_gather_kernel<T><<<148 * 8, 256, 0, st>>>(pool, active, dir, db.tile, db.cap, dstat, pool_cap, D);
+    det_spill_kernel<T><<<1, 1024, 0, st>>>(pool, dir, db.spill, dstat, pool_cap, D, slab ? 1 : 0);
+    launches += 2;
   }
 
   // Kernels enqueue_step launches (status reset, key/footprint, 5 per radix
@@ -1561,6 +1566,7 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaSetDevice(device));
     dfree(plane_start);
     plane_start = dalloc<uint32_t>(uint64_t(D) + 1);
+    if (det) set_det_cap(std::min<uint32_t>(pool_cap, 1u << 18));  // slots are global: every rank's blocks
     return CKG_OK;
   }
 
@@ -1609,11 +1615,20 @@ struct Context final : CtxBase {
     return CKG_OK;
   }
 
-  // op 0: pack plane -> buf, 1: add buf into plane, 2: copy buf into plane
+  // op 0: pack plane -> buf, 1: add buf into plane, 2: copy buf into plane;
+  // deterministic mode: 3 pack the plane's P2G tiles, 4 copy buf into them
   int slab_halo(int op, int sel, void* buf) override {
     const int bx = plane_bx(sel);
     if (bx < 0 || bx >= D) return CKG_OK;
     CKG_CUDA(cudaSetDevice(device));
+    if (op >= 3) {
+      if (!det) return CKG_ERR_CONFIG;
+      tile_halo_kernel<T><<<148 * 4, 256, 0, st>>>(dtile, dcap, plane_start, bx, op, static_cast<T*>(buf),
+                                                   &dstat->overflow);
+      launches += 1;
+      CKG_CUDA(cudaStreamSynchronize(st));
+      return CKG_OK;
+    }
     halo_kernel<T><<<148 * 4, 256, 0, st>>>(pool, plane_start, bx, op, static_cast<T*>(buf));
     launches += 1;
     CKG_CUDA(cudaStreamSynchronize(st));
@@ -1623,6 +1638,7 @@ struct Context final : CtxBase {
   int slab_grid() override {
     CKG_CUDA(cudaSetDevice(device));
     const StepConst<T> c = make_const(slab_dt);
+    if (det) enqueue_det_gather();  // own planes, from local and received tiles
     grid_update_kernel<T><<<148 * 8, 256, 0, st>>>(pool, active, dstat, pool_cap, c, dbcs);
     CKG_CUDA(cudaEventRecord(ev[5], st));
     launches += 1;
@@ -1827,6 +1843,13 @@ struct Context final : CtxBase {
     out->slab_migration = region ? 1 : 2;
     grid_valid = true;
     last_active = hstat->n_active;
+    if (hstat->overflow) {
+      last_error = (hstat->overflow & 8u)
+                       ? "deterministic x-slab mode: out-of-tile particles (needs a power-of-two cell size)"
+                       : "grid block pool / deterministic tile buffer capacity exceeded";
+      out->status = CKG_ERR_DEVICE;
+      return CKG_ERR_DEVICE;
+    }
     int rc = decode_status(out, CKG_PHASE_G2P);
     if (rc == CKG_OK) step_count += 1;
     out->status = rc;
@@ -1979,6 +2002,7 @@ int32_t ckg_download(ckg_ctx* ctx, void* particles, uint64_t n) {
 
 uint64_t ckg_particle_count(const ckg_ctx* ctx) { return ctx ? ctx->impl->count() : 0; }
 int32_t ckg_fused(const ckg_ctx* ctx) { return ctx && ctx->impl->is_fused() ? 1 : 0; }
+int32_t ckg_slab_tile_words(void) { return ckg::kDetVals; }
 
 int32_t ckg_set_mass_epsilon(ckg_ctx* ctx, double eps) {
   if (!ctx) return CKG_ERR_CONFIG;
@@ -2058,7 +2082,7 @@ int32_t ckg_slab_p2g(ckg_ctx* ctx, const void* core_in, uint64_t plane_blocks[4]
   return guard(ctx, "ckg_slab_p2g", [&] { return ctx->impl->slab_p2g(core_in, plane_blocks); });
 }
 int32_t ckg_slab_halo(ckg_ctx* ctx, int32_t op, int32_t plane, void* buf) {
-  if (!ctx || op < 0 || op > 2 || plane < 0 || plane > 3) return CKG_ERR_CONFIG;
+  if (!ctx || op < 0 || op > 4 || plane < 0 || plane > 3) return CKG_ERR_CONFIG;
   return guard(ctx, "ckg_slab_halo", [&] { return ctx->impl->slab_halo(op, plane, buf); });
 }
 int32_t ckg_slab_grid(ckg_ctx* ctx) {

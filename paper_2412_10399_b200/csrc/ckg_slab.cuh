@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "ckg_kernels.cuh"
+#include "ckg_transfer.cuh"
 
 namespace ckg {
 
@@ -60,6 +61,26 @@ __global__ void halo_kernel(T* __restrict__ pool, const uint32_t* __restrict__ p
       buf[k] = p[k];
     else if (op == 1)
       p[k] += buf[k];
+    else
+      p[k] = buf[k];
+  }
+}
+
+// Deterministic mode: a plane's per-block P2G tiles (kDetVals words per slot)
+// op 3: dst[...] = tiles of the plane; op 4: tiles of the plane = src.
+template <typename T>
+__global__ void tile_halo_kernel(T* __restrict__ dtile, uint32_t dcap, const uint32_t* __restrict__ plane_start,
+                                 int bx, int op, T* __restrict__ buf, unsigned int* overflow) {
+  const uint64_t s0 = plane_start[bx], s1 = plane_start[bx + 1];
+  if (s1 > dcap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(overflow, 2u);
+    return;
+  }
+  const uint64_t total = (s1 - s0) * uint64_t(kDetVals);
+  T* p = dtile + s0 * uint64_t(kDetVals);
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total; k += uint64_t(gridDim.x) * blockDim.x) {
+    if (op == 3)
+      buf[k] = p[k];
     else
       p[k] = buf[k];
   }

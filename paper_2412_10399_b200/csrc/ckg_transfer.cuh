@@ -876,10 +876,14 @@ constexpr int kDetSpillMax = 4096;
 template <typename T>
 __global__ void __launch_bounds__(1024) det_spill_kernel(T* __restrict__ pool, const int32_t* __restrict__ dir,
                                                          const DetSpill<T>* __restrict__ spill, DevStatus* st,
-                                                         uint32_t cap, int D) {
+                                                         uint32_t cap, int D, int slab) {
   __shared__ unsigned long long key[kDetSpillMax];
   const uint32_t n = min(st->spill_n, uint32_t(kDetSpillMax));
   if (n == 0) return;
+  if (slab) {  // x-slab ranks exchange tiles only: no out-of-tile records
+    if (threadIdx.x == 0) atomicOr(&st->overflow, 8u);
+    return;
+  }
   uint32_t m = 1;
   while (m < n) m <<= 1;
   for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)

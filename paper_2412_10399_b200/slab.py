@@ -153,6 +153,7 @@ class SlabRank:
         self.core = torch.zeros(D * D * D, dtype=torch.int32, device=self.device)
         self.block_words = 512
         self.rec_words = int(self.lib.ckg_slab_record_words())
+        self.tile_words = int(self.lib.ckg_slab_tile_words())
         self.out = abi.StepOut()
         self.vmax = 0.0
         self.min_j = [1.0] * len(cfg.materials)
@@ -175,20 +176,39 @@ class SlabRank:
         _check(lib, ctx, lib.ckg_slab_p2g(ctx, C.c_void_p(self.core.data_ptr()), planes), "ckg_slab_p2g")
         pb = [int(v) for v in planes]  # blocks of planes ghostL, ownL, ownR, ghostR
         W = self.block_words
-        # halo reduce-add: ghost planes -> owners
-        send_l = self._buf(pb[0], W) if has_l else None
-        send_r = self._buf(pb[3], W) if has_r else None
-        if send_l is not None:
-            _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 0, C.c_void_p(send_l.data_ptr())), "halo pack")
-        if send_r is not None:
-            _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 3, C.c_void_p(send_r.data_ptr())), "halo pack")
-        recv_l = self._buf(pb[1], W) if has_l else None
-        recv_r = self._buf(pb[2], W) if has_r else None
-        yield Neighbor(send_l, send_r, recv_l, recv_r)
-        if recv_l is not None:
-            _check(lib, ctx, lib.ckg_slab_halo(ctx, 1, 1, C.c_void_p(recv_l.data_ptr())), "halo add")
-        if recv_r is not None:
-            _check(lib, ctx, lib.ckg_slab_halo(ctx, 1, 2, C.c_void_p(recv_r.data_ptr())), "halo add")
+        if self.cfg.deterministic:
+            # the boundary planes' P2G tiles -> the neighbours' ghost planes;
+            # each rank then sums its nodes over local and received tiles in
+            # the single-domain order (ckg_slab_grid)
+            TW = self.tile_words
+            send_l = self._buf(pb[1], TW) if has_l else None
+            send_r = self._buf(pb[2], TW) if has_r else None
+            if send_l is not None:
+                _check(lib, ctx, lib.ckg_slab_halo(ctx, 3, 1, C.c_void_p(send_l.data_ptr())), "tile pack")
+            if send_r is not None:
+                _check(lib, ctx, lib.ckg_slab_halo(ctx, 3, 2, C.c_void_p(send_r.data_ptr())), "tile pack")
+            recv_l = self._buf(pb[0], TW) if has_l else None
+            recv_r = self._buf(pb[3], TW) if has_r else None
+            yield Neighbor(send_l, send_r, recv_l, recv_r)
+            if recv_l is not None:
+                _check(lib, ctx, lib.ckg_slab_halo(ctx, 4, 0, C.c_void_p(recv_l.data_ptr())), "tile set")
+            if recv_r is not None:
+                _check(lib, ctx, lib.ckg_slab_halo(ctx, 4, 3, C.c_void_p(recv_r.data_ptr())), "tile set")
+        else:
+            # halo reduce-add: ghost planes -> owners
+            send_l = self._buf(pb[0], W) if has_l else None
+            send_r = self._buf(pb[3], W) if has_r else None
+            if send_l is not None:
+                _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 0, C.c_void_p(send_l.data_ptr())), "halo pack")
+            if send_r is not None:
+                _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 3, C.c_void_p(send_r.data_ptr())), "halo pack")
+            recv_l = self._buf(pb[1], W) if has_l else None
+            recv_r = self._buf(pb[2], W) if has_r else None
+            yield Neighbor(send_l, send_r, recv_l, recv_r)
+            if recv_l is not None:
+                _check(lib, ctx, lib.ckg_slab_halo(ctx, 1, 1, C.c_void_p(recv_l.data_ptr())), "halo add")
+            if recv_r is not None:
+                _check(lib, ctx, lib.ckg_slab_halo(ctx, 1, 2, C.c_void_p(recv_r.data_ptr())), "halo add")
         _check(lib, ctx, lib.ckg_slab_grid(ctx), "ckg_slab_grid")
         # halo broadcast of velocities: own boundary planes -> neighbours' ghosts
         send_l = self._buf(pb[1], W) if has_l else None
