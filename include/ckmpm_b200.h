@@ -303,7 +303,9 @@ int32_t ckg_diagnostics_compute(ckg_ctx* ctx, ckg_diagnostics* out);
  *   ckg_slab_p2g      global activation from the reduced flags, clear, P2G;
  *                     block counts of planes {bx_lo-1, bx_lo, bx_hi-1, bx_hi}
  *   ckg_slab_halo     op 0 pack a plane, 1 add into it, 2 overwrite it
- *                     (block = 2 grids x 4 values x 64 nodes of T);
+ *                     (block = 2 grids x 4 values x 64 nodes of T); op 5 / 6
+ *                     pack / overwrite the velocities only (2 x 3 x 64 of T
+ *                     per block: the broadcast after the grid update);
  *                     deterministic mode: op 3 pack the plane's P2G tiles,
  *                     4 overwrite them (ckg_slab_tile_words() T per block):
  *                     the boundary planes' tiles replace the ghost-node
@@ -326,6 +328,10 @@ int32_t ckg_slab_pack(ckg_ctx* ctx, uint64_t nl_in, void* left, void* right);
 int32_t ckg_slab_finish(ckg_ctx* ctx, const void* left, uint64_t nl, const void* right, uint64_t nr,
                         ckg_step_out* out);
 int32_t ckg_slab_record_words(void);
+/* The context's CUDA stream (cudaStream_t): a host driving the slab exchanges
+ * with NCCL enqueues them on it, so the library's kernels and the transfers
+ * are ordered on the device with no host synchronisation in between. */
+void* ckg_stream(ckg_ctx* ctx);
 /* Words (T) per block of a deterministic-mode P2G tile message (ckg_slab_halo ops 3/4). */
 int32_t ckg_slab_tile_words(void);
 

@@ -103,6 +103,7 @@ struct CtxBase {
   virtual int debug_bases(int32_t* bases, uint64_t n) = 0;
   virtual uint64_t active_blocks() = 0;
   virtual bool is_fused() const = 0;
+  virtual void* stream() const = 0;
   virtual int grid_download(int32_t* coords, double* nodes, uint64_t nb) = 0;
   virtual int grid_totals(double* mass, double* mom) = 0;
   virtual int diagnostics(ckg_diagnostics* out) = 0;
@@ -311,6 +312,7 @@ struct Context final : CtxBase {
   }
 
   bool is_fused() const override { return fused; }
+  void* stream() const override { return static_cast<void*>(st); }
 
   bool fused_supported() const {
     return !quad() && cfg.scheme != CKG_SCHEME_MLS && !slab && !det && pool_cap >= nd;
@@ -1621,7 +1623,7 @@ struct Context final : CtxBase {
     const int bx = plane_bx(sel);
     if (bx < 0 || bx >= D) return CKG_OK;
     CKG_CUDA(cudaSetDevice(device));
-    if (op >= 3) {
+    if (op == 3 || op == 4) {
       if (!det) return CKG_ERR_CONFIG;
       tile_halo_kernel<T><<<148 * 4, 256, 0, st>>>(dtile, dcap, plane_start, bx, op, static_cast<T*>(buf),
                                                    &dstat->overflow);
@@ -2003,6 +2005,7 @@ int32_t ckg_download(ckg_ctx* ctx, void* particles, uint64_t n) {
 uint64_t ckg_particle_count(const ckg_ctx* ctx) { return ctx ? ctx->impl->count() : 0; }
 int32_t ckg_fused(const ckg_ctx* ctx) { return ctx && ctx->impl->is_fused() ? 1 : 0; }
 int32_t ckg_slab_tile_words(void) { return ckg::kDetVals; }
+void* ckg_stream(ckg_ctx* ctx) { return ctx ? ctx->impl->stream() : nullptr; }
 
 int32_t ckg_set_mass_epsilon(ckg_ctx* ctx, double eps) {
   if (!ctx) return CKG_ERR_CONFIG;
@@ -2082,7 +2085,7 @@ int32_t ckg_slab_p2g(ckg_ctx* ctx, const void* core_in, uint64_t plane_blocks[4]
   return guard(ctx, "ckg_slab_p2g", [&] { return ctx->impl->slab_p2g(core_in, plane_blocks); });
 }
 int32_t ckg_slab_halo(ckg_ctx* ctx, int32_t op, int32_t plane, void* buf) {
-  if (!ctx || op < 0 || op > 4 || plane < 0 || plane > 3) return CKG_ERR_CONFIG;
+  if (!ctx || op < 0 || op > 6 || plane < 0 || plane > 3) return CKG_ERR_CONFIG;
   return guard(ctx, "ckg_slab_halo", [&] { return ctx->impl->slab_halo(op, plane, buf); });
 }
 int32_t ckg_slab_grid(ckg_ctx* ctx) {

@@ -49,20 +49,30 @@ __global__ void slab_ranges_kernel(const uint32_t* __restrict__ plane_start, int
   st->clear_hi = plane_start[g1];
 }
 
-// op 0: dst[...] = pool plane; op 1: pool plane += src; op 2: pool plane = src.
+// op 0: dst[...] = pool plane; op 1: pool plane += src; op 2: pool plane = src;
+// op 5 / 6: the same as 0 / 2 for the nodal velocities only (the broadcast
+// after the grid update: 3 of each block's 4 values per grid, 384 of 512
+// words).
 template <typename T>
 __global__ void halo_kernel(T* __restrict__ pool, const uint32_t* __restrict__ plane_start, int bx, int op,
                             T* __restrict__ buf) {
   const uint64_t s0 = plane_start[bx], s1 = plane_start[bx + 1];
-  const uint64_t total = (s1 - s0) * kBlockVals;
+  const bool vel = op >= 5;
+  const uint64_t per = vel ? 384 : kBlockVals;
+  const uint64_t total = (s1 - s0) * per;
   T* p = pool + s0 * kBlockVals;
   for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < total; k += uint64_t(gridDim.x) * blockDim.x) {
-    if (op == 0)
-      buf[k] = p[k];
+    uint64_t w = k;
+    if (vel) {  // block b, word r of its 384: grid r / 192, value 1 + (r % 192) / 64, node r % 64
+      const uint64_t b = k / 384, r = k % 384;
+      w = b * kBlockVals + (r / 192) * 256 + 64 + (r % 192);
+    }
+    if (op == 0 || op == 5)
+      buf[k] = p[w];
     else if (op == 1)
-      p[k] += buf[k];
+      p[w] += buf[k];
     else
-      p[k] = buf[k];
+      p[w] = buf[k];
   }
 }
 

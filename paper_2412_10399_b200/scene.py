@@ -389,8 +389,13 @@ def _aabb(shape: Shape, T):
     return [c[a] - ext[a] for a in range(3)], [c[a] + ext[a] for a in range(3)]
 
 
-def sample_shape(shape: Shape, dx, ppc: int, seed: int = 0, precision: int = 8) -> np.ndarray:
-    """sample_shape (scene.hpp:78-131): (n, 3) positions in emission order."""
+def sample_shape(shape: Shape, dx, ppc: int, seed: int = 0, precision: int = 8,
+                 i_range: Optional[tuple] = None) -> np.ndarray:
+    """sample_shape (scene.hpp:78-131): (n, 3) positions in emission order.
+
+    i_range = (lo, hi): only the lattice cells with lo <= i <= hi (the outer,
+    x loop), i.e. exactly that part of the emission order (ppc 8 / 27; the
+    jittered ppc 16 draws its random stream over every cell and ignores it)."""
     T = _T(precision)
     dx = T(dx)
     if not (dx > 0):
@@ -401,7 +406,8 @@ def sample_shape(shape: Shape, dx, ppc: int, seed: int = 0, precision: int = 8) 
     if ppc in (8, 27):
         nsub = 2 if ppc == 8 else 3
         offs = np.array([T(2 * s + 1) / T(2 * nsub) for s in range(nsub)], dtype=T)
-        ii = np.arange(i0, i1 + 1)
+        ii = np.arange(i0 if i_range is None else max(i0, i_range[0]),
+                       (i1 if i_range is None else min(i1, i_range[1])) + 1)
         jj = np.arange(j0, j1 + 1)
         kk = np.arange(k0, k1 + 1)
         # loop order i, j, k, a, b, c (scene.hpp:90-101)
@@ -431,14 +437,19 @@ def sample_shape(shape: Shape, dx, ppc: int, seed: int = 0, precision: int = 8) 
     return np.stack([X[m], Y[m], Z[m]], axis=1)
 
 
-def seed_particles(cfg: SceneConfig, precision: int = 8) -> np.ndarray:
-    """seed_particles (scene.hpp:204-230) -> Particle<T> structured array."""
+def seed_particles(cfg: SceneConfig, precision: int = 8, i_range: Optional[tuple] = None,
+                   allow_empty: bool = False) -> np.ndarray:
+    """seed_particles (scene.hpp:204-230) -> Particle<T> structured array.
+
+    i_range: only the lattice x-cells lo..hi of every body (sample_shape),
+    i.e. that part of the global emission order (x-slab ranks seed their own
+    slab without ever holding the whole set)."""
     T = _T(precision)
     dx = cfg.dx(precision)
     parts = []
     for body in cfg.bodies:
         mat = cfg.materials[body.material]
-        xs = sample_shape(body.shape, dx, body.ppc, body.seed, precision)
+        xs = sample_shape(body.shape, dx, body.ppc, body.seed, precision, i_range)
         cell_vol = dx * dx * dx
         vol = cell_vol / T(body.ppc)
         mass = T(mat.density) * vol
@@ -463,7 +474,7 @@ def seed_particles(cfg: SceneConfig, precision: int = 8) -> np.ndarray:
         p["material"] = body.material
         parts.append(p)
     out = np.concatenate(parts) if parts else np.zeros(0, dtype=abi.particle_dtype(precision))
-    if len(out) == 0:
+    if len(out) == 0 and not allow_empty:
         raise ConfigError("bodies: seeding produced no particles")
     return out
 

@@ -152,6 +152,7 @@ class SlabRank:
         D = cfg.resolution // 4 + 2
         self.core = torch.zeros(D * D * D, dtype=torch.int32, device=self.device)
         self.block_words = 512
+        self.vel_words = 384  # 2 grids x 3 velocity components x 64 nodes
         self.rec_words = int(self.lib.ckg_slab_record_words())
         self.tile_words = int(self.lib.ckg_slab_tile_words())
         self.out = abi.StepOut()
@@ -210,20 +211,22 @@ class SlabRank:
             if recv_r is not None:
                 _check(lib, ctx, lib.ckg_slab_halo(ctx, 1, 2, C.c_void_p(recv_r.data_ptr())), "halo add")
         _check(lib, ctx, lib.ckg_slab_grid(ctx), "ckg_slab_grid")
-        # halo broadcast of velocities: own boundary planes -> neighbours' ghosts
-        send_l = self._buf(pb[1], W) if has_l else None
-        send_r = self._buf(pb[2], W) if has_r else None
+        # halo broadcast of velocities (only: G2P reads no ghost masses): own
+        # boundary planes -> neighbours' ghosts
+        VW = self.vel_words
+        send_l = self._buf(pb[1], VW) if has_l else None
+        send_r = self._buf(pb[2], VW) if has_r else None
         if send_l is not None:
-            _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 1, C.c_void_p(send_l.data_ptr())), "vel pack")
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 5, 1, C.c_void_p(send_l.data_ptr())), "vel pack")
         if send_r is not None:
-            _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 2, C.c_void_p(send_r.data_ptr())), "vel pack")
-        recv_l = self._buf(pb[0], W) if has_l else None
-        recv_r = self._buf(pb[3], W) if has_r else None
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 5, 2, C.c_void_p(send_r.data_ptr())), "vel pack")
+        recv_l = self._buf(pb[0], VW) if has_l else None
+        recv_r = self._buf(pb[3], VW) if has_r else None
         yield Neighbor(send_l, send_r, recv_l, recv_r)
         if recv_l is not None:
-            _check(lib, ctx, lib.ckg_slab_halo(ctx, 2, 0, C.c_void_p(recv_l.data_ptr())), "vel set")
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 6, 0, C.c_void_p(recv_l.data_ptr())), "vel set")
         if recv_r is not None:
-            _check(lib, ctx, lib.ckg_slab_halo(ctx, 2, 3, C.c_void_p(recv_r.data_ptr())), "vel set")
+            _check(lib, ctx, lib.ckg_slab_halo(ctx, 6, 3, C.c_void_p(recv_r.data_ptr())), "vel set")
         # G2P and migration
         counts = (C.c_uint64 * 2)()
         _check(lib, ctx, lib.ckg_slab_g2p(ctx, counts), "ckg_slab_g2p")
@@ -382,12 +385,23 @@ class DistTransport:
 
     def step(self, rank_obj: SlabRank, dt: float):
         import torch
-        for req in rank_obj.stages(dt):
-            self.handle(req)
-            # the library runs on its own (non-blocking) stream: make the
-            # received data visible before handing control back to it
-            if torch.cuda.is_available():
-                torch.cuda.synchronize()
+        if self.host_staged or not torch.cuda.is_available():
+            for req in rank_obj.stages(dt):
+                self.handle(req)
+                # the library runs on its own (non-blocking) stream: make the
+                # received data visible before handing control back to it
+                if torch.cuda.is_available():
+                    torch.cuda.synchronize()
+            return
+        # NCCL: every exchange is enqueued on the library's own stream (the
+        # process group orders its communication stream after it and the
+        # stream after the transfer), so packing kernel -> send/recv -> the
+        # kernels consuming the halo are ordered on the device; the host only
+        # waits where the library itself needs a count
+        ext = torch.cuda.ExternalStream(rank_obj.lib.ckg_stream(rank_obj.ctx), device=self.device)
+        with torch.cuda.stream(ext):
+            for req in rank_obj.stages(dt):
+                self.handle(req)
 
 
 def build_ranks(cfg: SceneConfig, world: int, precision: int = 8, particles: Optional[np.ndarray] = None,
@@ -417,45 +431,92 @@ def build_ranks(cfg: SceneConfig, world: int, precision: int = 8, particles: Opt
     return bounds, ranks
 
 
-def build_rank_for_box(cfg: SceneConfig, world: int, rank: int, precision: int = 8, device: int = 0):
-    """Rank-local seeding for single-box scenes (the bench's C5 family): the
-    slab bounds come from the x-marginal of the lattice, and each rank seeds
-    only the part of the box whose sort-key plane it owns.  Seeding order is
-    the lattice order restricted to the slab, i.e. exactly the slab's part of
-    the global stable sort (no rank ever holds the whole body)."""
-    import copy
+def _lattice_i_extent(cfg: SceneConfig, precision: int):
+    """Outer (x) cell range of every body's lattice sampler (scene.hpp:85-88)."""
+    import math
 
-    assert len(cfg.bodies) == 1 and cfg.bodies[0].shape.kind == "box" and cfg.bodies[0].ppc in (8, 27)
+    from .scene import _aabb
     T = np.float64 if precision == 8 else np.float32
     dx = cfg.dx(precision)
-    inv_dx = T(1) / dx
+    lo, hi = None, None
+    for b in cfg.bodies:
+        blo, bhi = _aabb(b.shape, T)
+        i0 = int(math.floor(T(blo[0]) / dx)) - 1
+        i1 = int(math.ceil(T(bhi[0]) / dx)) + 1
+        lo = i0 if lo is None else min(lo, i0)
+        hi = i1 if hi is None else max(hi, i1)
+    return lo, hi
+
+
+def scene_marginals(cfg: SceneConfig, precision: int = 8, chunk_cells: int = 16):
+    """Particles per sort-key block plane, the (mass, count) multiset and the
+    largest initial speed of the whole scene, by seeding it in chunks of x
+    cells (every rank can compute them without holding the particle set)."""
+    T = np.float64 if precision == 8 else np.float32
     D = cfg.resolution // 4 + 2
-    body = cfg.bodies[0]
-    lo, hi = [T(v) for v in body.shape.lo], [T(v) for v in body.shape.hi]
-    nsub = 2 if body.ppc == 8 else 3
-    offs = np.array([T(2 * s + 1) / T(2 * nsub) for s in range(nsub)], dtype=T)
-    i0, i1 = int(np.floor(lo[0] / dx)) - 1, int(np.ceil(hi[0] / dx)) + 1
-    ii = np.arange(i0, i1 + 1)
-    xs = ((ii[:, None].astype(T) + offs[None, :]) * dx).ravel()
-    xs = xs[(xs >= lo[0]) & (xs < hi[0])]
-    bx = np.clip(np.floor(xs * inv_dx + T(0.25)).astype(np.int64) >> 2, 0, D - 1)
-    bounds = partition_planes(np.bincount(bx, minlength=D).astype(np.float64), world)
-    # the box restricted to key planes [X_r, X_{r+1}): x in [(4X - 1/4) dx, (4X' - 1/4) dx)
-    xa, xb = (T(4 * bounds[rank]) - T(0.25)) * dx, (T(4 * bounds[rank + 1]) - T(0.25)) * dx
-    sub = copy.deepcopy(cfg)
-    sh = sub.bodies[0].shape
-    sh.lo = (float(max(lo[0], xa)), sh.lo[1], sh.lo[2])
-    sh.hi = (float(min(hi[0], xb)), sh.hi[1], sh.hi[2])
-    if not (sh.lo[0] < sh.hi[0]):
-        part = np.zeros(0, dtype=abi.particle_dtype(precision))
-    else:
-        part = seed_particles(sub, precision)
-        kbx = np.clip(np.floor(part["x"][:, 0] * inv_dx + T(0.25)).astype(np.int64) >> 2, 0, D - 1)
-        part = part[(kbx >= bounds[rank]) & (kbx < bounds[rank + 1])]
-    mat = cfg.materials[body.material]
-    vol = (dx * dx * dx) / T(body.ppc)
-    me = float(T(1e-12) * (T(mat.density) * vol))  # every particle has the same mass
+    counts = np.zeros(D, dtype=np.int64)
+    masses = {}
+    vmax2 = T(0)
+    lattice = all(b.ppc in (8, 27) for b in cfg.bodies)
+    lo, hi = _lattice_i_extent(cfg, precision)
+    ranges = [(a, min(a + chunk_cells - 1, hi)) for a in range(lo, hi + 1, chunk_cells)] if lattice else [None]
+    for r in ranges:
+        p = seed_particles(cfg, precision, i_range=r, allow_empty=True)
+        if len(p) == 0:
+            continue
+        counts += np.bincount(block_x_of(p, cfg, precision), minlength=D)
+        m, c = np.unique(p["mass"], return_counts=True)
+        for mv, cv in zip(m.tolist(), c.tolist()):
+            masses[mv] = masses.get(mv, 0) + cv
+        v = p["v"].astype(T)
+        s2 = (v[:, 0] * v[:, 0] + v[:, 1] * v[:, 1]) + v[:, 2] * v[:, 2]
+        vmax2 = max(vmax2, T(np.max(s2)))
+    return counts, masses, float(np.sqrt(vmax2))
+
+
+def _median_mass_eps(masses: dict, precision: int) -> float:
+    """compute_mass_epsilon (simulation.hpp:227-232, nth_element at n/2) over a
+    (mass, count) multiset."""
+    T = np.float64 if precision == 8 else np.float32
+    n = sum(masses.values())
+    k = n // 2
+    run = 0
+    for m in sorted(masses):
+        run += masses[m]
+        if run > k:
+            return float(T(1e-12) * T(m))
+    raise ValueError("no particles")
+
+
+def build_rank_local(cfg: SceneConfig, world: int, rank: int, precision: int = 8, device: int = 0):
+    """Rank-local seeding for any scene of lattice bodies (ppc 8 / 27;
+    jittered ppc 16 bodies are seeded whole and filtered): slab bounds from
+    the x-marginal of the scene (scene_marginals), then each rank seeds only
+    the lattice x-cells whose particles can have their sort-key plane in its
+    slab and keeps those that do.  The seeding order restricted to a slab is
+    the global emission order restricted to it (bodies in order, each i-major),
+    so the first substep's stable sort gives exactly the slab's part of the
+    global stable order; mass_eps and the initial vmax are the global ones."""
+    bounds, part, me, vmax = rank_local_particles(cfg, world, rank, precision)
     rk = SlabRank(cfg, rank, world, bounds, part, me, precision, device)
-    v = np.array(body.velocity, dtype=T)
-    rk.vmax = float(np.sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]))
+    rk.vmax = vmax
+    # (seeded J = 1: min J of every material stays 1)
     return bounds, rk
+
+
+def rank_local_particles(cfg: SceneConfig, world: int, rank: int, precision: int = 8):
+    """(bounds, this rank's particles in seeding order, global mass_eps,
+    global initial vmax) -- see build_rank_local."""
+    counts, masses, vmax = scene_marginals(cfg, precision)
+    bounds = partition_planes(counts.astype(np.float64), world)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    # key plane X <=> x/dx + 1/4 in [4X, 4X + 4): cells 4 lo - 1 .. 4 hi
+    part = seed_particles(cfg, precision, i_range=(4 * lo - 1, 4 * hi), allow_empty=True)
+    if len(part):
+        kbx = block_x_of(part, cfg, precision)
+        part = part[(kbx >= lo) & (kbx < hi)]
+    return bounds, part, _median_mass_eps(masses, precision), vmax
+
+
+# the bench's single-box scenes (kept name)
+build_rank_for_box = build_rank_local

@@ -103,3 +103,43 @@ def test_transport_semantics_gloo(world):
         else:
             assert d["rr"] is None and d["counts"][1] == 0
         assert d["scalars"] == [float(world - 1), -1.0, 0.0]
+
+
+C4_SMALL = {"name": "c4_small", "resolution": 64, "scheme": "apic", "gravity": [0, -0.1, 0],
+            "materials": [{"model": "drucker_prager", "density": 1400.0, "E": 10000.0, "nu": 0.4,
+                           "friction_angle_deg": 30.0},
+                          {"model": "fixed_corotated", "density": 1000.0, "E": 10000000.0, "nu": 0.2}],
+            "bodies": [{"shape": {"kind": "box", "lo": [0.40625, 0.0625, 0.39453125],
+                                  "hi": [0.6171875, 0.2734375, 0.60546875]}, "material": 0, "ppc": 8},
+                       {"shape": {"kind": "sphere", "center": [0.30625, 0.16796875, 0.5], "radius": 0.0625},
+                        "material": 1, "ppc": 8, "velocity": [10.0, 0, 0]},
+                       {"shape": {"kind": "cylinder", "center": [0.7, 0.2, 0.5], "radius": 0.05,
+                                  "half_length": 0.08, "axis": 1}, "material": 1, "ppc": 27}],
+            "boundaries": [{"kind": "separate", "lo": [0, 0, 0], "hi": [1, 0.0625, 1], "normal": [0, 1, 0]}]}
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("precision", [8, 4])
+def test_rank_local_seeding_multibody(world, precision):
+    """Rank-local seeding of a multi-body scene (sandcastle-like: DP box, fast
+    FC ball, ppc-27 cylinder): each rank's part, stably sorted by block key,
+    is bit-identical to its slab of the globally seeded and sorted set, and
+    mass_eps / vmax are the global ones."""
+    from paper_2412_10399_b200.scene import SceneConfig, mass_epsilon, seed_particles
+    from paper_2412_10399_b200.slab import rank_local_particles, split_particles
+
+    cfg = SceneConfig.from_json(C4_SMALL, precision)
+    full = seed_particles(cfg, precision)
+    bounds_ref, parts_ref = split_particles(full, cfg, world, precision)
+    T = np.float64 if precision == 8 else np.float32
+    D = cfg.resolution // 4 + 2
+    inv_dx = T(1) / cfg.dx(precision)
+    for r in range(world):
+        bounds, part, me, vmax = rank_local_particles(cfg, world, r, precision)
+        assert bounds == bounds_ref
+        c = np.clip(np.floor(part["x"].astype(T) * inv_dx + T(0.25)).astype(np.int64) >> 2, 0, D - 1)
+        key = (c[:, 0] * D + c[:, 1]) * D + c[:, 2]
+        got = part[np.argsort(key, kind="stable")]
+        assert got.tobytes() == parts_ref[r].tobytes(), r
+        assert me == mass_epsilon(full, precision)
+        assert vmax == pytest.approx(10.0)
