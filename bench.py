@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cells", type=int, default=108, help="C5 block edge in cells (108 -> 10.08M p)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak (~10M particles per GPU) or strong (the fixed --strong-cells block)")
+    ap.add_argument("--strong-cells", type=int, default=232, help="strong-scaling block edge (232 -> 99.9M p)")
     ap.add_argument("--res", type=int, default=512)
     ap.add_argument("--scheme", default="apic")
     ap.add_argument("--kernel", default="compact", choices=["compact", "quadratic"],
@@ -188,7 +191,7 @@ def single_precision_rate(args, cfg, local):
 
 
 def cpu_cells(args):
-    return args.cells if args.cpu_cells is None else args.cpu_cells
+    return workload_cells(args, 1) if args.cpu_cells is None else args.cpu_cells
 
 
 def cpu_baseline(args, threads):
@@ -218,8 +221,11 @@ def cpu_baseline(args, threads):
 
 
 def workload_cells(args, ws):
-    """Block edge of the workload at N GPUs: the C5 block at N=1; weak
-    scaling grows it so every GPU keeps ~10M particles."""
+    """Block edge of the workload at N GPUs: weak scaling (default) keeps the
+    C5 block at N=1 and grows it so every GPU keeps ~10M particles; strong
+    scaling runs the fixed --strong-cells block at every N."""
+    if args.scaling == "strong":
+        return args.strong_cells
     return args.cells if ws == 1 else int(round(args.cells * ws ** (1.0 / 3.0)))
 
 
@@ -266,7 +272,7 @@ def run_reference(args):
               f"ckmpm::Simulation<T>::step, atomic P2G, {threads} threads, {steps} timed substeps")
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": steps,
             "warmup": args.warmup, "ms_per_step": el / steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.precision == 8 else "f32",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64" if args.precision == 8 else "f32",
             "data": "synthetic", "impl": "reference",
             "config": bench_config(args, cells, len(p), dt, nblocks),
             "parallelism": f"cpu threads={threads}",
@@ -278,22 +284,34 @@ def run_reference(args):
 
 def run_slab(args, ws, rank, local):
     """N>1: x-slab decomposition (paper_2412_10399_b200/slab.py), one rank
-    per GPU over NCCL.  Weak scaling: the C5 block grows with N so every GPU
-    keeps ~10M particles (cells = 108 * N^(1/3))."""
+    per GPU over NCCL, every exchange ordered on the library's stream.
+    Weak scaling (default): the C5 block grows with N so every GPU keeps ~10M
+    particles (cells = 108 * N^(1/3)); strong (--scaling strong): the fixed
+    --strong-cells block (232: 99.9M particles) split over the N GPUs.  Each
+    rank seeds only its own slab (build_rank_local)."""
     import torch
     import torch.distributed as dist
 
     from paper_2412_10399_b200._lib import lib
-    from paper_2412_10399_b200.slab import DistTransport, build_rank_for_box
+    from paper_2412_10399_b200.slab import DistTransport, build_rank_local
 
+    # CKMPM_BENCH_BACKEND=gloo: the same path with host-staged exchanges and
+    # every rank on the GPUs present (tests on a single GPU; not a bench value)
+    backend = os.environ.get("CKMPM_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
     L = lib()
-    cells = int(round(args.cells * ws ** (1.0 / 3.0)))
+    dev = f"cuda:{local}"
+    cells = workload_cells(args, ws)
     cfg = block_scene(cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
-    bounds, rk = build_rank_for_box(cfg, ws, rank, args.precision, local)
+    bounds, rk = build_rank_local(cfg, ws, rank, args.precision, local)
     tr = DistTransport(dist, rank, ws, torch.device("cuda", local))
-    n_local = torch.tensor([rk.n], dtype=torch.int64, device=f"cuda:{local}")
+    n_local = torch.tensor([rk.n], dtype=torch.int64, device=dev)
     dist.all_reduce(n_local)
     n_total = int(n_local.item())
     dt = rk.cfl_dt(1.0)
@@ -306,17 +324,31 @@ def run_slab(args, ws, rank, local):
     time.sleep(0.3)
     L.ckg_timer_mark(rk.ctx, 0)
     launches = 0
+    phase = np.zeros(6)
     for _ in range(args.steps):
         tr.step(rk, dt)
         launches += int(rk.out.kernel_launches)
+        phase += np.array(list(rk.out.phase_ms)) / args.steps
     L.ckg_timer_mark(rk.ctx, 1)
     el = C.c_double()
     L.ckg_timer_elapsed(rk.ctx, 0, 1, C.byref(el))
     clocks = sampler.stop()
-    t = torch.tensor([el.value], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([el.value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_ms = float(t.item())
     value = n_total * args.steps / (t_ms * 1e-3)
+    # roofline of the slowest rank's transfer kernels: algorithmic bytes of
+    # its own particles / blocks over its own P2G and G2P device times
+    p2g_b, g2p_b = algorithmic_bytes(rk.n, int(rk.out.active_blocks), args.scheme, args.precision)
+    peak, peak_kind = measured_peak_hbm()
+    mine = torch.tensor([phase[3], phase[5], p2g_b, g2p_b], dtype=torch.float64, device=dev)
+    allr = [torch.zeros(4, dtype=torch.float64, device=dev) for _ in range(ws)]
+    dist.all_gather(allr, mine)
+    rows = [r.cpu().numpy() for r in allr]
+    worst = max(rows, key=lambda r: r[0] + r[1])
+    dom_p2g = worst[0] >= worst[1]
+    dom_b, dom_ms = (worst[2], worst[0]) if dom_p2g else (worst[3], worst[1])
+    achieved = dom_b / (dom_ms * 1e-3) / 1e9
     # e2e: each step the rank's state goes host -> device -> host through the ABI
     e2e_steps = max(1, args.e2e_steps)
     dist.barrier()
@@ -330,23 +362,29 @@ def run_slab(args, ws, rank, local):
         tr.step(rk, dt)
     L.ckg_timer_mark(rk.ctx, 3)
     L.ckg_timer_elapsed(rk.ctx, 2, 3, C.byref(el))
-    t = torch.tensor([el.value], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([el.value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64" if args.precision == 8 else "f32", "data": "synthetic",
-            "config": {"workload": f"C5_block_{cells} (weak scaling: ~{args.cells}^3 cells per GPU)",
-                       "particles_total": n_total, "resolution": args.res, "scheme": args.scheme,
-                       "material": "fixed_corotated", "ppc": 8, "dt": dt,
-                       "parallelism": f"x-slab decomposition over {ws} GPUs (NCCL halo reduce/broadcast, migration)",
-                       "slab_bounds": list(map(int, bounds))},
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64" if args.precision == 8 else "f32",
+            "data": "synthetic",
+            "config": bench_config(args, cells, n_total, dt),
+            "parallelism": f"x-slab decomposition over {ws} GPUs (NCCL halo reduce / velocity broadcast, "
+                           f"ordered migration), {args.scaling} scaling",
+            "slab_bounds": list(map(int, bounds)),
+            "phase_ms_rank0": dict(zip(abi.PHASE_NAMES, phase.tolist())),
             "e2e": {"value": n_total * e2e_steps / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": hb // e2e_steps, "d2h_bytes_per_step": hd // e2e_steps,
                     "steps": e2e_steps, "path": "per rank: ckg_download + ckg_upload + slab substep"},
-            "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None,
+            "gpu_launches": launches, "clocks": clocks,
+            "roofline": {"bound": "hbm", "kernel": "p2g_kernel" if dom_p2g else "g2p_kernel",
+                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "algorithmic_bytes": dom_b,
+                         "avg_ms": dom_ms, "rank": "slowest rank (max P2G + G2P time)"},
+            "cpu_baseline": None,  # measured at N=1 only (the reference arm runs this config)
         }
         print(json.dumps(line), flush=True)
     rk.close()
@@ -370,7 +408,8 @@ def main():
 
     L = lib()
     prec = args.precision
-    cfg = block_scene(args.cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
+    cells = workload_cells(args, 1)
+    cfg = block_scene(cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
     host = seed_particles(cfg, prec)
     n = len(host)
     sim = Simulation(cfg, precision=prec, device=local, particles=host, fused=True if args.fused else None)
@@ -543,9 +582,9 @@ def main():
         ms_step = t_ms / args.steps
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64" if prec == 8 else "f32", "data": "synthetic",
-            "config": bench_config(args, args.cells, n, dt, nblocks),
+            "config": bench_config(args, cells, n, dt, nblocks),
             "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas (weak)",
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
