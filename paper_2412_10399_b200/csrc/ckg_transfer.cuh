@@ -78,9 +78,14 @@ constexpr int kXferWarps = kXferThreads / 32;
 #define CKG_G2P_MINB_F32 4
 #endif
 constexpr int kG2PThreads = CKG_G2P_THREADS;
+#ifndef CKG_G2P_PREFETCH
+#define CKG_G2P_PREFETCH 1  // G2P: next item's velocity tile fetched with cp.async during this item
+#endif
+// G2P dynamic shared memory: [+1 grid sin/cos stash (6 x threads)][2 velocity tiles]
 template <typename T>
 constexpr size_t g2p_dyn_smem() {
-  return CKG_G2P_DUAL_SINCOS ? size_t(6) * kG2PThreads * sizeof(T) : 0;
+  return (CKG_G2P_DUAL_SINCOS ? size_t(6) * kG2PThreads * sizeof(T) : 0) +
+         (CKG_G2P_PREFETCH ? size_t(2) * kVelVals * sizeof(T) : 0);
 }
 constexpr int kG2PWarps = kG2PThreads / 32;
 constexpr int kP2GChunk = 512;  // particles binned per pass (segment of a full lattice block)
@@ -462,6 +467,10 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
     const uint32_t key = s_rec[kRecKey];
     const uint32_t s0 = s_rec[kRecS0], s1 = s_rec[kRecS1];
     if (s1 <= s0) {
+      // deterministic mode: an empty block (activation halo) contributes a
+      // zero tile (its slot may hold a stale one from an earlier substep)
+      if (det.tile && item < det.cap)
+        for (int e = tid; e < kDetVals; e += kP2GThreads) det.tile[uint64_t(item) * kDetVals + e] = T(0);
       if (warp == 0) stage((k + 2) % 3, __shfl_sync(0xffffffffu, pend, 0));
       continue;
     }
@@ -1114,7 +1123,9 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
     g2p_tile_kernel(PState<T> cur, PState<T> nxt, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
                     const T* __restrict__ pool, uint32_t cap, DevStatus* st, int step) {
+#if !CKG_G2P_PREFETCH
   __shared__ T vt[kVelVals];
+#endif
   // per-thread gather results {v, grad v row, B row} x 3 components: the
   // -1 grid's partials, then (after the +1 grid) the final values, so no
   // accumulator is held in registers across the two grids' gathers
@@ -1125,13 +1136,20 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
   // (dynamic) per-thread +1 grid sin/cos (unscaled) of the three axes, see
   // the gather (CKG_G2P_DUAL_SINCOS)
   extern __shared__ __align__(16) unsigned char g2p_dyn[];
+#if CKG_G2P_PREFETCH
+  // (dynamic, after the stash) two velocity tiles: the next item's is
+  // fetched with cp.async while this item's particles are processed
+  T* vtb = reinterpret_cast<T*>(g2p_dyn) + (CKG_G2P_DUAL_SINCOS ? 6 * kG2PThreads : 0);
+  __shared__ uint32_t s_recb[2][kRecNbr + 27];
+  __shared__ uint32_t s_itemb[2];
+#else
   __shared__ uint32_t s_rec[kRecNbr + 27];
   __shared__ uint32_t s_item;
+#endif
   __shared__ T wmax[kG2PWarps];
   // material table in shared memory: indexing the by-value kernel parameter
   // with the particle's material would copy the whole table to local memory
   __shared__ MatParam<T> s_mats[kMaxMaterials];
-  const int32_t* nbr = reinterpret_cast<const int32_t*>(s_rec + kRecNbr);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #pragma unroll
   for (int m = 0; m < kMaxMaterials; ++m)
@@ -1140,6 +1158,78 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
   const int D = c.D;
   const T dx = c.dx, dt = step_dt(c);
   T vmax2 = T(0);
+  // nodal velocity e of an item's tile (KQ = 0: both grids' 6^3; KQ = 1: the
+  // quadratic baseline's 7^3 slot-0 nodes from 4b - 1): pool offset or -1
+  auto tile_src = [&](const int32_t* nb, int bx, int by, int bz, int e) -> int64_t {
+    if (KQ) {
+      if (e >= 3 * kQGNodes) return -1;
+      const int cc = e / kQGNodes, node = e % kQGNodes;
+      const int gi = 4 * bx - 1 + node / (kQG * kQG), gj = 4 * by - 1 + (node / kQG) % kQG,
+                gk = 4 * bz - 1 + node % kQG;
+      const int64_t off = nbr_offset(nb, 0, gi, gj, gk, bx, by, bz);
+      return (off >= 0 && uint64_t(off) < uint64_t(cap) * kBlockVals) ? off + (1 + cc) * 64 : -1;
+    }
+    if (e >= kVelVals) return -1;
+    const int g = e / (3 * kTileNodes);
+    const int cc = (e / kTileNodes) % 3;
+    const int node = e % kTileNodes;
+    const int gi = 4 * bx - g + node / (kTileN * kTileN);
+    const int gj = 4 * by - g + (node / kTileN) % kTileN;
+    const int gk = 4 * bz - g + node % kTileN;
+    const int64_t off = nbr_offset(nb, g, gi, gj, gk, bx, by, bz);
+    return (off >= 0 && uint64_t(off) < uint64_t(cap) * kBlockVals) ? off + (1 + cc) * 64 : -1;
+  };
+#if CKG_G2P_PREFETCH
+  // claim an item (warp 0) and fetch its record into s_recb[b]
+  auto claim = [&](int b) {
+    if (warp == 0) {
+      uint32_t it = 0;
+      if (lane == 0) it = item0 + atomicAdd(&st->work[1], 1u);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (lane == 0) s_itemb[b] = it;
+      if (it < na) {
+        const uint32_t* r = rec + uint64_t(it) * kRecWords;
+        if (lane < kRecNbr + 27) s_recb[b][lane] = __ldg(r + lane);
+      }
+    }
+  };
+  // all threads: cp.async of item s_itemb[b]'s velocity tile into buffer b
+  auto stage_async = [&](int b) {
+    const uint32_t it = s_itemb[b];
+    if (it < na && s_recb[b][kRecS1] > s_recb[b][kRecS0]) {
+      int bx, by, bz;
+      decode_key(s_recb[b][kRecKey], D, bx, by, bz);
+      const int32_t* nb = reinterpret_cast<const int32_t*>(s_recb[b] + kRecNbr);
+      T* dst = vtb + b * kVelVals;
+      for (int e = tid; e < kVelVals; e += kG2PThreads) {
+        const int64_t off = tile_src(nb, bx, by, bz, e);
+        cp_async_t(dst + e, pool + (off >= 0 ? off : 0), off >= 0);
+      }
+    }
+    cp_async_commit();
+  };
+  claim(0);
+  __syncthreads();
+  stage_async(0);
+  for (int k = 0;; ++k) {
+    const int buf = k & 1;
+    __syncthreads();  // everyone is done with buffer buf ^ 1 (item k - 1)
+    claim(buf ^ 1);
+    cp_async_wait_all();  // item k's tile (issued one item ago)
+    __syncthreads();
+    const uint32_t item = s_itemb[buf];
+    if (item >= na) break;
+    stage_async(buf ^ 1);  // item k + 1's tile, behind this item's work
+    const uint32_t* s_rec = s_recb[buf];
+    const int32_t* nbr = reinterpret_cast<const int32_t*>(s_rec + kRecNbr);
+    const T* vt = vtb + buf * kVelVals;
+    const uint32_t key = s_rec[kRecKey];
+    const uint32_t s0 = s_rec[kRecS0], s1 = s_rec[kRecS1];
+    if (s1 <= s0) continue;
+    int bx, by, bz;
+    decode_key(key, D, bx, by, bz);
+#else
+  const int32_t* nbr = reinterpret_cast<const int32_t*>(s_rec + kRecNbr);
   for (;;) {
     __syncthreads();
     if (warp == 0) {
@@ -1168,24 +1258,8 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
 #pragma unroll
       for (int r = 0; r < kPer; ++r) {
         const int e = tid + r * kG2PThreads;
-        val[r] = T(0);
-        if (KQ && e < 3 * kQGNodes) {
-          // quadratic: slot-0 velocities of the 7^3 nodes from 4b - 1
-          const int cc = e / kQGNodes, node = e % kQGNodes;
-          const int gi = 4 * bx - 1 + node / (kQG * kQG), gj = 4 * by - 1 + (node / kQG) % kQG,
-                    gk = 4 * bz - 1 + node % kQG;
-          const int64_t off = nbr_offset(nbr, 0, gi, gj, gk, bx, by, bz);
-          if (off >= 0 && uint64_t(off) < uint64_t(cap) * kBlockVals) val[r] = __ldg(pool + off + (1 + cc) * 64);
-        } else if (!KQ && e < kVelVals) {
-          const int g = e / (3 * kTileNodes);
-          const int cc = (e / kTileNodes) % 3;
-          const int node = e % kTileNodes;
-          const int gi = 4 * bx - g + node / (kTileN * kTileN);
-          const int gj = 4 * by - g + (node / kTileN) % kTileN;
-          const int gk = 4 * bz - g + node % kTileN;
-          const int64_t off = nbr_offset(nbr, g, gi, gj, gk, bx, by, bz);
-          if (off >= 0 && uint64_t(off) < uint64_t(cap) * kBlockVals) val[r] = __ldg(pool + off + (1 + cc) * 64);
-        }
+        const int64_t off = tile_src(nbr, bx, by, bz, e);
+        val[r] = off >= 0 ? __ldg(pool + off) : T(0);
       }
 #pragma unroll
       for (int r = 0; r < kPer; ++r) {
@@ -1194,6 +1268,7 @@ __global__ void __launch_bounds__(kG2PThreads, sizeof(T) == 4 ? CKG_G2P_MINB_F32
       }
     }
     __syncthreads();
+#endif
     // software pipeline over this thread's particles of the block: the next
     // particle's index is loaded when one starts, its position during the
     // gather (the perm -> position chain is off the critical path)

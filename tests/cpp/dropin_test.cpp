@@ -10,6 +10,8 @@
 //   dropin_test spheres   acceptance criterion 3 at 128^3, PIC (tests/acceptance_main.cpp:214-238)
 //   dropin_test stress    acceptance criterion 10 (tests/acceptance_main.cpp:530-562)
 //   dropin_test io        CKCHKPT1 / CKSNAP1 files vs the reference's writers, restart
+//   dropin_test jelly [dir]    acceptance criteria 8 + 9a (compact vs quadratic, jelly cube)
+//   dropin_test contact [dir]  acceptance criterion 9b (contact gap, ball through a tube)
 //
 // Each prints one JSON line and exits 0 on PASS, 1 on FAIL.
 #include <algorithm>
@@ -386,6 +388,75 @@ int io() {
   return pass ? 0 : 1;
 }
 
+#ifdef DROPIN_HAVE_REF_IO
+// Acceptance criteria 8 + 9a (tests/acceptance_main.cpp:419-471, :499-528):
+// the jelly cube dropped twice on an identical substep schedule, compact
+// kernel then the quadratic B-spline baseline (replaying the compact run's
+// dts); transfer-phase speed-up (soft gate 1.2x) and the compact run's kinetic
+// energy oscillation amplitude over the last quarter of the frames >= 2x.
+int jelly(const std::string& dir) {
+  SimConfig<double> cfg = load_config<double>(dir + "/jelly_cube.json");
+  b200::Simulation<double> compact(cfg);
+  std::vector<double> dts, ke_c, ke_q;
+  std::vector<std::size_t> ends;
+  for (int f = 0; f < cfg.frames; ++f) {
+    compact.advance_frame([&](b200::Simulation<double>&, double dt) { dts.push_back(dt); });
+    ends.push_back(dts.size());
+    ke_c.push_back(compact.device_diagnostics().kinetic_energy);
+  }
+  SimConfig<double> qcfg = cfg;
+  qcfg.kernel = KernelKind::quadratic;
+  b200::Simulation<double> quad(qcfg);
+  std::size_t idx = 0;
+  for (int f = 0; f < cfg.frames; ++f) {
+    while (idx < ends[static_cast<std::size_t>(f)]) quad.step(dts[idx++]);
+    ke_q.push_back(quad.device_diagnostics().kinetic_energy);
+  }
+  auto amplitude = [](const std::vector<double>& ke) {
+    std::size_t lo = ke.size() - ke.size() / 4;
+    auto mm = std::minmax_element(ke.begin() + lo, ke.end());
+    return *mm.second - *mm.first;
+  };
+  const double amp_c = amplitude(ke_c), amp_q = amplitude(ke_q);
+  const double ct = compact.timers().transfer_total(), qt = quad.timers().transfer_total();
+  const double speedup = ct > 0 ? qt / ct : 0.0;
+  const bool ke_ok = amp_c >= 2.0 * amp_q;
+  std::printf("{\"test\":\"jelly\",\"pass\":%s,\"substeps\":%zu,\"speedup\":%.3f,\"speedup_soft_gate_1_2\":%s,"
+              "\"compact_transfer_s\":%.4f,\"quadratic_transfer_s\":%.4f,\"ke_amp_compact\":%.4e,"
+              "\"ke_amp_quadratic\":%.4e,\"ke_amp_ok\":%s}\n",
+              ke_ok ? "true" : "false", dts.size(), speedup, speedup >= 1.2 ? "true" : "false", ct, qt, amp_c,
+              amp_q, ke_ok ? "true" : "false");
+  return ke_ok ? 0 : 1;
+}
+
+// Acceptance criterion 9b (tests/acceptance_main.cpp:473-497): a ball falls
+// through a tube whose bore clears it by 1.5 cells; the compact kernel lets
+// it pass the tube midpoint, the quadratic baseline couples it to the wall.
+double contact_ball_y(const std::string& dir, KernelKind kernel) {
+  SimConfig<double> cfg = load_config<double>(dir + "/contact_cylinder.json");
+  cfg.kernel = kernel;
+  b200::Simulation<double> sim(cfg);
+  for (int f = 0; f < cfg.frames; ++f) sim.advance_frame();
+  Vec3d sum{};
+  std::size_t count = 0;
+  for (const P& p : sim.particles())
+    if (p.material == 1u) {
+      sum = sum + p.x;
+      ++count;
+    }
+  if (count == 0) throw NumericalError("contact scene lost every ball particle");
+  return sum.y / static_cast<double>(count);
+}
+
+int contact(const std::string& dir) {
+  const double yc = contact_ball_y(dir, KernelKind::compact), yq = contact_ball_y(dir, KernelKind::quadratic);
+  const bool ok = yc < 0.5 && yq > 0.5;
+  std::printf("{\"test\":\"contact\",\"pass\":%s,\"ball_y_compact\":%.5f,\"ball_y_quadratic\":%.5f}\n",
+              ok ? "true" : "false", yc, yq);
+  return ok ? 0 : 1;
+}
+#endif
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -397,6 +468,11 @@ int main(int argc, char** argv) {
     if (what == "spheres") return spheres();
     if (what == "stress") return stress();
     if (what == "io") return io();
+#ifdef DROPIN_HAVE_REF_IO
+    const std::string dir = argc > 2 ? argv[2] : "tests/golden/configs";
+    if (what == "jelly") return jelly(dir);
+    if (what == "contact") return contact(dir);
+#endif
   } catch (const std::exception& e) {
     std::printf("{\"test\":\"%s\",\"pass\":false,\"exception\":\"%s\"}\n", what.c_str(), e.what());
     return 1;

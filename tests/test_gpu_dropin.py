@@ -13,10 +13,13 @@ pytestmark = pytest.mark.gpu
 BIN = os.path.join(os.path.dirname(__file__), "cpp", "_bin", "dropin_test")
 
 
-def run(what, timeout=900):
+CONFIGS = os.path.join(os.path.dirname(__file__), "golden", "configs")
+
+
+def run(what, timeout=900, *extra):
     if not os.path.exists(BIN):
         pytest.skip("dropin_test not built (needs the reference headers at build time)")
-    r = subprocess.run([BIN, what], capture_output=True, text=True, timeout=timeout)
+    r = subprocess.run([BIN, what, *extra], capture_output=True, text=True, timeout=timeout)
     line = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert line, r.stdout + r.stderr
     d = json.loads(line[-1])
@@ -54,3 +57,17 @@ def test_dropin_checkpoint_snapshot_files():
     assert d["checkpoint_bytes_equal"] and d["snapshot_binary_equal"] and d["snapshot_text_equal"]
     assert d["restart_roundtrip"]
 
+
+
+def test_acceptance_8_9a_jelly_compact_vs_quadratic():
+    """Criteria 8 + 9a through the drop-in: the quadratic baseline replays
+    the compact run's substep schedule; the compact run keeps >= 2x the KE
+    oscillation amplitude (hard gate); the transfer speed-up is reported
+    against the reference's soft 1.2x gate."""
+    d = run("jelly", 1800, CONFIGS)
+    assert d["ke_amp_ok"] and d["substeps"] > 1000
+
+
+def test_acceptance_9b_contact_gap():
+    d = run("contact", 1800, CONFIGS)
+    assert d["ball_y_compact"] < 0.5 < d["ball_y_quadratic"]

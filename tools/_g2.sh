@@ -1,3 +1,8 @@
-CKMPM_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --cells 40 --res 128 --steps 3 --warmup 3 --e2e-steps 1 > gpurun_out/slab_bench.log 2>&1; echo rc=$?; tail -c 3000 gpurun_out/slab_bench.log
-CKMPM_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --gpus 2 --scaling strong --strong-cells 48 --res 128 --steps 3 --warmup 3 --e2e-steps 1 > gpurun_out/slab_bench2.log 2>&1; echo rc=$?; tail -c 1500 gpurun_out/slab_bench2.log
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29535 bench.py --impl reference --gpus 2 --cells 40 --res 128 --steps 3 --warmup 3 > gpurun_out/slab_ref.log 2>&1; echo rc=$?; tail -c 1500 gpurun_out/slab_ref.log
+for v in default build/var_nopf.so; do
+  if [ $v = default ]; then unset CKMPM_B200_LIB; else export CKMPM_B200_LIB=$PWD/$v; fi
+  timeout 300 python tools/time_phases.py
+  PREC=4 timeout 300 python tools/time_phases.py
+  MODEL=drucker_prager timeout 300 python tools/time_phases.py
+done
+unset CKMPM_B200_LIB
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_quad.py tests/test_gpu_frame.py tests/test_gpu_dense.py -q -x 2>&1 | tail -3
