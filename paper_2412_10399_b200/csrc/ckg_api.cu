@@ -472,6 +472,10 @@ struct Context final : CtxBase {
     int nsm = 0, per = 0;
     CKG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
     const size_t smem = p2g_smem_bytes<T>();
+    CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem)));
+    set_two_cta_carveout(p2g_tile_kernel<T, S, true>, smem,
+                         CKG_P2G_CPW * (sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB));
     CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     set_two_cta_carveout(p2g_tile_kernel<T, S>, smem,
                          CKG_P2G_CPW * (sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB));
@@ -747,8 +751,9 @@ struct Context final : CtxBase {
       return;
     }
     const DetBuf<T> db = detbuf();
-    p2g_tile_kernel<T, S><<<p2g_ctas, kP2GThreads, p2g_smem_bytes<T>(), st>>>(
-        state(cur), perm, c, dir, rec, cord, ccnt, pool, pool_cap, dstat, step_idx, db);
+    (db.tile ? p2g_tile_kernel<T, S, true> : p2g_tile_kernel<T, S, false>)
+        <<<p2g_ctas, kP2GThreads, p2g_smem_bytes<T>(), st>>>(state(cur), perm, c, dir, rec, cord, ccnt, pool,
+                                                              pool_cap, dstat, step_idx, db);
     // deterministic mode: the fixed-order tile sums (x-slab ranks first
     // exchange their boundary planes' tiles: slab_grid runs the gather)
     if (db.tile && !slab) enqueue_det_gather();

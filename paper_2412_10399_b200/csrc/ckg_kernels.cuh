@@ -187,22 +187,47 @@ __device__ __forceinline__ int axis_base(T x, T dx, T inv_dx, int pow2, T kq) {
 // Polynomial coefficients in the constant bank: DFMA reads c[bank][off]
 // operands directly, where literal FP64 constants cost two uniform-register
 // moves (UMOV) per use in every unrolled evaluation.
+#ifndef CKG_SINCOS_CBANK
+#define CKG_SINCOS_CBANK 1
+#endif
+#if CKG_SINCOS_CBANK
 __constant__ double kSinPoly[8] = {-0.7181223017785006, 3.819952584848282,  -15.09464257682299, 42.058693944897655,
                                    -76.70585975306139,  81.60524927607506,  -41.34170224039976, 6.283185307179586};
 __constant__ double kCosPoly[9] = {0.28200596845579123, -1.714390711088672, 7.903536371318469,
                                    -26.4262567833744,   60.24464137187666,  -85.45681720669373,
                                    64.9393940226683,    -19.739208802178716, 1.0};
+#endif
 __device__ __forceinline__ void sincos_2pi(double f, double* s, double* c) {
   const double r = f - rint(f);
   const double qd = rint(4.0 * r);
   const double t = fma(qd, -0.25, r);
   const double t2 = t * t;
+#if CKG_SINCOS_CBANK
   double ps = kSinPoly[0];
 #pragma unroll
   for (int k = 1; k < 8; ++k) ps = fma(ps, t2, kSinPoly[k]);
   double pc = kCosPoly[0];
 #pragma unroll
   for (int k = 1; k < 9; ++k) pc = fma(pc, t2, kCosPoly[k]);
+#else
+  double ps = -0.7181223017785006;
+  ps = fma(ps, t2, 3.819952584848282);
+  ps = fma(ps, t2, -15.09464257682299);
+  ps = fma(ps, t2, 42.058693944897655);
+  ps = fma(ps, t2, -76.70585975306139);
+  ps = fma(ps, t2, 81.60524927607506);
+  ps = fma(ps, t2, -41.34170224039976);
+  ps = fma(ps, t2, 6.283185307179586);
+  double pc = 0.28200596845579123;
+  pc = fma(pc, t2, -1.714390711088672);
+  pc = fma(pc, t2, 7.903536371318469);
+  pc = fma(pc, t2, -26.4262567833744);
+  pc = fma(pc, t2, 60.24464137187666);
+  pc = fma(pc, t2, -85.45681720669373);
+  pc = fma(pc, t2, 64.9393940226683);
+  pc = fma(pc, t2, -19.739208802178716);
+  pc = fma(pc, t2, 1.0);
+#endif
   const double sn = t * ps;
   const int q = int(qd) & 3;  // quadrant: angle = 2 pi t + q pi/2
   *s = (q == 0) ? sn : (q == 1) ? pc : (q == 2) ? -sn : -pc;

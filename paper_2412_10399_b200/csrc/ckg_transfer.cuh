@@ -353,6 +353,11 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
 #ifndef CKG_P2G_SEPARABLE
 #define CKG_P2G_SEPARABLE 1
 #endif
+// P2G: the two grids' scatters as a rolled loop (half the code: instruction
+// cache) instead of unrolled
+#ifndef CKG_P2G_ROLL_GRIDS
+#define CKG_P2G_ROLL_GRIDS 0
+#endif
 template <typename T, int SCHEME, bool SWZ>
 __device__ __forceinline__ void scatter_separable(const Axis<T> (&ax)[3], T m, const T (&u0)[3], const M3<T>& Q,
                                                   const M3<T>& Ap, T dx, T* tb, T* p0, int g, int lx, int ly,
@@ -413,7 +418,9 @@ __device__ __forceinline__ void scatter_separable(const Axis<T> (&ax)[3], T m, c
     }
 }
 
-template <typename T, int SCHEME>
+// DET: deterministic mode (per-block tiles stored for det_gather_kernel);
+// a separate instance so the default kernel carries none of its code.
+template <typename T, int SCHEME, bool DET = false>
 __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB))
     p2g_tile_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
@@ -469,7 +476,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
     if (s1 <= s0) {
       // deterministic mode: an empty block (activation halo) contributes a
       // zero tile (its slot may hold a stale one from an earlier substep)
-      if (det.tile && item < det.cap)
+      if (DET && item < det.cap)
         for (int e = tid; e < kDetVals; e += kP2GThreads) det.tile[uint64_t(item) * kDetVals + e] = T(0);
       if (warp == 0) stage((k + 2) % 3, __shfl_sync(0xffffffffu, pend, 0));
       continue;
@@ -587,7 +594,11 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
       // k = +1/4 is bit-identical to the dual evaluation) instead of being
       // carried through the -1 grid's scatter, which frees the registers
       // that let each node's four read-modify-writes overlap.
+#if CKG_P2G_ROLL_GRIDS
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
       for (int g = 0; g < 2; ++g) {
         Axis<T> ax[3];
         if (g == 0) {
@@ -694,7 +705,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
             }
           }
         }
-        if (valid && !in_tile && det.tile) {
+        if (DET && valid && !in_tile) {
           // deterministic mode: the contribution is recorded and applied in
           // sorted-particle order after the tile gather (det_spill_kernel)
           const uint32_t k = atomicAdd(&st->spill_n, 1u);
@@ -800,7 +811,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
           }
         }
       }
-      if (det.tile) {
+      if constexpr (DET) {
         // deterministic mode: the block's summed tile is stored as is; the
         // nodes are summed over the neighbouring tiles in a fixed order by
         // det_gather_kernel
