@@ -1,5 +1,7 @@
-for v in default build/var_nosep.so build/var_nocb.so build/var_nosepcb.so default; do
-  if [ $v = default ]; then unset CKMPM_B200_LIB; else export CKMPM_B200_LIB=$PWD/$v; fi
-  timeout 300 python tools/time_phases.py | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['lib'][-20:], d['prec'], 'p2g', round(d['phase_ms']['p2g'],4), 'g2p', round(d['phase_ms']['g2p'],4), 'tot', round(d['total_ms'],4))"
-  PREC=4 timeout 300 python tools/time_phases.py | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['lib'][-20:], d['prec'], 'p2g', round(d['phase_ms']['p2g'],4), 'g2p', round(d['phase_ms']['g2p'],4), 'tot', round(d['total_ms'],4))"
-done
+mkdir -p gpurun_out
+KERNEL=quadratic timeout 300 python tools/time_phases.py > gpurun_out/r02_quad.json; cat gpurun_out/r02_quad.json
+timeout 300 python tools/time_phases.py > gpurun_out/r02_compact.json; cat gpurun_out/r02_compact.json
+timeout 900 python profiles/scenes.py > gpurun_out/r02_scenes.jsonl 2>&1; tail -5 gpurun_out/r02_scenes.jsonl
+OUT=r02_launches bash tools/gpu_tasks.sh launches
+NCUOUT=r02_full_10M NCU="p2g_tile|g2p_tile" SKIP=6 COUNT=2 bash tools/gpu_tasks.sh prof
+NCUOUT=r02_full_10M_f32 NCU="p2g_tile|g2p_tile" SKIP=6 COUNT=2 BENCH_ARGS="--precision 4" bash tools/gpu_tasks.sh prof

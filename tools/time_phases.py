@@ -20,7 +20,7 @@ K = int(os.environ.get("STEPS", "10"))
 model = os.environ.get("MODEL", "fixed_corotated")
 scheme = os.environ.get("SCHEME", "apic")
 kw = {"E": 1e4, "density": 1400.0, "boundary": "separate", "gravity": (0, -2.0, 0)} if model == "drucker_prager" else {}
-cfg = block_scene(cells, model=model, scheme=scheme, **kw)
+cfg = block_scene(cells, model=model, scheme=scheme, kernel=os.environ.get("KERNEL", "compact"), **kw)
 host = seed_particles(cfg, prec)
 sim = Simulation(cfg, precision=prec, particles=host, fused=None if fused else False)
 L = lib()
@@ -35,5 +35,5 @@ for _ in range(K):
     for k in range(6):
         acc[k] += out.phase_ms[k] / K
 print(json.dumps({"lib": os.environ.get("CKMPM_B200_LIB", "default"), "fused": sim.fused(), "prec": prec,
-                  "model": model, "scheme": scheme, "n": len(host),
+                  "model": model, "scheme": scheme, "kernel": cfg.kernel, "n": len(host),
                   "phase_ms": dict(zip(abi.PHASE_NAMES, acc)), "total_ms": sum(acc), "rcs": sorted(rcs)}))
