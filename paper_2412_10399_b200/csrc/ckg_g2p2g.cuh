@@ -383,7 +383,6 @@ CKG_FB_INL void fused_scatter_round(const T* r, bool valid, uint32_t err_index, 
                 __syncwarp(tmask);
               }
         }
-#ifndef CKG_FX_NO2L
       } else if (maxrank == 1) {
         // two rank layers (a lattice chunk's same-cell class pair on
         // the +1 grid), unrolled
@@ -401,7 +400,6 @@ CKG_FB_INL void fused_scatter_round(const T* r, bool valid, uint32_t err_index, 
               if (in_tile && rank == 1) tile_add4(p, o, VS);
               __syncwarp();
             }
-#endif
       } else {
 #pragma unroll 1
         for (int nid = 0; nid < 8; ++nid) {
@@ -571,7 +569,7 @@ __global__ void __launch_bounds__(kFThreads, sizeof(T) == 4 ? CKG_FUSED_MINB_F32
       if (tid < 32) s_wcnt[tid >> 3][tid & 7] = 0u;
       __syncthreads();
       // =============================== phase B: scatter (substep n+1)
-#ifndef CKG_FX_NOB
+#ifndef CKG_FUSED_NO_SCATTER  // (defined: phase A alone, a timing experiment)
       {
         const uint32_t lo = s_cstart[2 * warp], hi = s_cstart[2 * warp + 2];
         for (uint32_t rb = lo; rb < hi; rb += 32) {
