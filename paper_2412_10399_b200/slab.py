@@ -5,8 +5,11 @@ the particles whose sort key lies there.  The device work of a substep runs in
 the library (libckmpm_b200.so, csrc/ckg_slab.cuh); between its stages this
 module moves the exchange buffers:
 
-  1. footprint flags of every rank, MAX-all-reduced -> identical global block
-     directory, so a block plane is the same contiguous pool slice everywhere;
+  1. footprint flags of the planes shared with the neighbours (planes
+     bx_lo-2..bx_lo from the left, bx_hi-1..bx_hi from the right), OR-merged:
+     the block set, and so the block order, of every plane two neighbours
+     share is identical on both, so a halo plane is one contiguous pool slice
+     on either side (the rest of each rank's directory is local);
   2. after P2G: ghost planes (bx_lo-1, bx_hi) sent to their owners and added
      (halo reduce-add of mass + momentum, both grids);
   3. after the grid update: boundary planes sent back into the neighbours'
@@ -150,6 +153,7 @@ class SlabRank:
         _check(self.lib, ctx, self.lib.ckg_upload(ctx, abi.ptr(p), len(p)), "ckg_upload")
         self.n = len(p)
         D = cfg.resolution // 4 + 2
+        self.D = D
         self.core = torch.zeros(D * D * D, dtype=torch.int32, device=self.device)
         self.block_words = 512
         self.vel_words = 384  # 2 grids x 3 velocity components x 64 nodes
@@ -172,7 +176,39 @@ class SlabRank:
         lib, ctx = self.lib, self.ctx
         has_l, has_r = self.rank > 0, self.rank < self.world - 1
         _check(lib, ctx, lib.ckg_slab_bin(ctx, float(dt), C.c_void_p(self.core.data_ptr())), "ckg_slab_bin")
-        yield AllReduceMax(self.core)
+        # footprint flags of the planes shared with the neighbours (no global
+        # all-reduce): the active set of a plane X (the one-block positive
+        # halo, grid.hpp:137-139) needs the footprint flags of X - 1 and X,
+        # which particles of key planes X - 2 .. X + 1 set.  This rank keeps
+        # planes lo - 1 .. hi (own + ghosts) and so needs the left
+        # neighbour's flags of lo - 2 .. lo and the right one's of
+        # hi - 1 .. hi; each side's plane set is then identical on both
+        # ranks, and so is its block order (halo messages match block for
+        # block) while the rest of the directory stays local.
+        D, PL = self.D, self.D * self.D
+
+        def span(a, b):
+            a, b = max(a, 0), min(b, D - 1)
+            return (a, b) if a <= b else None
+
+        def view(sp):
+            return self.core[sp[0] * PL:(sp[1] + 1) * PL]
+
+        sl_span = span(self.bx_lo - 1, self.bx_lo) if has_l else None  # -> left
+        sr_span = span(self.bx_hi - 2, self.bx_hi) if has_r else None  # -> right
+        rl_span = span(self.bx_lo - 2, self.bx_lo) if has_l else None  # <- left
+        rr_span = span(self.bx_hi - 1, self.bx_hi) if has_r else None  # <- right
+        send_l = view(sl_span).clone() if sl_span else None
+        send_r = view(sr_span).clone() if sr_span else None
+        recv_l = self.torch.empty_like(view(rl_span)) if rl_span else None
+        recv_r = self.torch.empty_like(view(rr_span)) if rr_span else None
+        yield Neighbor(send_l, send_r, recv_l, recv_r)
+        if recv_l is not None:
+            v = view(rl_span)
+            v.copy_(self.torch.maximum(v, recv_l))
+        if recv_r is not None:
+            v = view(rr_span)
+            v.copy_(self.torch.maximum(v, recv_r))
         planes = (C.c_uint64 * 4)()
         _check(lib, ctx, lib.ckg_slab_p2g(ctx, C.c_void_p(self.core.data_ptr()), planes), "ckg_slab_p2g")
         pb = [int(v) for v in planes]  # blocks of planes ghostL, ownL, ownR, ghostR

@@ -197,3 +197,26 @@ def test_clamp_singular_vs_reference():
                            fields=("x", "v", "F", "B"))
     sv = np.linalg.svd(a["F"].astype(np.float64), compute_uv=False)
     assert np.min(sv) >= 0.9 * (1 - 1e-12)
+
+
+def test_c5_bench_scene_float_vs_reference_float():
+    """The bench scene in the reference's single precision (Simulation<float>,
+    tools/ckmpm_main.cpp:122 `--precision single`; the bench's secondary
+    figure): keys and stable order bit-exact in float, state <= 1e-5 after 2
+    substeps."""
+    cfg = block_scene(108)
+    p = tag_volumes(seed_particles(cfg, 4))
+    ref = bind.Ref(cfg, p, precision=4, threads=THREADS, deterministic=False)
+    with Simulation(cfg, precision=4, particles=p) as sim:
+        k, o = sim.debug_sort()
+        k_ref, o_ref = bind.ref_sort(cfg, p, precision=4)
+        assert np.array_equal(k, k_ref) and np.array_equal(o, o_ref)
+        for _ in range(2):
+            dt = ref.cfl_dt(1.0)
+            assert ref.step(dt)[0] == 0
+            sim.step(dt)
+        a, b = sim.particles(), ref.particles()
+    ref.close()
+    assert np.array_equal(a["volume0"], b["volume0"])
+    for f in ("x", "v", "F"):
+        assert field_rel(a, b, f, floor=1.0 if f != "v" else 0.01) <= 1e-5, f
