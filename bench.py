@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak (~10M particles per GPU) or strong (the fixed --strong-cells block)")
     ap.add_argument("--strong-cells", type=int, default=232, help="strong-scaling block edge (232 -> 99.9M p)")
+    ap.add_argument("--model", default="fixed_corotated", choices=["fixed_corotated", "drucker_prager"],
+                    help="block material (drucker_prager: the sand scene of the north star's scaling target)")
+    ap.add_argument("--rebalance-every", type=int, default=0,
+                    help="N>1: move the slab bounds towards balance every K substeps (0: never)")
     ap.add_argument("--res", type=int, default=512)
     ap.add_argument("--scheme", default="apic")
     ap.add_argument("--kernel", default="compact", choices=["compact", "quadratic"],
@@ -199,7 +203,7 @@ def cpu_baseline(args, threads):
     Simulation<double>::step on the bench's own scene (same config; a bounded
     number of substeps), atomic (default) mode."""
     from oracle import bind
-    cfg = block_scene(cpu_cells(args), resolution=args.res, scheme=args.scheme, kernel=args.kernel)
+    cfg = bench_scene(args, cpu_cells(args))
     p = seed_particles(cfg, args.precision)
     ref = bind.Ref(cfg, p, precision=args.precision, threads=threads, deterministic=False)
     dt = ref.cfl_dt(1.0)
@@ -220,6 +224,17 @@ def cpu_baseline(args, threads):
                       f"ckmpm::Simulation<T>::step (atomic P2G), wall clock"}
 
 
+def bench_scene(args, cells):
+    """The C5 block of `cells`^3 cells; --model drucker_prager: the same block
+    of sand (E 1e4, rho 1400, phi 30 deg as SURVEY App. C's C3/C4, separating
+    floor, gravity -2)."""
+    if args.model == "drucker_prager":
+        return block_scene(cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel,
+                           model="drucker_prager", E=1e4, density=1400.0, gravity=(0, -2.0, 0),
+                           boundary="separate")
+    return block_scene(cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
+
+
 def workload_cells(args, ws):
     """Block edge of the workload at N GPUs: weak scaling (default) keeps the
     C5 block at N=1 and grows it so every GPU keeps ~10M particles; strong
@@ -231,8 +246,9 @@ def workload_cells(args, ws):
 
 def bench_config(args, cells, n, dt, nblocks=None):
     """The `config` object both arms print (same keys, same values)."""
-    return {"workload": f"C5_block_{cells}", "particles": n, "resolution": args.res, "kernel": args.kernel,
-            "scheme": args.scheme, "material": "fixed_corotated", "ppc": 8, "dt": dt,
+    name = f"C5_block_{cells}" if args.model == "fixed_corotated" else f"sand_block_{cells}"
+    return {"workload": name, "particles": n, "resolution": args.res, "kernel": args.kernel,
+            "scheme": args.scheme, "material": args.model, "ppc": 8, "dt": dt,
             "active_blocks": nblocks, "l2": "state >> 126 MB L2 (no flush needed)"}
 
 
@@ -248,7 +264,7 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     from oracle import bind
     cells = workload_cells(args, ws)
-    cfg = block_scene(cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
+    cfg = bench_scene(args, cells)
     p = seed_particles(cfg, args.precision)
     ref = bind.Ref(cfg, p, precision=args.precision, threads=threads, deterministic=False)
     dt = ref.cfl_dt(1.0)
@@ -308,8 +324,9 @@ def run_slab(args, ws, rank, local):
     L = lib()
     dev = f"cuda:{local}"
     cells = workload_cells(args, ws)
-    cfg = block_scene(cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
+    cfg = bench_scene(args, cells)
     bounds, rk = build_rank_local(cfg, ws, rank, args.precision, local)
+    rk.rebalance_every = args.rebalance_every
     tr = DistTransport(dist, rank, ws, torch.device("cuda", local))
     n_local = torch.tensor([rk.n], dtype=torch.int64, device=dev)
     dist.all_reduce(n_local)
@@ -374,7 +391,8 @@ def run_slab(args, ws, rank, local):
             "config": bench_config(args, cells, n_total, dt),
             "parallelism": f"x-slab decomposition over {ws} GPUs (NCCL halo reduce / velocity broadcast, "
                            f"ordered migration), {args.scaling} scaling",
-            "slab_bounds": list(map(int, bounds)),
+            "slab_bounds": list(map(int, bounds)), "slab_bounds_final": list(map(int, rk.bounds)),
+            "rebalance_every": args.rebalance_every,
             "phase_ms_rank0": dict(zip(abi.PHASE_NAMES, phase.tolist())),
             "e2e": {"value": n_total * e2e_steps / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": hb // e2e_steps, "d2h_bytes_per_step": hd // e2e_steps,
@@ -409,7 +427,7 @@ def main():
     L = lib()
     prec = args.precision
     cells = workload_cells(args, 1)
-    cfg = block_scene(cells, resolution=args.res, scheme=args.scheme, kernel=args.kernel)
+    cfg = bench_scene(args, cells)
     host = seed_particles(cfg, prec)
     n = len(host)
     sim = Simulation(cfg, precision=prec, device=local, particles=host, fused=True if args.fused else None)

@@ -319,6 +319,14 @@ int32_t ckg_diagnostics_compute(ckg_ctx* ctx, ckg_diagnostics* out);
  *   ckg_slab_finish   incoming records appended [left][survivors][right]
  * Must be called before ckg_upload. */
 int32_t ckg_slab_set(ckg_ctx* ctx, int32_t rank, int32_t world, int32_t bx_lo, int32_t bx_hi);
+/* Rebalancing: particles of the current state per sort-key plane bx
+ * (counts[D], D = resolution/4 + 2), and new slab bounds that take effect at
+ * the next substep's migration (ckg_slab_g2p classifies against them, the
+ * planes that change hands travel with the migrants, ckg_slab_finish commits
+ * them).  Every rank must apply one consistent partition, in which each
+ * rank's new slab only overlaps its neighbours' old ones. */
+int32_t ckg_slab_plane_counts(ckg_ctx* ctx, uint64_t* counts);
+int32_t ckg_slab_rebound(ckg_ctx* ctx, int32_t bx_lo, int32_t bx_hi);
 int32_t ckg_slab_bin(ckg_ctx* ctx, double dt, void* core_out);
 int32_t ckg_slab_p2g(ckg_ctx* ctx, const void* core_in, uint64_t plane_blocks[4]);
 int32_t ckg_slab_halo(ckg_ctx* ctx, int32_t op, int32_t plane, void* buf);

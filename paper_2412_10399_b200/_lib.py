@@ -92,6 +92,10 @@ def _declare(lib: C.CDLL) -> None:
     lib.ckg_slab_finish.restype = i32
     lib.ckg_slab_record_words.restype = i32
     lib.ckg_slab_tile_words.restype = i32
+    lib.ckg_slab_plane_counts.argtypes = [vp, P(u64)]
+    lib.ckg_slab_plane_counts.restype = i32
+    lib.ckg_slab_rebound.argtypes = [vp, i32, i32]
+    lib.ckg_slab_rebound.restype = i32
     lib.ckg_stream.argtypes = [vp]
     lib.ckg_stream.restype = vp
     lib.ckg_last_error_message.argtypes = [vp, C.c_char_p, u64]
@@ -106,7 +110,7 @@ EXPORTED = (
     "ckg_grid_active_block_count", "ckg_grid_download", "ckg_grid_totals",
     "ckg_diagnostics_compute", "ckg_timer_mark", "ckg_timer_elapsed", "ckg_last_error_message",
     "ckg_slab_set", "ckg_slab_bin", "ckg_slab_p2g", "ckg_slab_halo", "ckg_slab_grid", "ckg_slab_g2p",
-    "ckg_slab_pack", "ckg_slab_finish", "ckg_slab_record_words", "ckg_slab_tile_words", "ckg_stream",
+    "ckg_slab_pack", "ckg_slab_finish", "ckg_slab_record_words", "ckg_slab_tile_words", "ckg_stream", "ckg_slab_plane_counts", "ckg_slab_rebound",
 )
 
 

@@ -108,6 +108,8 @@ struct CtxBase {
   virtual int grid_totals(double* mass, double* mom) = 0;
   virtual int diagnostics(ckg_diagnostics* out) = 0;
   virtual int slab_set(int rank, int world, int lo, int hi) = 0;
+  virtual int slab_rebound(int lo, int hi) = 0;
+  virtual int slab_plane_counts(uint64_t* counts) = 0;
   virtual int slab_bin(double dt, void* core_out) = 0;
   virtual int slab_p2g(const void* core_in, uint64_t* plane_blocks) = 0;
   virtual int slab_halo(int op, int plane, void* buf) = 0;
@@ -141,6 +143,7 @@ struct Context final : CtxBase {
   // x-slab decomposition (ckg_slab.cuh)
   bool slab = false;
   int srank = 0, sworld = 1, bx_lo = 0, bx_hi = 0;
+  int pend_lo = -1, pend_hi = -1;  // rebalanced bounds, effective from this substep's migration
   uint32_t* plane_start = nullptr;
   uint32_t *fl_stay = nullptr, *fl_left = nullptr, *fl_right = nullptr;
   uint32_t *pos_stay = nullptr, *pos_left = nullptr, *pos_right = nullptr;
@@ -1577,6 +1580,29 @@ struct Context final : CtxBase {
     return CKG_OK;
   }
 
+  // Rebalancing: the new slab [lo, hi) takes effect at this substep's
+  // migration (its P2G, grid update and halos still use the old bounds);
+  // slab_finish commits it.  Particles of planes that change hands travel
+  // with the substep's migrants (full relayout path).
+  int slab_rebound(int lo, int hi) override {
+    if (!slab || lo < 0 || hi > D || lo >= hi) return CKG_ERR_CONFIG;
+    pend_lo = lo;
+    pend_hi = hi;
+    return CKG_OK;
+  }
+
+  // Particles of the current state per key plane bx (D counters).
+  int slab_plane_counts(uint64_t* counts) override {
+    CKG_CUDA(cudaSetDevice(device));
+    unsigned long long* d = dalloc<unsigned long long>(uint64_t(D));
+    CKG_CUDA(cudaMemsetAsync(d, 0, uint64_t(D) * sizeof(unsigned long long), st));
+    if (n) plane_count_kernel<T><<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(state(cur), T(cfg.inv_dx), D, d);
+    CKG_CUDA(cudaMemcpyAsync(counts, d, uint64_t(D) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d);
+    return CKG_OK;
+  }
+
   int plane_bx(int sel) const {
     return sel == 0 ? bx_lo - 1 : sel == 1 ? bx_lo : sel == 2 ? bx_hi - 1 : bx_hi;
   }
@@ -1661,8 +1687,10 @@ struct Context final : CtxBase {
     else enqueue_g2p<kSchemeMls>(c, 0);
     CKG_CUDA(cudaEventRecord(ev[6], st));
     PState<T> nx = state(cur ^ 1);
-    classify_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(nx, T(cfg.inv_dx), D, bx_lo, bx_hi, fl_stay,
-                                                                   fl_left, fl_right);
+    const bool rebound = pend_lo >= 0;
+    classify_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(nx, T(cfg.inv_dx), D, rebound ? pend_lo : bx_lo,
+                                                                   rebound ? pend_hi : bx_hi, fl_stay, fl_left,
+                                                                   fl_right);
     launches += 2;
     // crossers can only come from the first and last owned plane: find the
     // sorted regions of those planes and check the middle holds none
@@ -1675,7 +1703,7 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaStreamSynchronize(st));
     reg_pl = hreg[0];
     reg_pr = hreg[1];
-    mig_region = !force_full_relayout && bx_hi - bx_lo >= 2 && reg_pl <= reg_pr;
+    mig_region = !force_full_relayout && !rebound && bx_hi - bx_lo >= 2 && reg_pl <= reg_pr;
     if (mig_region) {
       // no crosser in the middle, none leaving the "wrong" side of a region
       if (reg_pr > reg_pl)
@@ -1850,6 +1878,11 @@ struct Context final : CtxBase {
     out->slab_migration = region ? 1 : 2;
     grid_valid = true;
     last_active = hstat->n_active;
+    if (pend_lo >= 0) {  // rebalanced slab committed
+      bx_lo = pend_lo;
+      bx_hi = pend_hi;
+      pend_lo = pend_hi = -1;
+    }
     if (hstat->overflow) {
       last_error = (hstat->overflow & 8u)
                        ? "deterministic x-slab mode: out-of-tile particles (needs a power-of-two cell size)"
@@ -2077,6 +2110,14 @@ int32_t ckg_diagnostics_compute(ckg_ctx* ctx, ckg_diagnostics* out) {
   return guard(ctx, "ckg_diagnostics_compute", [&] { return ctx->impl->diagnostics(out); });
 }
 
+int32_t ckg_slab_rebound(ckg_ctx* ctx, int32_t bx_lo, int32_t bx_hi) {
+  if (!ctx) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_rebound", [&] { return ctx->impl->slab_rebound(bx_lo, bx_hi); });
+}
+int32_t ckg_slab_plane_counts(ckg_ctx* ctx, uint64_t* counts) {
+  if (!ctx || !counts) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_plane_counts", [&] { return ctx->impl->slab_plane_counts(counts); });
+}
 int32_t ckg_slab_set(ckg_ctx* ctx, int32_t rank, int32_t world, int32_t bx_lo, int32_t bx_hi) {
   if (!ctx) return CKG_ERR_CONFIG;
   return guard(ctx, "ckg_slab_set", [&] { return ctx->impl->slab_set(rank, world, bx_lo, bx_hi); });

@@ -96,6 +96,13 @@ __global__ void tile_halo_kernel(T* __restrict__ dtile, uint32_t dcap, const uin
   }
 }
 
+// Particles per sort-key plane bx (rebalancing input).
+template <typename T>
+__global__ void plane_count_kernel(PState<T> p, T inv_dx, int D, unsigned long long* __restrict__ counts) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.n; i += uint64_t(gridDim.x) * blockDim.x)
+    atomicAdd(counts + key_axis(p.f[uint64_t(kX) * p.stride + i], inv_dx, D), 1ull);
+}
+
 // Migration class of each particle of the new state: 0 stays, 1 left, 2 right.
 template <typename T>
 __global__ void classify_kernel(PState<T> st_new, T inv_dx, int D, int bx_lo, int bx_hi,

@@ -69,6 +69,25 @@ def partition_planes(plane_counts: np.ndarray, world: int) -> List[int]:
     return bounds
 
 
+def rebalanced_bounds(bounds: Sequence[int], plane_counts: np.ndarray, max_shift: int = 1) -> List[int]:
+    """Slab bounds for the current particle distribution: the balanced
+    partition (partition_planes), each interior boundary moved at most
+    `max_shift` planes towards it (a rank's new slab then only overlaps its
+    neighbours' old ones, so planes change hands through the ordinary
+    neighbour migration) and every rank keeps at least one plane."""
+    world = len(bounds) - 1
+    target = partition_planes(plane_counts, world)
+    out = [int(bounds[0])]
+    for r in range(1, world):
+        b = int(bounds[r])
+        b = min(max(int(target[r]), b - max_shift), b + max_shift)
+        b = max(b, out[-1] + 1)
+        b = min(b, int(bounds[r + 1]) - 1 if r + 1 < world else int(bounds[world]) - 1)
+        out.append(b)
+    out.append(int(bounds[world]))
+    return out
+
+
 def split_particles(particles: np.ndarray, cfg: SceneConfig, world: int, precision: int = 8):
     """Global stable order by key (the reference's sort_particles), then the
     contiguous slab ranges of it.  Returns (bounds, [per-rank arrays])."""
@@ -92,6 +111,11 @@ def split_particles(particles: np.ndarray, cfg: SceneConfig, world: int, precisi
 @dataclass
 class AllReduceMax:
     buf: object           # torch.Tensor (int32, device)
+
+
+@dataclass
+class AllReduceSum:
+    buf: object           # torch.Tensor (int64, device): summed in place
 
 
 @dataclass
@@ -138,6 +162,9 @@ class SlabRank:
         self.cfg = cfg
         self.rank, self.world = rank, world
         self.bx_lo, self.bx_hi = int(bounds[rank]), int(bounds[rank + 1])
+        self.bounds = [int(b) for b in bounds]
+        self.substep = 0
+        self.rebalance_every = 0
         self.precision = precision
         self.T = np.float64 if precision == 8 else np.float32
         self.tdtype = torch.float64 if precision == 8 else torch.float32
@@ -172,9 +199,27 @@ class SlabRank:
         return self.torch.empty(max(1, blocks_or_recs) * words, dtype=self.tdtype, device=self.device)
 
     def stages(self, dt: float):
-        """One substep; yields exchange requests (see module docstring)."""
+        """One substep; yields exchange requests (see module docstring).
+        Every `rebalance_every` substeps (0: never) the slab bounds are first
+        moved towards the balanced partition of the current particles
+        (rebalanced_bounds); the planes that change hands travel with this
+        substep's migrants."""
         lib, ctx = self.lib, self.ctx
         has_l, has_r = self.rank > 0, self.rank < self.world - 1
+        self.substep += 1
+        new_bounds = None
+        if self.rebalance_every > 0 and self.substep % self.rebalance_every == 0 and self.world > 1:
+            D = self.D
+            counts = (C.c_uint64 * D)()
+            _check(lib, ctx, lib.ckg_slab_plane_counts(ctx, counts), "ckg_slab_plane_counts")
+            t = self.torch.tensor(np.frombuffer(counts, dtype=np.uint64).astype(np.int64), device=self.device)
+            yield AllReduceSum(t)
+            new_bounds = rebalanced_bounds(self.bounds, t.cpu().numpy().astype(np.float64))
+            if new_bounds != list(self.bounds):
+                _check(lib, ctx, lib.ckg_slab_rebound(ctx, new_bounds[self.rank], new_bounds[self.rank + 1]),
+                       "ckg_slab_rebound")
+            else:
+                new_bounds = None
         _check(lib, ctx, lib.ckg_slab_bin(ctx, float(dt), C.c_void_p(self.core.data_ptr())), "ckg_slab_bin")
         # footprint flags of the planes shared with the neighbours (no global
         # all-reduce): the active set of a plane X (the one-block positive
@@ -281,6 +326,9 @@ class SlabRank:
                        recv_l[: nl_in * R] if has_l else None, recv_r[: nr_in * R] if has_r else None)
         rc = lib.ckg_slab_finish(ctx, C.c_void_p(recv_l.data_ptr()), nl_in, C.c_void_p(recv_r.data_ptr()), nr_in,
                                  C.byref(self.out))
+        if new_bounds is not None:  # committed by ckg_slab_finish
+            self.bounds = list(new_bounds)
+            self.bx_lo, self.bx_hi = new_bounds[self.rank], new_bounds[self.rank + 1]
         # errors travel through the all-reduce below so every rank stops together
         self.out.status = rc
         self.n = self.n - out_l - out_r + nl_in + nr_in
@@ -340,7 +388,13 @@ def run_loopback(ranks: List[SlabRank], dt: float):
             return
         kind = type(reqs[0])
         assert all(type(q) is kind for q in reqs), "ranks out of step"
-        if kind is AllReduceMax:
+        if kind is AllReduceSum:
+            acc = reqs[0].buf.clone()
+            for q in reqs[1:]:
+                acc = acc + q.buf
+            for q in reqs:
+                q.buf.copy_(acc)
+        elif kind is AllReduceMax:
             acc = reqs[0].buf.clone()
             for q in reqs[1:]:
                 acc = ranks[0].torch.maximum(acc, q.buf)
@@ -381,7 +435,12 @@ class DistTransport:
     def handle(self, req):
         import torch
         d = self.dist
-        if isinstance(req, AllReduceMax):
+        if isinstance(req, AllReduceSum):
+            buf = self._out(req.buf)
+            d.all_reduce(buf, op=d.ReduceOp.SUM)
+            if buf is not req.buf:
+                req.buf.copy_(buf)
+        elif isinstance(req, AllReduceMax):
             buf = self._out(req.buf)
             d.all_reduce(buf, op=d.ReduceOp.MAX)
             if buf is not req.buf:

@@ -211,3 +211,57 @@ def test_slab_multibody_rank_local_matches_single_domain(world):
     for r in ranks:
         r.close()
     single.close()
+
+
+def test_rebalance_moves_bounds_and_matches_single_domain():
+    """Rebalancing every 3 substeps from a deliberately skewed partition: the
+    bounds move towards balance (one plane per boundary per rebalance), the
+    planes that change hands travel with the migrants, and the ranks still
+    reproduce the single-domain run (global sorted order, state)."""
+    from paper_2412_10399_b200.scene import mass_epsilon
+    from paper_2412_10399_b200.slab import SlabRank, block_x_of
+    cfg = scene("apic", "fixed_corotated")
+    p0 = tag_volumes(perturb(seed_particles(cfg), seed=3, fscale=0.002, vscale=0.05, bscale=0.05, xscale=0.1,
+                             dx=1 / 48))
+    single = Simulation(cfg, particles=p0)
+    D = cfg.resolution // 4 + 2
+    bx = block_x_of(p0, cfg)
+    occupied = np.nonzero(np.bincount(bx, minlength=D))[0]
+    # skewed: rank 0 gets one occupied plane, rank 1 the rest
+    cut = int(occupied[0]) + 1
+    bounds = [0, cut, D]
+    T = np.float64
+    c = np.clip(np.floor(p0["x"].astype(T) * T(48) + T(0.25)).astype(np.int64) >> 2, 0, D - 1)
+    key = (c[:, 0] * D + c[:, 1]) * D + c[:, 2]
+    order = np.argsort(key, kind="stable")
+    ps, pbx = p0[order], c[order, 0]
+    me = mass_epsilon(p0)
+    ranks = []
+    for r in range(2):
+        rk = SlabRank(cfg, r, 2, bounds, ps[(pbx >= bounds[r]) & (pbx < bounds[r + 1])], me)
+        rk.vmax = float(np.max(np.linalg.norm(p0["v"], axis=1)))
+        rk.rebalance_every = 3
+        ranks.append(rk)
+    n0 = [r.n for r in ranks]
+    for step in range(15):
+        dt = single.cfl_dt(1.0)
+        assert abs(ranks[0].cfl_dt(1.0) - dt) <= 1e-9 * dt
+        single.step(dt)
+        run_loopback(ranks, dt)
+        assert ranks[0].bounds == ranks[1].bounds
+        a = single.particles()
+        b = np.concatenate([r.particles() for r in ranks])
+        key_of = dict(zip(a["volume0"].tolist(), _keys(a, cfg).tolist()))
+        ka = np.array([key_of[t] for t in a["volume0"].tolist()])
+        kb = np.array([key_of[t] for t in b["volume0"].tolist()])
+        assert np.array_equal(a["volume0"][np.argsort(ka, kind="stable")], b["volume0"][np.argsort(kb, kind="stable")])
+        ia, ib = np.argsort(a["volume0"]), np.argsort(b["volume0"])
+        for f in ("x", "v", "F"):
+            x = np.asarray(a[f][ia], dtype=np.float64)
+            y = np.asarray(b[f][ib], dtype=np.float64)
+            assert np.max(np.abs(x - y)) <= 1e-10 * max(np.max(np.abs(x)), 1.0), (step, f)
+    assert ranks[0].bounds[1] > cut, "the boundary did not move towards balance"
+    assert abs(ranks[0].n - ranks[1].n) < abs(n0[0] - n0[1])
+    for r in ranks:
+        r.close()
+    single.close()
