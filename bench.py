@@ -568,12 +568,31 @@ def main():
         dom, dom_bytes, dom_ms = "g2p_kernel", g2p_bytes, g2p_avg
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
+    flops = {}
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(dom)
+            tj = json.load(open(tfile))
+            traffic = tj.get(dom)
+            flops = tj.get("fp64_flop_per_launch", {})
         except Exception:
             traffic = None
+    # the FP64 pipe as the second ceiling: ncu's FP64 op count of
+    # the same launch (bench scene only) over the live kernel time, against the
+    # measured DFMA peak (tools/fp64_peak.cu -> profiles/fp64_peak.json)
+    roof64 = None
+    try:
+        peak64 = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["fp64_fma_tflops"]
+        if prec == 8 and cells == 108 and args.scheme == "apic" and args.model == "fixed_corotated" and not fused \
+                and "p2g_kernel" in flops:
+            f_p2g, f_g2p = flops["p2g_kernel"], flops["g2p_kernel"]
+            roof64 = {"bound": "fp64", "unit": "TFLOP/s", "peak": peak64, "peak_kind": "measured (DFMA loop)",
+                      "p2g": f_p2g / (p2g_avg * 1e-3) / 1e12, "g2p": f_g2p / (g2p_avg * 1e-3) / 1e12,
+                      "p2g_frac": f_p2g / (p2g_avg * 1e-3) / 1e12 / peak64,
+                      "g2p_frac": f_g2p / (g2p_avg * 1e-3) / 1e12 / peak64,
+                      "flop_source": flops.get("source")}
+    except Exception:
+        roof64 = None
 
     single = None
     if ws == 1 and prec == 8 and not args.no_single:
@@ -607,6 +626,7 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes": dom_bytes, "avg_ms": dom_ms},
+            "roofline_fp64": roof64,
             "transfer_path": "fused G2P2G kernel (G2P of substep n + P2G of n+1)" if fused else
                              "separate P2G and G2P kernels",
             "p2g_g2p": {"p2g_ms": p2g_avg, "g2p_ms": g2p_avg,
