@@ -220,3 +220,37 @@ def test_c5_bench_scene_float_vs_reference_float():
     assert np.array_equal(a["volume0"], b["volume0"])
     for f in ("x", "v", "F"):
         assert field_rel(a, b, f, floor=1.0 if f != "v" else 0.01) <= 1e-5, f
+
+
+@pytest.mark.parametrize("variant", ["pic", "quadratic"])
+def test_c5_bench_scene_other_transfers_vs_reference(variant):
+    """The bench scene with the PIC transfer (no affine term) and with the
+    quadratic B-spline baseline (27-node single grid) against the reference
+    engine run the same way."""
+    cfg = block_scene(108, scheme="pic") if variant == "pic" else block_scene(108, kernel="quadratic")
+    p = seed_particles(cfg, 8)
+    fields = ("x", "v", "F") if variant == "pic" else ("x", "v", "F", "B")
+    _run_pair(cfg, p, 2, {1: 1e-12, 2: 1e-12}, fields=fields)
+
+
+def test_c2_two_spheres_mls_vs_reference():
+    """MLS (mls_moment / gauss_inverse4 / the force through grad Phi,
+    transfer.hpp:127-150, :335-369) at 1M particles."""
+    obj = dict(C2)
+    obj["scheme"] = "mls"
+    cfg = SceneConfig.from_json(obj)
+    p = seed_particles(cfg, 8)
+    _run_pair(cfg, p, 3, {1: 1e-12, 3: 1e-11})
+
+
+def test_fluid_column_4m_vs_reference():
+    """A J-fluid (weakly compressible, viscous: material.hpp:132-143, the
+    dam-break scenes' model) column of 4,194,304 particles at res 256."""
+    obj = dict(C3)
+    obj["name"] = "fluid_column_4M"
+    obj["materials"] = [{"model": "j_fluid", "density": 1000.0, "bulk": 10.0, "gamma": 7.15, "viscosity": 0.1}]  # configs/dam_break_reduced.json
+    obj["boundaries"] = [{"kind": "slip", "lo": [0, 0, 0], "hi": [1, 0.0625, 1], "normal": [0, 1, 0]}]
+    cfg = SceneConfig.from_json(obj)
+    p = seed_particles(cfg, 8)
+    assert len(p) == 4_194_304
+    _run_pair(cfg, p, 3, {1: 1e-12, 3: 1e-11}, fields=("x", "v", "F", "B", "J"))
