@@ -480,7 +480,9 @@ class DistTransport:
 
     def step(self, rank_obj: SlabRank, dt: float):
         import torch
-        if self.host_staged or not torch.cuda.is_available():
+        import os
+        host_sync = os.environ.get("CKMPM_SLAB_HOST_SYNC", "0") == "1"  # round-1 behaviour, a fallback switch
+        if self.host_staged or host_sync or not torch.cuda.is_available():
             for req in rank_obj.stages(dt):
                 self.handle(req)
                 # the library runs on its own (non-blocking) stream: make the
