@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--strong-cells", type=int, default=232, help="strong-scaling block edge (232 -> 99.9M p)")
     ap.add_argument("--model", default="fixed_corotated", choices=["fixed_corotated", "drucker_prager"],
                     help="block material (drucker_prager: the sand scene of the north star's scaling target)")
+    ap.add_argument("--force-slab", action="store_true",
+                    help="testing: run the x-slab path even at N=1 (one slab, NCCL process group of one)")
     ap.add_argument("--rebalance-every", type=int, default=0,
                     help="N>1: move the slab bounds towards balance every K substeps (0: never)")
     ap.add_argument("--res", type=int, default=512)
@@ -415,7 +417,12 @@ def main():
         run_reference(args)
         return
     ws, rank, local = dist_env()
-    if ws > 1:
+    if ws > 1 or args.force_slab:
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29577")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         run_slab(args, ws, rank, local)
         return
     dist = None

@@ -265,3 +265,21 @@ def test_rebalance_moves_bounds_and_matches_single_domain():
     for r in ranks:
         r.close()
     single.close()
+
+
+def test_bench_slab_path_nccl_single_rank():
+    """The bench's x-slab path over NCCL with every exchange on the library's
+    stream (ExternalStream; a process group of one: the scalar / rebalance
+    all-reduces run through NCCL, the neighbour messages are empty)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MASTER_PORT="29588")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--force-slab", "--cells", "32", "--res", "128",
+                        "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--rebalance-every", "2"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["value"] > 0 and line["n_gpus"] == 1 and line["config"]["particles"] == 32 ** 3 * 8
