@@ -211,7 +211,8 @@ struct Context final : CtxBase {
   uint32_t dcap = 0;
   DetSpill<T>* dspill = nullptr;
   DetBuf<T> detbuf() const {
-    if (!det) return DetBuf<T>{nullptr, 0u, nullptr, 0u};
+    // (the quadratic baseline's P2G keeps its atomic flush)
+    if (!det || quad()) return DetBuf<T>{nullptr, 0u, nullptr, 0u};
     return DetBuf<T>{dtile, dcap, dspill, uint32_t(kDetSpillMax)};
   }
   void set_det_cap(uint32_t c) {
