@@ -127,6 +127,30 @@ BodySpec<T> to_body(const ckref_body& b) {
   return r;
 }
 
+// Resizes the reference's process-wide pool ahead of the Simulation ctor
+// (which resizes it only when the count differs, simulation.hpp:94-99).
+// Workaround for a reference-side race: ThreadPool::set_thread_count
+// (parallel.hpp:30-37) starts new workers with seen = 0 while generation_
+// keeps its old value, so after any earlier parallel loop each new worker
+// wakes at once, calls the cleared job_ (std::bad_function_call, stored in
+// worker_ex_) and decrements pending_; the next for_range then rethrows it.
+// Tests that alternate thread counts in one process hit it.  Here the
+// spurious wake-ups are let to finish, then one no-op loop resets pending_
+// and drains the stored exception.
+inline void prepare_pool(int threads) {
+  int want = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+  if (want < 1) want = 1;
+  ThreadPool& pool = ThreadPool::instance();
+  if (pool.thread_count() == want) return;
+  pool.set_thread_count(want);
+  if (want == 1) return;
+  std::this_thread::sleep_for(std::chrono::milliseconds(50));
+  try {
+    pool.for_range(std::size_t(want), [](std::size_t, std::size_t, int) {});
+  } catch (const std::bad_function_call&) {
+  }
+}
+
 // Materials are taken as given (already finalized by the caller); the
 // config-level validation of the reference still runs in the Simulation ctor.
 template <typename T>
@@ -148,6 +172,7 @@ SimConfig<T> to_config(const ckg_config& c, const ckref_extra* ex) {
   }
   for (int i = 0; i < c.n_materials; ++i) cfg.materials.push_back(to_material<T>(c.materials[i]));
   for (int i = 0; i < c.n_boundaries; ++i) cfg.boundaries.push_back(to_bc<T>(c.boundaries[i]));
+  prepare_pool(cfg.threads);
   return cfg;
 }
 

@@ -4,6 +4,7 @@ the reference's own known-answer values (proj/tests/test_kernel.cpp:37-47,
 :73-79, :130-147)."""
 import ctypes as C
 import os
+import time
 
 import numpy as np
 import pytest
@@ -129,3 +130,20 @@ def test_oracle_errors_match_reference():
     rc2, m2, out = orc.step(1e-4)
     assert rc1 == rc2 == 3 and m1 == m2
     assert "violates the 2-cell domain inset on axis 0" in m1
+
+
+@needs_ref
+def test_reference_pool_resize_between_instances():
+    """Alternating thread counts across reference instances in one process
+    (the at-size GPU tests do): the shim's prepare_pool absorbs the
+    reference pool's spurious wake-ups after a resize, which otherwise
+    surface as std::bad_function_call from the next parallel loop."""
+    cfg = small_scene(res=32, lo=(0.375, 0.3125, 0.375), hi=(0.5, 0.4375, 0.5))
+    p0 = seed_particles(cfg)
+    for threads in (4, 2, 4, 1, 3):
+        ref = bind.Ref(cfg, p0, threads=threads, deterministic=False)
+        time.sleep(0.05)  # let freshly started workers run first
+        for _ in range(2):
+            rc, msg = ref.step(ref.cfl_dt(1.0))
+            assert rc == 0, msg
+        ref.close()
