@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--cpu-cells", type=int, default=None,
                     help="CPU baseline block edge (default: the bench's own --cells, i.e. the same config)")
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--cpu-det-steps", type=int, default=1,
+                    help="CPU baseline: substeps also timed in the reference's deterministic (serial scatter) mode")
     ap.add_argument("--ref-warmup", type=int, default=1, help="reference arm: untimed substeps before timing")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="reference arm: bound on the timed substeps' wall time (N>1 workloads)")
@@ -219,11 +221,25 @@ def cpu_baseline(args, threads):
             raise RuntimeError(msg)
     el = time.perf_counter() - t0
     ref.close()
+    det = None
+    if args.cpu_det_steps > 0:
+        # the reference's other mode (SimConfig::deterministic: serial scatter,
+        # simulation.hpp:326-327), reported beside the default
+        ref = bind.Ref(cfg, p, precision=args.precision, threads=threads, deterministic=True)
+        t0 = time.perf_counter()
+        for _ in range(args.cpu_det_steps):
+            rc, msg = ref.step(dt)
+            if rc:
+                raise RuntimeError(msg)
+        det = {"value": len(p) * args.cpu_det_steps / (time.perf_counter() - t0), "unit": UNIT,
+               "steps": args.cpu_det_steps, "mode": "deterministic (serial scatter)"}
+        ref.close()
     kind = "reference"
     return {"value": len(p) * args.cpu_steps / el, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"C5 block {cpu_cells(args)}^3 cells ({len(p)} p) res {args.res} {args.scheme} "
                       f"FP{8 * args.precision}, {args.cpu_steps} substeps after 1 warm-up, "
-                      f"ckmpm::Simulation<T>::step (atomic P2G), wall clock"}
+                      f"ckmpm::Simulation<T>::step (atomic P2G), wall clock",
+            "deterministic": det}
 
 
 def bench_scene(args, cells):
@@ -632,6 +648,7 @@ def main():
             "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas (weak)",
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "frac_vs_spec_8tbs": achieved / 8000.0,
                          "traffic": traffic, "algorithmic_bytes": dom_bytes, "avg_ms": dom_ms},
             "roofline_fp64": roof64,
             "transfer_path": "fused G2P2G kernel (G2P of substep n + P2G of n+1)" if fused else
