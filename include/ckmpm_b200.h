@@ -299,10 +299,16 @@ int32_t ckg_diagnostics_compute(ckg_ctx* ctx, ckg_diagnostics* out);
  * substep is split into stages and the host moves the exchange buffers
  * (device pointers) between them with NCCL (paper_2412_10399_b200/slab.py):
  *   ckg_slab_bin      key/sort of own particles; footprint flags (D^3 u32) -> core_out
- *   (host: MAX-allreduce core over ranks)
- *   ckg_slab_p2g      global activation from the reduced flags, clear, P2G;
+ *   (host: the flags of the planes shared with each neighbour, MAX-merged)
+ *   ckg_slab_p2g      activation from the merged flags, clear, P2G;
  *                     block counts of planes {bx_lo-1, bx_lo, bx_hi-1, bx_hi}
- *   ckg_slab_halo     op 0 pack a plane, 1 add into it, 2 overwrite it
+ *   ckg_slab_p2g_part the same in two parts: 1 = activation, clear and the
+ *                     P2G of the boundary planes bx_lo, bx_hi-1 (the only
+ *                     ones whose tiles reach the ghost planes; counts as
+ *                     above), 2 = the interior planes' P2G, enqueued while
+ *                     part 1's halo is in flight (part 0 = ckg_slab_p2g)
+ *   ckg_slab_halo     (stream-ordered on ckg_stream, no host synchronisation)
+ *                     op 0 pack a plane, 1 add into it, 2 overwrite it
  *                     (block = 2 grids x 4 values x 64 nodes of T); op 5 / 6
  *                     pack / overwrite the velocities only (2 x 3 x 64 of T
  *                     per block: the broadcast after the grid update);
@@ -329,6 +335,7 @@ int32_t ckg_slab_plane_counts(ckg_ctx* ctx, uint64_t* counts);
 int32_t ckg_slab_rebound(ckg_ctx* ctx, int32_t bx_lo, int32_t bx_hi);
 int32_t ckg_slab_bin(ckg_ctx* ctx, double dt, void* core_out);
 int32_t ckg_slab_p2g(ckg_ctx* ctx, const void* core_in, uint64_t plane_blocks[4]);
+int32_t ckg_slab_p2g_part(ckg_ctx* ctx, const void* core_in, uint64_t plane_blocks[4], int32_t part);
 int32_t ckg_slab_halo(ckg_ctx* ctx, int32_t op, int32_t plane, void* buf);
 int32_t ckg_slab_grid(ckg_ctx* ctx);
 int32_t ckg_slab_g2p(ckg_ctx* ctx, uint64_t counts[2]);

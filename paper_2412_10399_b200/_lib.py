@@ -80,6 +80,8 @@ def _declare(lib: C.CDLL) -> None:
     lib.ckg_slab_bin.restype = i32
     lib.ckg_slab_p2g.argtypes = [vp, vp, P(u64)]
     lib.ckg_slab_p2g.restype = i32
+    lib.ckg_slab_p2g_part.argtypes = [vp, vp, P(u64), i32]
+    lib.ckg_slab_p2g_part.restype = i32
     lib.ckg_slab_halo.argtypes = [vp, i32, i32, vp]
     lib.ckg_slab_halo.restype = i32
     lib.ckg_slab_grid.argtypes = [vp]
@@ -109,7 +111,7 @@ EXPORTED = (
     "ckg_records_wait", "ckg_debug_sort", "ckg_debug_bases",
     "ckg_grid_active_block_count", "ckg_grid_download", "ckg_grid_totals",
     "ckg_diagnostics_compute", "ckg_timer_mark", "ckg_timer_elapsed", "ckg_last_error_message",
-    "ckg_slab_set", "ckg_slab_bin", "ckg_slab_p2g", "ckg_slab_halo", "ckg_slab_grid", "ckg_slab_g2p",
+    "ckg_slab_set", "ckg_slab_bin", "ckg_slab_p2g", "ckg_slab_p2g_part", "ckg_slab_halo", "ckg_slab_grid", "ckg_slab_g2p",
     "ckg_slab_pack", "ckg_slab_finish", "ckg_slab_record_words", "ckg_slab_tile_words", "ckg_stream", "ckg_slab_plane_counts", "ckg_slab_rebound",
 )
 

@@ -111,7 +111,7 @@ struct CtxBase {
   virtual int slab_rebound(int lo, int hi) = 0;
   virtual int slab_plane_counts(uint64_t* counts) = 0;
   virtual int slab_bin(double dt, void* core_out) = 0;
-  virtual int slab_p2g(const void* core_in, uint64_t* plane_blocks) = 0;
+  virtual int slab_p2g(const void* core_in, uint64_t* plane_blocks, int part) = 0;
   virtual int slab_halo(int op, int plane, void* buf) = 0;
   virtual int slab_grid() = 0;
   virtual int slab_g2p(uint64_t* counts) = 0;
@@ -1621,9 +1621,32 @@ struct Context final : CtxBase {
     return CKG_OK;
   }
 
-  int slab_p2g(const void* core_in, uint64_t* plane_blocks) override {
+  template <int S>
+  void enqueue_p2g_range(const StepConst<T>& c, int a, int b) {
+    slab_item_range_kernel<<<1, 1, 0, st>>>(plane_start, a, b, dstat);
+    enqueue_p2g<S>(c, 0);
+  }
+  void enqueue_p2g_range_any(const StepConst<T>& c, int a, int b) {
+    if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g_range<kSchemePic>(c, a, b);
+    else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_p2g_range<kSchemeApic>(c, a, b);
+    else enqueue_p2g_range<kSchemeMls>(c, a, b);
+  }
+
+  // part 0: activation + the whole P2G; 1: activation + the P2G of the two
+  // boundary planes (bx_lo, bx_hi - 1: the only ones whose tiles reach the
+  // ghost planes); 2: the interior planes' P2G (the halo exchange of part 1's
+  // ghost planes can run meanwhile).  Parts 0 and 1 return the block counts
+  // of planes ghostL, ownL, ownR, ghostR.
+  int slab_p2g(const void* core_in, uint64_t* plane_blocks, int part) override {
     CKG_CUDA(cudaSetDevice(device));
     const StepConst<T> c = make_const(slab_dt);
+    if (part == 2) {
+      if (bx_hi - bx_lo > 2) enqueue_p2g_range_any(c, bx_lo + 1, bx_hi - 1);
+      slab_item_range_kernel<<<1, 1, 0, st>>>(plane_start, bx_lo, bx_hi, dstat);  // G2P's range
+      CKG_CUDA(cudaEventRecord(ev[4], st));
+      launches += 3;
+      return CKG_OK;
+    }
     CKG_CUDA(cudaMemcpyAsync(core, core_in, nd * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
     CKG_CUDA(cudaEventRecord(ev[1], st));
     enqueue_activate(0);
@@ -1634,10 +1657,16 @@ struct Context final : CtxBase {
       stress_kernel<T><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(state(cur), perm, c, dstat, 0);
       stress_valid = true;
     }
-    if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, 0);
-    else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_p2g<kSchemeApic>(c, 0);
-    else enqueue_p2g<kSchemeMls>(c, 0);
-    CKG_CUDA(cudaEventRecord(ev[4], st));
+    if (part == 1) {
+      enqueue_p2g_range_any(c, bx_lo, bx_lo + 1);
+      if (bx_hi - 1 > bx_lo) enqueue_p2g_range_any(c, bx_hi - 1, bx_hi);
+      launches += 4;
+    } else {
+      if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, 0);
+      else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_p2g<kSchemeApic>(c, 0);
+      else enqueue_p2g<kSchemeMls>(c, 0);
+      CKG_CUDA(cudaEventRecord(ev[4], st));
+    }
     launches += 12;
     std::vector<uint32_t> ps(uint64_t(D) + 1);
     CKG_CUDA(cudaMemcpyAsync(ps.data(), plane_start, ps.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -1660,12 +1689,12 @@ struct Context final : CtxBase {
       tile_halo_kernel<T><<<148 * 4, 256, 0, st>>>(dtile, dcap, plane_start, bx, op, static_cast<T*>(buf),
                                                    &dstat->overflow);
       launches += 1;
-      CKG_CUDA(cudaStreamSynchronize(st));
       return CKG_OK;
     }
+    // stream-ordered: an exchange enqueued on this stream (ckg_stream) sees
+    // the packed buffer; a host or another stream synchronises first
     halo_kernel<T><<<148 * 4, 256, 0, st>>>(pool, plane_start, bx, op, static_cast<T*>(buf));
     launches += 1;
-    CKG_CUDA(cudaStreamSynchronize(st));
     return CKG_OK;
   }
 
@@ -2128,8 +2157,12 @@ int32_t ckg_slab_bin(ckg_ctx* ctx, double dt, void* core_out) {
   return guard(ctx, "ckg_slab_bin", [&] { return ctx->impl->slab_bin(dt, core_out); });
 }
 int32_t ckg_slab_p2g(ckg_ctx* ctx, const void* core_in, uint64_t plane_blocks[4]) {
-  if (!ctx || !core_in || !plane_blocks) return CKG_ERR_CONFIG;
-  return guard(ctx, "ckg_slab_p2g", [&] { return ctx->impl->slab_p2g(core_in, plane_blocks); });
+  return guard(ctx, "ckg_slab_p2g", [&] { return ctx->impl->slab_p2g(core_in, plane_blocks, 0); });
+}
+
+int32_t ckg_slab_p2g_part(ckg_ctx* ctx, const void* core_in, uint64_t plane_blocks[4], int32_t part) {
+  if (!ctx || part < 0 || part > 2) return CKG_ERR_CONFIG;
+  return guard(ctx, "ckg_slab_p2g_part", [&] { return ctx->impl->slab_p2g(core_in, plane_blocks, part); });
 }
 int32_t ckg_slab_halo(ckg_ctx* ctx, int32_t op, int32_t plane, void* buf) {
   if (!ctx || op < 0 || op > 6 || plane < 0 || plane > 3) return CKG_ERR_CONFIG;

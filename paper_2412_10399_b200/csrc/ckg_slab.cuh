@@ -49,6 +49,15 @@ __global__ void slab_ranges_kernel(const uint32_t* __restrict__ plane_start, int
   st->clear_hi = plane_start[g1];
 }
 
+// Transfer item range [plane_start[a], plane_start[b]) for the next P2G
+// launch (its work counter restarted): the x-slab P2G runs the two boundary
+// planes first, so their halo leaves while the interior planes scatter.
+__global__ void slab_item_range_kernel(const uint32_t* __restrict__ plane_start, int a, int b, DevStatus* st) {
+  st->item_lo = plane_start[a];
+  st->item_hi = plane_start[b];
+  st->work[0] = 0u;
+}
+
 // op 0: dst[...] = pool plane; op 1: pool plane += src; op 2: pool plane = src;
 // op 5 / 6: the same as 0 / 2 for the nodal velocities only (the broadcast
 // after the grid update: 3 of each block's 4 values per grid, 384 of 512

@@ -124,6 +124,15 @@ class Neighbor:
     send_right: Optional[object]
     recv_left: Optional[object]
     recv_right: Optional[object]
+    # True: the transport may leave the transfer in flight (NCCL: on a side
+    # stream after the sends' producers) until the next Join
+    overlap: bool = False
+
+
+@dataclass
+class Join:
+    """The transfers left in flight by overlap Neighbor requests complete
+    before the library's next kernels (NCCL: the library stream waits)."""
 
 
 @dataclass
@@ -254,9 +263,19 @@ class SlabRank:
         if recv_r is not None:
             v = view(rr_span)
             v.copy_(self.torch.maximum(v, recv_r))
+        # P2G: with neighbours, the two boundary planes first (the only ones
+        # whose tiles reach the ghost planes), their halo then travels while
+        # the interior planes scatter
+        split = has_l or has_r
         planes = (C.c_uint64 * 4)()
-        _check(lib, ctx, lib.ckg_slab_p2g(ctx, C.c_void_p(self.core.data_ptr()), planes), "ckg_slab_p2g")
+        _check(lib, ctx, lib.ckg_slab_p2g_part(ctx, C.c_void_p(self.core.data_ptr()), planes, 1 if split else 0),
+               "ckg_slab_p2g_part")
         pb = [int(v) for v in planes]  # blocks of planes ghostL, ownL, ownR, ghostR
+
+        def interior_p2g():
+            if split:
+                _check(lib, ctx, lib.ckg_slab_p2g_part(ctx, None, (C.c_uint64 * 4)(), 2), "ckg_slab_p2g_part")
+
         W = self.block_words
         if self.cfg.deterministic:
             # the boundary planes' P2G tiles -> the neighbours' ghost planes;
@@ -271,7 +290,9 @@ class SlabRank:
                 _check(lib, ctx, lib.ckg_slab_halo(ctx, 3, 2, C.c_void_p(send_r.data_ptr())), "tile pack")
             recv_l = self._buf(pb[0], TW) if has_l else None
             recv_r = self._buf(pb[3], TW) if has_r else None
-            yield Neighbor(send_l, send_r, recv_l, recv_r)
+            yield Neighbor(send_l, send_r, recv_l, recv_r, overlap=True)
+            interior_p2g()
+            yield Join()
             if recv_l is not None:
                 _check(lib, ctx, lib.ckg_slab_halo(ctx, 4, 0, C.c_void_p(recv_l.data_ptr())), "tile set")
             if recv_r is not None:
@@ -286,7 +307,9 @@ class SlabRank:
                 _check(lib, ctx, lib.ckg_slab_halo(ctx, 0, 3, C.c_void_p(send_r.data_ptr())), "halo pack")
             recv_l = self._buf(pb[1], W) if has_l else None
             recv_r = self._buf(pb[2], W) if has_r else None
-            yield Neighbor(send_l, send_r, recv_l, recv_r)
+            yield Neighbor(send_l, send_r, recv_l, recv_r, overlap=True)
+            interior_p2g()  # (its flushes also add into the own boundary planes:
+            yield Join()    # the received halo is added after it, on the same stream)
             if recv_l is not None:
                 _check(lib, ctx, lib.ckg_slab_halo(ctx, 1, 1, C.c_void_p(recv_l.data_ptr())), "halo add")
             if recv_r is not None:
@@ -388,6 +411,11 @@ def run_loopback(ranks: List[SlabRank], dt: float):
             return
         kind = type(reqs[0])
         assert all(type(q) is kind for q in reqs), "ranks out of step"
+        # the library kernels that produced the send buffers run on the
+        # contexts' own streams, the copies below on torch's
+        ranks[0].torch.cuda.synchronize()
+        if kind is Join:
+            continue
         if kind is AllReduceSum:
             acc = reqs[0].buf.clone()
             for q in reqs[1:]:
@@ -428,6 +456,14 @@ class DistTransport:
         # memory (used to run several ranks on one GPU in tests)
         self.host_staged = dist.get_backend() == "gloo" and getattr(device, "type", "cpu") == "cuda"
         self.comm_device = "cpu" if self.host_staged else device
+        self.pending = []  # works of overlap Neighbor requests (until Join)
+        self._side = None
+
+    def _side_stream(self):
+        import torch
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
 
     def _out(self, t):
         return t.cpu() if (self.host_staged and t is not None) else t
@@ -460,6 +496,16 @@ class DistTransport:
                 if rr is not None:
                     ops.append(d.P2POp(d.irecv, rr, self.rank + 1))
             ops = [o for o in ops if o.tensor.numel() > 0]
+            if req.overlap and ops and not self.host_staged and torch.cuda.is_available():
+                # in flight on a side stream (ordered after the packing
+                # kernels) while the library enqueues its next kernels; Join
+                # makes the library stream wait for it
+                cur = torch.cuda.current_stream(self.device)
+                side = self._side_stream()
+                side.wait_stream(cur)
+                with torch.cuda.stream(side):
+                    self.pending.extend(d.batch_isend_irecv(ops))
+                return
             if ops:
                 for w in d.batch_isend_irecv(ops):
                     w.wait()
@@ -467,6 +513,10 @@ class DistTransport:
                 req.recv_left.copy_(rl)
             if rr is not None and rr is not req.recv_right:
                 req.recv_right.copy_(rr)
+        elif isinstance(req, Join):
+            for w in self.pending:
+                w.wait()  # NCCL: the current (library) stream waits, not the host
+            self.pending = []
         elif isinstance(req, Counts):
             t = torch.tensor([req.to_left, req.to_right], dtype=torch.int64, device=self.comm_device)
             allc = [torch.zeros(2, dtype=torch.int64, device=self.comm_device) for _ in range(self.world)]
@@ -484,9 +534,12 @@ class DistTransport:
         host_sync = os.environ.get("CKMPM_SLAB_HOST_SYNC", "0") == "1"  # round-1 behaviour, a fallback switch
         if self.host_staged or host_sync or not torch.cuda.is_available():
             for req in rank_obj.stages(dt):
+                # the library runs on its own (non-blocking) stream: its send
+                # buffers are complete before the host reads them, and the
+                # received data is visible before control returns to it
+                if torch.cuda.is_available():
+                    torch.cuda.synchronize()
                 self.handle(req)
-                # the library runs on its own (non-blocking) stream: make the
-                # received data visible before handing control back to it
                 if torch.cuda.is_available():
                     torch.cuda.synchronize()
             return
