@@ -133,7 +133,12 @@ def full(path, out, traffic=None):
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if traffic:
-        json.dump(tr, open(traffic, "w"), indent=1)
+        try:  # keep the file's other keys (e.g. fp64_flop_per_launch)
+            merged = json.load(open(traffic))
+        except (OSError, ValueError):
+            merged = {}
+        merged.update(tr)
+        json.dump(merged, open(traffic, "w"), indent=1)
         print("traffic:", tr)
 
 
