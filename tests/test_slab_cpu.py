@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from paper_2412_10399_b200.scene import block_scene, seed_particles
-from paper_2412_10399_b200.slab import (AllReduceMax, Counts, DistTransport, Neighbor, Scalars, block_x_of,
+from paper_2412_10399_b200.slab import (AllReduceMax, Counts, DistTransport, Join, Neighbor, Scalars, block_x_of,
                                         partition_planes, split_particles)
 
 
@@ -66,6 +66,14 @@ def _worker(rank, world, port, q):
     tr.handle(Neighbor(sl, sr, rl, rr))
     res["rl"] = None if rl is None else rl.tolist()
     res["rr"] = None if rr is None else rr.tolist()
+    # the same exchange as an overlap request completed by Join (the P2G
+    # halo's protocol: in flight while the interior planes scatter)
+    rl2 = torch.zeros_like(rl) if rl is not None else None
+    rr2 = torch.zeros_like(rr) if rr is not None else None
+    tr.handle(Neighbor(sl, sr, rl2, rr2, overlap=True))
+    tr.handle(Join())
+    res["overlap_same"] = all(a is None and b is None or (a is not None and b is not None and a.tolist() == b.tolist())
+                              for a, b in ((rl, rl2), (rr, rr2)))
     got = [None, None]
     tr.handle(Counts(100 + rank, 200 + rank, got))
     res["counts"] = got
@@ -103,6 +111,7 @@ def test_transport_semantics_gloo(world):
         else:
             assert d["rr"] is None and d["counts"][1] == 0
         assert d["scalars"] == [float(world - 1), -1.0, 0.0]
+        assert d["overlap_same"]
 
 
 C4_SMALL = {"name": "c4_small", "resolution": 64, "scheme": "apic", "gravity": [0, -0.1, 0],
