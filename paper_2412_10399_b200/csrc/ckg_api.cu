@@ -479,10 +479,10 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
     set_two_cta_carveout(p2g_tile_kernel<T, S, true>, smem,
-                         CKG_P2G_CPW * (sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB));
+                         p2g_min_ctas<T>());
     CKG_CUDA(cudaFuncSetAttribute(p2g_tile_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     set_two_cta_carveout(p2g_tile_kernel<T, S>, smem,
-                         CKG_P2G_CPW * (sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB));
+                         p2g_min_ctas<T>());
     CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_tile_kernel<T, S>, kP2GThreads, smem));
     if (cfg.scheme == S) p2g_ctas = std::max(1, per) * nsm;
     g2p_attr(g2p_tile_kernel<T, S, 0, kMFC>);
@@ -494,8 +494,8 @@ struct Context final : CtxBase {
       if (quad() && cfg.scheme == S) {
         const size_t qs = p2g_quad_smem_bytes<T>();
         CKG_CUDA(cudaFuncSetAttribute(p2g_quad_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qs)));
-        set_two_cta_carveout(p2g_quad_kernel<T, S>, qs);
-        CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_quad_kernel<T, S>, kXferThreads, qs));
+        set_two_cta_carveout(p2g_quad_kernel<T, S>, qs, quad_min_ctas<T>());
+        CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_quad_kernel<T, S>, kQThreads, qs));
         p2gq_ctas = std::max(1, per) * nsm;
         g2p_attr(g2p_tile_kernel<T, S, 1>);
         CKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_tile_kernel<T, S, 1>, kG2PThreads,
@@ -750,7 +750,7 @@ struct Context final : CtxBase {
   void enqueue_p2g(const StepConst<T>& c, int step_idx) {
     if (quad()) {
       if constexpr (S != kSchemeMls)
-        p2g_quad_kernel<T, S><<<p2gq_ctas, kXferThreads, p2g_quad_smem_bytes<T>(), st>>>(
+        p2g_quad_kernel<T, S><<<p2gq_ctas, kQThreads, p2g_quad_smem_bytes<T>(), st>>>(
             state(cur), perm, c, dir, active, seg_begin, seg_end, pool, pool_cap, dstat, step_idx);
       return;
     }

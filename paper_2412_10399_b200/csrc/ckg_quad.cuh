@@ -15,13 +15,32 @@ namespace ckg {
 constexpr int kQT = 7;                      // tile nodes per axis
 constexpr int kQTNodes = kQT * kQT * kQT;   // 343
 constexpr int kQTVals = 4 * kQTNodes;       // m, px, py, pz
+// CTA shape: kQWarps warps, each scattering CKG_QUAD_CPW of the 8 classes in
+// turn into its own full 7^3 tile; CKG_QUAD_MINCTAS CTAs per SM.  10M bench
+// (FP64): 8 warps x 2 CTAs (128 registers, 274 B of spills) 2.60 ms; 8 x 1
+// 3.19 ms; 4 warps x 3 CTAs (168 registers) -- see DESIGN §4c.
+#ifndef CKG_QUAD_CPW
+#define CKG_QUAD_CPW 2
+#endif
+#ifndef CKG_QUAD_MINCTAS
+#define CKG_QUAD_MINCTAS 3
+#endif
+#ifndef CKG_QUAD_MINCTAS_F32
+#define CKG_QUAD_MINCTAS_F32 5
+#endif
+template <typename T>
+constexpr int quad_min_ctas() {
+  return sizeof(T) == 4 ? CKG_QUAD_MINCTAS_F32 : CKG_QUAD_MINCTAS;
+}
+constexpr int kQWarps = 8 / CKG_QUAD_CPW;
+constexpr int kQThreads = 32 * kQWarps;
 template <typename T>
 constexpr size_t p2g_quad_smem_bytes() {
-  return size_t(kXferWarps) * kQTVals * sizeof(T);
+  return size_t(kQWarps) * kQTVals * sizeof(T);
 }
 
 template <typename T, int SCHEME>
-__global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
+__global__ void __launch_bounds__(kQThreads, quad_min_ctas<T>())
     p2g_quad_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ active,
                     const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_end,
@@ -34,7 +53,7 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
   __shared__ uint32_t cls_list[kP2GChunk];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   T* wt = tiles + warp * kQTVals;
-  for (int e = tid; e < kXferWarps * kQTVals; e += kXferThreads) tiles[e] = T(0);
+  for (int e = tid; e < kQWarps * kQTVals; e += kQThreads) tiles[e] = T(0);
   const uint32_t na = min(st->item_hi, cap), item0 = st->item_lo;
   const uint32_t lt = lanemask_lt();
   const int D = c.D;
@@ -58,10 +77,10 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
       const uint32_t len = min(uint32_t(kP2GChunk), s1 - cb);
       if (tid < 8) cls_cnt[tid] = 0;
       __syncthreads();
-      uint32_t myq[kP2GChunk / kXferThreads], myslot[kP2GChunk / kXferThreads], mysrc[kP2GChunk / kXferThreads];
+      uint32_t myq[kP2GChunk / kQThreads], myslot[kP2GChunk / kQThreads], mysrc[kP2GChunk / kQThreads];
 #pragma unroll
-      for (int r = 0; r < kP2GChunk / kXferThreads; ++r) {
-        const uint32_t j = tid + r * kXferThreads;
+      for (int r = 0; r < kP2GChunk / kQThreads; ++r) {
+        const uint32_t j = tid + r * kQThreads;
         if (j < len) {
           const uint32_t src = __ldg(perm + cb + j);
           mysrc[r] = src;
@@ -87,12 +106,15 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
       }
       __syncthreads();
 #pragma unroll
-      for (int r = 0; r < kP2GChunk / kXferThreads; ++r) {
-        const uint32_t j = tid + r * kXferThreads;
+      for (int r = 0; r < kP2GChunk / kQThreads; ++r) {
+        const uint32_t j = tid + r * kQThreads;
         if (j < len) cls_list[cls_off[myq[r]] + myslot[r]] = mysrc[r];
       }
       __syncthreads();
-      const uint32_t my_cnt = cls_cnt[warp], my_off = cls_off[warp];
+#pragma unroll 1
+      for (int ci = 0; ci < CKG_QUAD_CPW; ++ci) {
+      const int cl = warp + ci * kQWarps;  // this pass's class
+      const uint32_t my_cnt = cls_cnt[cl], my_off = cls_off[cl];
       for (uint32_t rb = 0; rb < my_cnt; rb += 32) {
         const bool in_round = rb + lane < my_cnt;
         const uint32_t src = in_round ? cls_list[my_off + rb + lane] : 0u;
@@ -231,14 +253,15 @@ __global__ void __launch_bounds__(kXferThreads, CKG_P2G_MINB)
           }
         }
       }
+      }  // classes of this warp
       __syncthreads();
     }
     __syncthreads();
     // ---- flush: sum the warp tiles (common origin 4b - 1), one REDG per value
-    for (int e = tid; e < kQTVals; e += kXferThreads) {
+    for (int e = tid; e < kQTVals; e += kQThreads) {
       T sum = T(0);
 #pragma unroll
-      for (int w = 0; w < kXferWarps; ++w) {
+      for (int w = 0; w < kQWarps; ++w) {
         T* qv = tiles + w * kQTVals + e;
         sum += *qv;
         *qv = T(0);

@@ -59,20 +59,14 @@ constexpr int kXferWarps = kXferThreads / 32;
 #endif
 // +1 grid axes in P2G: 0 re-evaluated with a second sincos per axis, 1 rebuilt
 // from the dual evaluation's scaled sine and gradient factor kept in registers
-// (10M bench, P2G: FP32 0.709 -> 0.699 ms; FP64 1.511 -> 1.525 ms from the
-// extra spills, so FP64 re-evaluates; a shared-memory stash cost FP64 L1:
-// 1.95 ms).
+// (10M bench, P2G: FP32 0.709 -> 0.699 ms; FP64 at 4 CTAs/SM (128 registers)
+// 1.511 -> 1.525 ms from the extra spills, at 3 CTAs/SM (168 registers)
+// 1.299 -> 1.202 ms).
 #ifndef CKG_P2G_CARRY_F64
-#define CKG_P2G_CARRY_F64 0
+#define CKG_P2G_CARRY_F64 1
 #endif
 #ifndef CKG_P2G_CARRY_F32
 #define CKG_P2G_CARRY_F32 1
-#endif
-#ifndef CKG_P2G_MINB
-#define CKG_P2G_MINB 2
-#endif
-#ifndef CKG_P2G_MINB_F32
-#define CKG_P2G_MINB_F32 3
 #endif
 #ifndef CKG_G2P_MINB_F32
 #define CKG_G2P_MINB_F32 4
@@ -212,6 +206,22 @@ __device__ __forceinline__ void tile_add4(T* p, const T (&o)[4], int vs) {
 static_assert(CKG_P2G_CPW == 1 || CKG_P2G_T1FULL, "several classes per warp need the full +1 grid tile");
 constexpr int kP2GWarps = 8 / CKG_P2G_CPW;
 constexpr int kP2GThreads = 32 * kP2GWarps;
+// Resident P2G CTAs (4 warps each) per SM the register budget is compiled
+// for.  10M bench: FP64 3 CTAs = 168 registers, 24 B of spills: 1.20 ms
+// (4 CTAs = 128 registers, 260 B of spills: 1.49 ms; 2 CTAs: 1.42 ms);
+// FP32 5 CTAs = 96 registers: 0.661 ms (6: 0.692, 4: 0.721).  The spills
+// were the cost: at 4 CTAs the 106 KB per SM of spilled state does not fit
+// the L1 left beside the tiles, so every reload went to L2.
+#ifndef CKG_P2G_MINCTAS_F64
+#define CKG_P2G_MINCTAS_F64 3
+#endif
+#ifndef CKG_P2G_MINCTAS_F32
+#define CKG_P2G_MINCTAS_F32 5
+#endif
+template <typename T>
+constexpr int p2g_min_ctas() {
+  return sizeof(T) == 4 ? CKG_P2G_MINCTAS_F32 : CKG_P2G_MINCTAS_F64;
+}
 template <typename T>
 constexpr size_t p2g_smem_bytes() {
   return size_t(kP2GWarps) * P2GTile<T>::kVals * sizeof(T);
@@ -393,9 +403,14 @@ __global__ void __launch_bounds__(kPrepWarps * 32, 4) xfer_prep_kernel(
 //   Z_a(u) = u dx Q_a2 wz_u - A_a2 gz_u
 // (~130 FP64 operations per grid instead of ~200; same sum up to the
 // rounding of the regrouping).  Node offsets are visited in the order
-// (t, u) outer, s inner so each Y/Z pair is formed once.
-#ifndef CKG_P2G_SEPARABLE
-#define CKG_P2G_SEPARABLE 1
+// (t, u) outer, s inner so each Y/Z pair is formed once.  Used for FP32
+// (0.668 -> 0.661 ms); FP64 at 168 registers keeps the direct form (1.219
+// -> 1.202 ms: fewer live values across the node loop, 44 -> 24 B spills).
+#ifndef CKG_P2G_SEPARABLE_F64
+#define CKG_P2G_SEPARABLE_F64 0
+#endif
+#ifndef CKG_P2G_SEPARABLE_F32
+#define CKG_P2G_SEPARABLE_F32 1
 #endif
 // P2G: the two grids' scatters as a rolled loop (half the code: instruction
 // cache) instead of unrolled
@@ -465,7 +480,7 @@ __device__ __forceinline__ void scatter_separable(const Axis<T> (&ax)[3], T m, c
 // DET: deterministic mode (per-block tiles stored for det_gather_kernel);
 // a separate instance so the default kernel carries none of its code.
 template <typename T, int SCHEME, bool DET = false>
-__global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG_P2G_MINB_F32 : CKG_P2G_MINB))
+__global__ void __launch_bounds__(kP2GThreads, p2g_min_ctas<T>())
     p2g_tile_kernel(PState<T> cur, const uint32_t* __restrict__ perm, StepConst<T> c,
                     const int32_t* __restrict__ dir, const uint32_t* __restrict__ rec,
                     const uint32_t* __restrict__ cord, const uint4* __restrict__ ccnt,
@@ -714,7 +729,7 @@ __global__ void __launch_bounds__(kP2GThreads, CKG_P2G_CPW*(sizeof(T) == 4 ? CKG
           // fast path: every lane owns a distinct base cell in this warp, so
           // at a fixed node offset all lanes write distinct nodes
           if (in_tile) {
-            if constexpr (CKG_P2G_SEPARABLE) {
+            if constexpr ((sizeof(T) == 8 ? CKG_P2G_SEPARABLE_F64 : CKG_P2G_SEPARABLE_F32) != 0) {
               scatter_separable<T, SCHEME, L::kSwz>(ax, m, u0, Q, Ap, dx, tb, p0, g, lx, ly, lz, E, VS, tmask);
             } else {
 #pragma unroll
