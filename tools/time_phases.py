@@ -22,7 +22,7 @@ scheme = os.environ.get("SCHEME", "apic")
 kw = {"E": 1e4, "density": 1400.0, "boundary": "separate", "gravity": (0, -2.0, 0)} if model == "drucker_prager" else {}
 cfg = block_scene(cells, model=model, scheme=scheme, kernel=os.environ.get("KERNEL", "compact"), **kw)
 host = seed_particles(cfg, prec)
-sim = Simulation(cfg, precision=prec, particles=host, fused=None if fused else False)
+sim = Simulation(cfg, precision=prec, particles=host, fused=True if fused else False)
 L = lib()
 dt = sim.cfl_dt(1.0)
 out = abi.StepOut()
