@@ -125,6 +125,13 @@ template <typename T>
 struct Context final : CtxBase {
   int device = 0;
   cudaStream_t st = nullptr;
+  // activation (dilate / directory scan / compaction) forked onto st_act after
+  // the key pass, concurrent with the incremental sort on st (joined by
+  // enqueue_activate): it needs only the footprint flags
+  cudaStream_t st_act = nullptr;
+  cudaEvent_t ev_key = nullptr, ev_act = nullptr;
+  bool act_pre = false;
+  bool clear_pre = false;  // the pool clear went with the forked activation
   cudaEvent_t ev[8] = {};  // phase boundaries; ev[7]: before a fused substep's deferred clear
   cudaEvent_t tev[16] = {};
   uint64_t launches = 0;  // kernels enqueued by the current API call
@@ -260,6 +267,9 @@ struct Context final : CtxBase {
     device = c.device;
     CKG_CUDA(cudaSetDevice(device));
     CKG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CKG_CUDA(cudaStreamCreateWithFlags(&st_act, cudaStreamNonBlocking));
+    CKG_CUDA(cudaEventCreateWithFlags(&ev_key, cudaEventDisableTiming));
+    CKG_CUDA(cudaEventCreateWithFlags(&ev_act, cudaEventDisableTiming));
     for (auto& e : ev) CKG_CUDA(cudaEventCreate(&e));
     for (auto& e : tev) CKG_CUDA(cudaEventCreate(&e));
     D = c.resolution / 4 + 2;
@@ -427,6 +437,9 @@ struct Context final : CtxBase {
       if (e) cudaEventDestroy(e);
     for (auto& e : tev)
       if (e) cudaEventDestroy(e);
+    if (ev_key) cudaEventDestroy(ev_key);
+    if (ev_act) cudaEventDestroy(ev_act);
+    if (st_act) cudaStreamDestroy(st_act);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -655,12 +668,17 @@ struct Context final : CtxBase {
   // sorted position i, skeys[i] its key).  With the stored order's sorted
   // keys at hand the sort is incremental (ckg_isort.cuh); one small host
   // read-back of the changed count picks identity / merge / full radix.
-  void enqueue_sort() {
+  void enqueue_sort(bool pre_activate = false, bool pre_clear = false) {
     PState<T> cs = state(cur);
+    if (act_pre) {  // a forked activation never joined (an abandoned substep)
+      CKG_CUDA(cudaStreamWaitEvent(st, ev_act, 0));
+      act_pre = false;
+    }
     (quad() ? key_footprint_kernel<T, 1> : key_footprint_kernel<T, 0>)
         <<<grid_for((n + kKeyPer - 1) / kKeyPer, 256, 1 << 30), 256, 0, st>>>(
         cs, T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko_valid ? ko : nullptr, chg, wcnt, quad() ? nullptr : cls8, dstat);
     launches += 1;
+    if (pre_activate) fork_activate(pre_clear);
     if (ko_valid) {
       CKG_CUDA(cudaMemcpyAsync(hcount, &dstat->nchanged, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
       CKG_CUDA(cudaStreamSynchronize(st));
@@ -729,17 +747,42 @@ struct Context final : CtxBase {
   }
 
   // K3-K6: inset error in sorted order, halo dilation, directory, segments.
+  // The part of the activation that needs only the footprint flags: halo
+  // dilation, directory scan, compaction into the active list.
+  void enqueue_activate_flags(cudaStream_t s) {
+    dilate_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, s>>>(core, flags, D);
+    exclusive_scan(flags, reinterpret_cast<uint32_t*>(dir), nd, scan_partials, s);
+    if (slab)
+      plane_start_kernel<<<(D + 1 + 127) / 128, 128, 0, s>>>(reinterpret_cast<const uint32_t*>(dir), flags, D,
+                                                            plane_start);
+    // (the segment table is reset on st below: the sort may still read it)
+    compact_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, s>>>(core, flags, dir, active, nullptr, nullptr, nd,
+                                                              pool_cap, dstat);
+    if (slab) slab_ranges_kernel<<<1, 1, 0, s>>>(plane_start, D, bx_lo, bx_hi, dstat);
+  }
+  // Fork the flag-only activation (and, with_clear, the pool clear, which
+  // needs only the new active list) after the key pass just enqueued on st.
+  void fork_activate(bool with_clear) {
+    CKG_CUDA(cudaEventRecord(ev_key, st));
+    CKG_CUDA(cudaStreamWaitEvent(st_act, ev_key, 0));
+    enqueue_activate_flags(st_act);
+    if (with_clear) clear_kernel<T><<<148 * 8, 256, 0, st_act>>>(pool, dstat, pool_cap);
+    clear_pre = with_clear;
+    CKG_CUDA(cudaEventRecord(ev_act, st_act));
+    act_pre = true;
+  }
+
   void enqueue_activate(int step_idx, bool want_cord = true) {
     PState<T> cs = state(cur);
+    if (act_pre) {
+      CKG_CUDA(cudaStreamWaitEvent(st, ev_act, 0));
+      act_pre = false;
+    } else {
+      enqueue_activate_flags(st);
+    }
+    CKG_CUDA(cudaMemsetAsync(seg_begin, 0, nd * sizeof(uint32_t), st));
+    CKG_CUDA(cudaMemsetAsync(seg_end, 0, nd * sizeof(uint32_t), st));
     inset_fixup_kernel<T><<<148, 256, 0, st>>>(cs, perm, T(cfg.inv_dx), cfg.resolution, dstat, step_idx);
-    dilate_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(core, flags, D);
-    exclusive_scan(flags, reinterpret_cast<uint32_t*>(dir), nd, scan_partials, st);
-    if (slab)
-      plane_start_kernel<<<(D + 1 + 127) / 128, 128, 0, st>>>(reinterpret_cast<const uint32_t*>(dir), flags, D,
-                                                             plane_start);
-    compact_kernel<<<grid_for(nd, 256, 1 << 30), 256, 0, st>>>(core, flags, dir, active, seg_begin, seg_end, nd,
-                                                               pool_cap, dstat);
-    if (slab) slab_ranges_kernel<<<1, 1, 0, st>>>(plane_start, D, bx_lo, bx_hi, dstat);
     segments_kernel<<<grid_for((n + 3) / 4, 256, 1 << 30), 256, 0, st>>>(skeys, n, seg_begin, seg_end);
     xfer_prep_kernel<T><<<148 * 8, kPrepWarps * 32, 0, st>>>(cs, perm, make_const(0.0), dir, active, seg_begin, seg_end,
                                                  pool_cap, dstat, rec, cord, ccnt,
@@ -811,12 +854,14 @@ struct Context final : CtxBase {
     launches += launches_per_step(stop_after);
     status_reset_kernel<<<1, 32, 0, st>>>(dstat, reset_err ? 1 : 0);
     if (timed) CKG_CUDA(cudaEventRecord(ev[0], st));
-    enqueue_sort();
+    // (deterministic mode: the tile gather writes every node of the active blocks)
+    const bool want_clear = stop_after >= CKG_PHASE_CLEAR && !detbuf().tile;
+    enqueue_sort(stop_after >= CKG_PHASE_ACTIVATE && !slab, want_clear);
     if (timed) CKG_CUDA(cudaEventRecord(ev[1], st));
     if (stop_after >= CKG_PHASE_ACTIVATE) enqueue_activate(step_idx);
     if (timed) CKG_CUDA(cudaEventRecord(ev[2], st));
-    // (deterministic mode: the tile gather writes every node of the active blocks)
-    if (stop_after >= CKG_PHASE_CLEAR && !detbuf().tile) clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
+    if (want_clear && !clear_pre) clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
+    clear_pre = false;
     if (timed) CKG_CUDA(cudaEventRecord(ev[3], st));
     if (stop_after >= CKG_PHASE_P2G) {
       if (!stress_valid) {
@@ -885,7 +930,7 @@ struct Context final : CtxBase {
     launches += 1;
     status_reset_kernel<<<1, 32, 0, st>>>(dstat, 1, need_p2g ? 1 : 0);
     if (timed) CKG_CUDA(cudaEventRecord(ev[0], st));
-    enqueue_sort();
+    enqueue_sort(stop_after >= CKG_PHASE_ACTIVATE && !slab);
     if (timed) CKG_CUDA(cudaEventRecord(ev[1], st));
     if (stop_after >= CKG_PHASE_ACTIVATE) {
       enqueue_activate(0, need_p2g);

@@ -283,8 +283,10 @@ __global__ void __launch_bounds__(256) compact_kernel(uint32_t* __restrict__ cor
     dir[d] = -1;
   }
   core[d] = 0u;
-  seg_begin[d] = 0u;
-  seg_end[d] = 0u;
+  if (seg_begin) {  // (null: the caller resets the segment table itself)
+    seg_begin[d] = 0u;
+    seg_end[d] = 0u;
+  }
   if (d == nd - 1) {
     st->n_active = s + f;
     st->item_lo = st->grid_lo = st->clear_lo = 0u;
