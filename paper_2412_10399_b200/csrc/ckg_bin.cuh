@@ -182,7 +182,10 @@ __device__ __forceinline__ void key_footprint_compact(uint64_t i, bool live, con
 // kKeyPer x 32 consecutive particles with all their position / stored-key
 // loads issued up front (memory-level parallelism: the pass is latency-bound
 // at one particle per thread).
-constexpr int kKeyPer = 2;
+#ifndef CKG_KEY_PER
+#define CKG_KEY_PER 2
+#endif
+constexpr int kKeyPer = CKG_KEY_PER;
 template <typename T, int QUAD>
 __global__ void __launch_bounds__(256) key_footprint_kernel(PState<T> cur, T inv_dx, int res, int D, int quad,
                                                             uint32_t* __restrict__ keys,
