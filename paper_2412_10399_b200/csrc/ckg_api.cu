@@ -1087,6 +1087,10 @@ struct Context final : CtxBase {
       return CKG_OK;
     }
     if (count_steps == 1) return step_one(dt, stop_after, true, out);
+    // several full substeps at one dt with the frame graph in its fixed-dt
+    // mode: no host round trip between substeps (the sort path is chosen on
+    // the device); it stops at a failing substep like the loop below
+    if (stop_after >= CKG_PHASE_G2P && graph_ready()) return graph_steps(dt, count_steps, out);
     // several substeps: one at a time, so a failing substep leaves the state
     // of the last completed one and a pool overflow grows the pool and
     // retries (every substep already waits for its key pass's changed count,
@@ -1102,6 +1106,51 @@ struct Context final : CtxBase {
     }
     out->kernel_launches = total_launches;
     out->substeps_done = done;
+    return rc;
+  }
+
+  // count substeps at fixed dt through the frame graph (graph_ready()).
+  int graph_steps(double dt, int count, ckg_step_out* out) {
+    const int c0 = cur;
+    if (!fexec[c0] || !(fkey[c0] == graph_key())) build_frame_graph(c0);
+    FrameState fs{};
+    fs.fixed_dt = double(T(dt));
+    fs.target = uint32_t(count);
+    fs.max_substeps = uint32_t(count);
+    fs.frame_dt = 1.0;
+    fs.frame_end = 0.0;
+    fs.vmax = 0.0;
+    for (int m = 0; m < kMaxMaterials; ++m) fs.min_j[m] = 1.0;
+    fs.parity = uint32_t(cur);
+    *hframe = fs;
+    CKG_CUDA(cudaMemcpyAsync(dframe, hframe, sizeof(FrameState), cudaMemcpyHostToDevice, st));
+    CKG_CUDA(cudaGraphLaunch(fexec[c0], st));
+    CKG_CUDA(cudaMemcpyAsync(hframe, dframe, sizeof(FrameState), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaMemcpyAsync(hstat, dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    CKG_CUDA(cudaStreamSynchronize(st));
+    const uint32_t done = hframe->substeps;
+    const bool failed = hframe->status == 2;
+    cur = int(hframe->parity);
+    step_count += done;
+    perm = perm_buf;
+    skeys = ko;
+    grid_valid = true;
+    last_active = hstat->n_active;
+    fill_out(out, false, CKG_PHASE_G2P);
+    out->kernel_launches = uint64_t(done + (failed ? 1 : 0)) * graph_kernels;
+    out->substeps_done = done;
+    if (!failed) {
+      out->status = CKG_OK;
+      return CKG_OK;
+    }
+    ko_valid = false;  // the failing substep re-sorted; the stored order did not move
+    if (hstat->overflow) {
+      last_error = "grid block pool capacity exceeded";
+      out->status = CKG_ERR_DEVICE;
+      return CKG_ERR_DEVICE;
+    }
+    const int rc = decode_status(out, CKG_PHASE_G2P);
+    out->status = rc;
     return rc;
   }
 

@@ -28,6 +28,10 @@ struct FrameState {
   unsigned int status;              // 0 running, 1 frame done, 2 device error latched, 3 substep limit
   unsigned int parity;              // state buffer holding the current particles
   unsigned int sort_paths[3];       // substeps per sort path: one-CTA, padded radix, full radix
+  // fixed-dt mode (ckg_step_many through the graph): every substep at
+  // fixed_dt, until `target` substeps are done (no CFL, no frame boundary)
+  double fixed_dt;
+  unsigned int target;
 };
 
 template <typename T>
@@ -70,7 +74,7 @@ template <typename T>
 __global__ void frame_ctl_kernel(FrameState* fs, StepConst<T> c, T* dtp) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const T rem = sub_rn(T(fs->frame_end), T(fs->time));
-  const T dt = device_cfl_dt(*fs, c, rem);
+  const T dt = fs->fixed_dt > 0.0 ? T(fs->fixed_dt) : device_cfl_dt(*fs, c, rem);
   *dtp = dt;
   fs->dt = double(dt);
 }
@@ -99,7 +103,10 @@ __global__ void frame_end_kernel(FrameState* fs, const DevStatus* st, cudaGraphC
     fs->time = double(add_rn(T(fs->time), T(fs->dt)));
     fs->substeps += 1;
     fs->parity ^= 1u;
-    if (fs->substeps > fs->max_substeps) {
+    if (fs->fixed_dt > 0.0) {
+      if (fs->substeps >= fs->target) fs->status = 1;
+      else cont = 1;
+    } else if (fs->substeps > fs->max_substeps) {
       fs->status = 3;
     } else {
       const T rem = sub_rn(T(fs->frame_end), T(fs->time));

@@ -233,6 +233,26 @@ def test_step_many_equals_single_steps():
         assert field_rel(a, b, f, floor=1e-3) <= 1e-12, f
 
 
+def test_step_many_graph_path_equals_single_steps():
+    """After a first substep (stored-order keys and stress cache in place)
+    step_many runs its substeps as one launch of the frame graph in fixed-dt
+    mode; the state equals single steps, odd and even counts."""
+    cfg = small_scene(scheme="apic", res=32)
+    p = seed_particles(cfg)
+    s1 = gpu_sim(cfg, p)
+    s2 = gpu_sim(cfg, p)
+    dt = s1.cfl_dt(1.0)
+    for _ in range(13):
+        s1.step(dt)
+    s2.step(dt)
+    s2.step_many(dt, 5)
+    s2.step_many(dt, 7)
+    assert s2.step_count() == 13
+    a, b = s1.particles(), s2.particles()
+    for f in ("x", "v", "F", "B"):
+        assert field_rel(a, b, f, floor=1e-3) <= 1e-12, f
+
+
 def test_stored_order_tracks_reference_sort():
     """Bodies moving across block boundaries every substep: the device's
     stored particle order (its incremental stable sort, ckg_isort.cuh) must
@@ -313,3 +333,14 @@ def test_step_many_stops_at_failing_substep():
     a, b = s1.particles(), s2.particles()
     for f in ("x", "v", "F", "B"):
         assert field_rel(a, b, f, floor=1e-3) <= 1e-12, f
+    # the same through the graph path (one single step first)
+    s3 = gpu_sim(cfg, p)
+    s3.step(dt)
+    with pytest.raises(OutOfDomainError) as ei:
+        s3.step_many(dt, k_ok + 5)
+    assert s3.step_count() == k_ok
+    c = s3.particles()
+    for f in ("x", "v", "F", "B"):
+        assert field_rel(a, c, f, floor=1e-3) <= 1e-12, f
+    # and stepping on from the restored state works
+    s3.set_particles(s1.particles())
