@@ -241,7 +241,11 @@ int32_t ckg_step(ckg_ctx* ctx, double dt, ckg_step_out* out);
  * the first failing substep, whose error `out` reports, leaving the state after
  * the last completed one (out->substeps_done), like the reference's state
  * after a throwing step() call in a loop.  A pool overflow grows the pool and
- * retries that substep.  `out` may be NULL. */
+ * retries that substep.  Once the stored-order keys and the stress cache
+ * exist (after a first substep) and the pool is dense, the substeps run as
+ * one launch of the frame graph in a fixed-dt mode (no host round trip in
+ * between; same results and the same stop-at-failure contract).  `out` may
+ * be NULL. */
 int32_t ckg_step_many(ckg_ctx* ctx, double dt, int32_t count, ckg_step_out* out);
 /* Simulation::advance_frame() without a callback (simulation.hpp:193-211, :213-215). */
 int32_t ckg_advance_frame(ckg_ctx* ctx, const ckg_frame_in* in, ckg_frame_out* out);
