@@ -45,9 +45,6 @@ constexpr int kXferWarps = kXferThreads / 32;
 #ifndef CKG_G2P_MINB
 #define CKG_G2P_MINB 3
 #endif
-#ifndef CKG_G2P_DUAL
-#define CKG_G2P_DUAL 0
-#endif
 #ifndef CKG_G2P_DUAL_SINCOS
 #define CKG_G2P_DUAL_SINCOS 1  // G2P: one sincos per axis for both grids
 #endif
