@@ -48,9 +48,6 @@ constexpr int kXferWarps = kXferThreads / 32;
 #ifndef CKG_G2P_DUAL_SINCOS
 #define CKG_G2P_DUAL_SINCOS 1  // G2P: one sincos per axis for both grids
 #endif
-#ifndef CKG_P2G_EXP
-#define CKG_P2G_EXP 0  // development experiments only (1: no node ordering, 2: no tile RMW)
-#endif
 // +1 grid axes in P2G: 0 re-evaluated with a second sincos per axis, 1 rebuilt
 // from the dual evaluation's scaled sine and gradient factor kept in registers
 // (10M bench, P2G: FP32 0.709 -> 0.699 ms; FP64 at 4 CTAs/SM (128 registers)
