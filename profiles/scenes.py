@@ -44,6 +44,13 @@ def run(name, frames, steps, frame_dt=None):
     row["step_device_ms"] = dev / steps * 1e3
     row["step_wall_ms"] = wall / steps * 1e3
     row["p_substeps_per_s_device"] = n * steps / dev
+    # the same substeps through step_many (one frame-graph launch, fixed dt)
+    sim.step_many(dt, steps)  # warm-up (graph instantiation)
+    t0 = time.perf_counter()
+    sim.step_many(dt, steps)
+    wall = time.perf_counter() - t0
+    row["step_many_wall_ms"] = wall / steps * 1e3
+    row["p_substeps_per_s_step_many"] = n * steps / wall
     sim.close()
     # frames: device driver vs host loop (same start state, warm-up frame first)
     for mode in ("device", "host"):
