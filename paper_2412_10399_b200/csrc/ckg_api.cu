@@ -241,7 +241,10 @@ struct Context final : CtxBase {
   FrameState* hframe = nullptr;  // pinned
   T* ddt = nullptr;
   uint32_t* dnc = nullptr;
-  cudaStream_t cst[3] = {nullptr, nullptr, nullptr};  // capture streams of the conditional bodies
+  // capture streams: conditional bodies (0..2) and the two substeps'
+  // forked activations (3, 4), with their fork / join events
+  cudaStream_t cst[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t gev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaGraphExec_t fexec[2] = {nullptr, nullptr};
   struct GraphKey {
     uint64_t n = ~0ull, cap = 0;
@@ -395,6 +398,8 @@ struct Context final : CtxBase {
       if (e) cudaGraphExecDestroy(e);
     for (auto& c : cst)
       if (c) cudaStreamDestroy(c);
+    for (auto& e : gev)
+      if (e) cudaEventDestroy(e);
     dfree(dframe);
     dfree(ddt);
     dfree(dnc);
@@ -1090,12 +1095,7 @@ struct Context final : CtxBase {
     // several full substeps at one dt with the frame graph in its fixed-dt
     // mode: no host round trip between substeps (the sort path is chosen on
     // the device); it stops at a failing substep like the loop below
-    // Used where launch latency matters (up to 2M particles: 110k 0.21 ->
-    // 0.16 ms, 1M 0.46 -> 0.42 ms per substep); larger scenes keep the host
-    // loop, whose activation runs concurrently with the sort (the graph's is
-    // serial: 4M sand 1.39 vs 1.45 ms).
-    if (stop_after >= CKG_PHASE_G2P && graph_ready() && n <= (uint64_t(2) << 20))
-      return graph_steps(dt, count_steps, out);
+    if (stop_after >= CKG_PHASE_G2P && graph_ready()) return graph_steps(dt, count_steps, out);
     // several substeps: one at a time, so a failing substep leaves the state
     // of the last completed one and a pool overflow grows the pool and
     // retries (every substep already waits for its key pass's changed count,
@@ -1265,11 +1265,17 @@ struct Context final : CtxBase {
   // One substep of the frame graph, captured on `s` (conditional sort bodies
   // on `s_aux`), reading and writing state buffer `cs` -> cs ^ 1.
   void capture_graph_substep(cudaStream_t s, cudaStream_t s_aux, int cs, cudaGraphConditionalHandle h_loop,
-                             cudaGraphConditionalHandle h_next) {
-    const cudaStream_t saved_st = st;
+                             cudaGraphConditionalHandle h_next, cudaStream_t s_fork, cudaEvent_t e_key,
+                             cudaEvent_t e_act) {
+    const cudaStream_t saved_st = st, saved_fork = st_act;
+    const cudaEvent_t saved_key = ev_key, saved_act = ev_act;
     const int saved_cur = cur;
     st = s;
     cur = cs;
+    // the activation forked off the sort as in the host loop (fork_activate)
+    st_act = s_fork;
+    ev_key = e_key;
+    ev_act = e_act;
     StepConst<T> c = make_const(0.0);
     c.dtp = ddt;
     uint64_t k = 0;
@@ -1280,6 +1286,7 @@ struct Context final : CtxBase {
     (quad() ? key_footprint_kernel<T, 1> : key_footprint_kernel<T, 0>)
         <<<grid_for((n + kKeyPer - 1) / kKeyPer, 256, 1 << 30), 256, 0, st>>>(
         state(cur), T(cfg.inv_dx), cfg.resolution, D, quad(), keys, core, ko, chg, wcnt, quad() ? nullptr : cls8, dstat);
+    fork_activate(true);
     const uint64_t nw = (n + 31) / 32;
     exclusive_scan(wcnt, cpre, nw, scan_partials_n, st);
     compact_changed_kernel<<<grid_for((n + 31) / 32, 256, 1 << 30), 256, 0, st>>>(keys, chg, cpre, n, ck, ci);
@@ -1335,8 +1342,9 @@ struct Context final : CtxBase {
     }
     perm = perm_buf;
     skeys = ko;
-    enqueue_activate(0);
-    clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
+    enqueue_activate(0);  // (joins the forked activation and clear)
+    if (!clear_pre) clear_kernel<T><<<148 * 8, 256, 0, st>>>(pool, dstat, pool_cap);
+    clear_pre = false;
     if (cfg.scheme == CKG_SCHEME_PIC) enqueue_p2g<kSchemePic>(c, 0);
     else if (cfg.scheme == CKG_SCHEME_APIC) enqueue_p2g<kSchemeApic>(c, 0);
     else enqueue_p2g<kSchemeMls>(c, 0);
@@ -1350,6 +1358,9 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaGetLastError());
     st = saved_st;
     cur = saved_cur;
+    st_act = saved_fork;
+    ev_key = saved_key;
+    ev_act = saved_act;
   }
 
   GraphKey graph_key() const {
@@ -1373,6 +1384,7 @@ struct Context final : CtxBase {
       dnc = dalloc<uint32_t>(1);
       CKG_CUDA(cudaMallocHost(&hframe, sizeof(FrameState)));
       for (auto& c : cst) CKG_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+      for (auto& e : gev) CKG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       CKG_CUDA(cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kSmallSort * sizeof(unsigned long long))));
     }
@@ -1397,10 +1409,10 @@ struct Context final : CtxBase {
     CKG_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     cudaGraphConditionalHandle hi;
     CKG_CUDA(cudaGraphConditionalHandleCreate(&hi, capture_graph_of(st), 0, cudaGraphCondAssignDefault));
-    capture_graph_substep(st, cst[0], c0, hw, hi);
+    capture_graph_substep(st, cst[0], c0, hw, hi, cst[3], gev[0], gev[1]);
     cudaGraph_t second = add_conditional(st, hi, cudaGraphCondTypeIf);
     CKG_CUDA(cudaStreamBeginCaptureToGraph(cst[1], second, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    capture_graph_substep(cst[1], cst[2], c0 ^ 1, hw, hw);
+    capture_graph_substep(cst[1], cst[2], c0 ^ 1, hw, hw, cst[4], gev[2], gev[3]);
     cudaGraph_t done;
     CKG_CUDA(cudaStreamEndCapture(cst[1], &done));
     CKG_CUDA(cudaStreamEndCapture(st, &done));
