@@ -346,3 +346,28 @@ def test_step_many_stops_at_failing_substep():
         assert field_rel(a, c, f, floor=1e-3) <= 1e-12, f
     # and stepping on from the restored state works
     s3.set_particles(s1.particles())
+
+
+def test_empty_and_single_particle_states():
+    """Edge cases of the particle count: an empty state steps (no work, the
+    step counter advances as in the reference's loop over zero particles) and
+    a single particle follows the reference engine."""
+    cfg = small_scene(scheme="apic", res=32)
+    p = seed_particles(cfg)
+    sim = gpu_sim(cfg, p)
+    sim.set_particles(p[:0])
+    assert len(sim.particles()) == 0
+    sim.step(1e-4)
+    sim.step_many(1e-4, 3)
+    assert len(sim.particles()) == 0
+    one = tag_volumes(p[len(p) // 2:len(p) // 2 + 1].copy())
+    ref = bind.Ref(cfg, one)
+    sim.set_particles(one)
+    for _ in range(5):
+        dt = ref.cfl_dt(1.0)
+        assert ref.step(dt)[0] == 0
+        sim.step(dt)
+    a, b = sim.particles(), ref.particles()
+    assert len(a) == 1
+    for f in ("x", "v", "F", "B"):
+        assert field_rel(a, b, f, floor=1e-3) <= 1e-12, f
